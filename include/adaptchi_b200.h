@@ -1,0 +1,239 @@
+/*
+ * adaptchi_b200.h — C-ABI of the B200-native two-site DMRG local update.
+ *
+ * This is the drop-in boundary for the hot path of arxiv/paper_2604_03960
+ * ("adaptchi", /root/reference/proj).  Every entry point takes plain pointers
+ * and sizes; no C++ or torch types cross it.  Each function names the
+ * reference interface it replaces (file:line relative to /root/reference).
+ *
+ * Conventions
+ *  - Return value: 0 (ACHI_OK) or one of the ACHI_E_* codes below, one per
+ *    reference exception type (proj/include/adaptchi/errors.hpp:8-59) plus
+ *    CUDA failures.  achi_last_error() returns the message of the last error
+ *    on a context.  The C++ mirror (paper_2604_03960_b200/host) rethrows the
+ *    matching typed exception.
+ *  - Host arrays are caller-owned.  Device buffers are owned by the context or
+ *    by a chain handle.  One context = one device + one CUDA stream; a context
+ *    is used by one host thread at a time ("a DMRG run is
+ *    strictly sequential; multiple runs may execute concurrently").
+ *  - Arithmetic is real FP64.  The reference stores complex128
+ *    (tensor.hpp:14-17); for the XXZ/Heisenberg family with the Neel start all
+ *    state data are real once the MPO's sigma^y channel is written in the real
+ *    gauge (iY, -jy*iY): the dense Hamiltonian is identical.
+ *  - Tensor layouts are the reference's row-major layouts: site tensors
+ *    (left, phys, right) (mps.hpp:28-29), environment blocks (bra, mpo, ket)
+ *    (dmrg.hpp:38-39), MPO tensors (left, phys_out, phys_in, right)
+ *    (models.hpp:25-26), two-site tensor theta (l, s1, s2, r) (dmrg.cpp:94).
+ */
+#ifndef ADAPTCHI_B200_H
+#define ADAPTCHI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes (errors.hpp:8-59) ---- */
+enum {
+  ACHI_OK = 0,
+  ACHI_E_ERROR = 1,                 /* Error */
+  ACHI_E_INVALID_MATRIX = 2,        /* InvalidMatrix */
+  ACHI_E_NUMERICAL_FAILURE = 3,     /* NumericalFailure */
+  ACHI_E_INVALID_RANK = 4,          /* InvalidRank */
+  ACHI_E_EIGEN_NONCONVERGENCE = 5,  /* EigenNonConvergence{best_residual} */
+  ACHI_E_INVALID_BASIS_STATE = 6,   /* InvalidBasisState */
+  ACHI_E_SIZE_GUARD = 7,            /* SizeGuard */
+  ACHI_E_DEGENERATE_SPECTRUM = 8,   /* DegenerateSpectrum */
+  ACHI_E_UNSUPPORTED_MODEL = 9,     /* UnsupportedModel */
+  ACHI_E_INVALID_CONFIG = 10,       /* InvalidConfig */
+  ACHI_E_INTERNAL = 11,             /* InternalConsistency */
+  ACHI_E_CUDA = 20,                 /* CUDA runtime / launch failure */
+  ACHI_E_NO_DEVICE = 21             /* no sm_100 device or extension misuse */
+};
+
+/* ---- model / config (models.hpp:16-21, controller.hpp:17-42, dmrg.hpp:12-22) ---- */
+enum { ACHI_HEISENBERG_XXZ = 0, ACHI_TRANSVERSE_ISING = 1 };
+enum { ACHI_SPIN_HALF = 0, ACHI_PAULI = 1 };
+enum { ACHI_MODE_FIXED = 0, ACHI_MODE_THRESHOLD = 1, ACHI_MODE_DIRECT = 2, ACHI_MODE_PID = 3 };
+enum { ACHI_PREDICT_OFF = 0, ACHI_PREDICT_LINEAR = 1, ACHI_PREDICT_QUADRATIC = 2 };
+enum { ACHI_PID_ADDITIVE = 0, ACHI_PID_MULTIPLICATIVE = 1 };
+enum { ACHI_INIT_AUTOMATIC = 0, ACHI_INIT_NEEL = 1, ACHI_INIT_RANDOM = 2 };
+
+typedef struct achi_model_spec {
+  int32_t family;      /* ACHI_HEISENBERG_XXZ | ACHI_TRANSVERSE_ISING */
+  int32_t n;           /* sites, >= 2 */
+  double jx, jy, jz, h;
+  int32_t convention;  /* ACHI_SPIN_HALF | ACHI_PAULI */
+  int32_t _pad;
+} achi_model_spec;
+
+typedef struct achi_controller_config {
+  int32_t mode;             /* ACHI_MODE_* (default pid) */
+  int32_t predictor_order;  /* ACHI_PREDICT_* (default linear) */
+  double alpha_ema;         /* 0.3 */
+  double gamma_margin;      /* 1.2 */
+  double s_target;          /* -1: resolve to ln(chi_max) - 0.5 */
+  double kp, ki, kd;        /* 2.0, 0.1, 0.5 */
+  double beta_predict;      /* 0.4 */
+  int32_t chi_min;          /* 2 */
+  int32_t chi_max;          /* 64 */
+  int32_t pid_scale;        /* ACHI_PID_* */
+  int32_t _pad;
+  double eps_trunc;         /* 1e-10 */
+} achi_controller_config;
+
+typedef struct achi_dmrg_config {
+  int32_t max_sweeps;       /* 24 */
+  int32_t eig_max_iter;     /* 200 */
+  double eps_conv;          /* 1e-8 */
+  double eig_tol;           /* 1e-10 */
+  int32_t initial_state;    /* ACHI_INIT_* */
+  int32_t _pad;
+  uint64_t seed;            /* 1234 */
+  double noise_floor;       /* 1e-14 */
+  achi_controller_config controller;
+} achi_dmrg_config;
+
+/* BondControllerState (controller.hpp:45-56) */
+typedef struct achi_bond_state {
+  double ema, prev_error, integral;
+  double history[3];
+  int32_t chi, history_len, initialized, _pad;
+} achi_bond_state;
+
+/* ControllerDecision + TraceRow (controller.hpp:77-83,116-120) */
+typedef struct achi_trace_row {
+  int32_t sweep, bond, chi, clamped;
+  int64_t delta_chi;
+  double s_raw, s_ema, s_pred, error, p_term, i_term, d_term;
+} achi_trace_row;
+
+/* Per-visit record: everything needed to attribute a chi-profile divergence
+ * to a threshold margin (north_star parity clause). */
+typedef struct achi_visit_record {
+  int32_t sweep, bond, moving_right, kept;
+  int32_t floor_rank, significant, n_sigma, matvecs;
+  int32_t degenerate_cut, _pad;
+  double energy, entropy, trunc_error;
+  double floor_margin;   /* min relative distance |tail - eps*total|/(eps*total) at the floor decision */
+  double sigma_kept, sigma_next;  /* sigma[kept-1], sigma[kept] (0 when absent), normalised by sigma[0] */
+  double lanczos_residual;
+} achi_visit_record;
+
+/* SweepRecord (dmrg.hpp:26-36); profiles are written to caller arrays of length n-1 */
+typedef struct achi_sweep_record {
+  int32_t sweep_index, max_chi_used;
+  double energy, delta_e_rel, max_trunc_error, wall_time;
+  int64_t parameter_count;
+  double average_chi;
+} achi_sweep_record;
+
+/* DmrgResult scalars (dmrg.hpp:71-80) */
+typedef struct achi_dmrg_result {
+  int32_t n_sweeps, converged, max_chi_used, _pad;
+  double energy, max_monotonicity_violation;
+} achi_dmrg_result;
+
+/* ---- context ---- */
+typedef struct achi_ctx achi_ctx;
+typedef struct achi_chain achi_chain;
+
+int achi_ctx_create(int device, achi_ctx** out);
+int achi_ctx_destroy(achi_ctx* ctx);
+/* copies the last error message (NUL-terminated, truncated to len) */
+int achi_last_error(const achi_ctx* ctx, char* buf, size_t len);
+/* EigenNonConvergence::best_residual of the last error (errors.hpp:302-306) */
+double achi_last_residual(const achi_ctx* ctx);
+/* number of device kernels this context launched so far (evidence counter) */
+int64_t achi_launch_count(const achi_ctx* ctx);
+int achi_synchronize(achi_ctx* ctx);
+
+/* ---- DMRG (dmrg.hpp:40-90, dmrg.cpp:216-282) ---- */
+/* run_dmrg setup: validate, build_mpo (real gauge), Neel product state,
+ * canonicalize(psi,0), Environment::rebuild(psi,mpo,0), controller cold start
+ * (dmrg.cpp:216-250).  Device-resident from here on. */
+int achi_chain_create(achi_ctx* ctx, const achi_model_spec* spec,
+                      const achi_dmrg_config* cfg, achi_chain** out);
+int achi_chain_destroy(achi_chain* chain);
+/* two_site_sweep (dmrg.cpp:175-214).  chi_profile/entropy_profile: n-1 each
+ * (may be NULL).  trace: capacity 2(n-1) rows (may be NULL).  visits:
+ * capacity 2(n-1) (may be NULL). */
+int achi_chain_sweep(achi_chain* chain, int sweep_index, achi_sweep_record* rec,
+                     int32_t* chi_profile, double* entropy_profile,
+                     achi_trace_row* trace, achi_visit_record* visits);
+/* run_dmrg sweep loop + convergence (dmrg.cpp:255-281) on an existing chain.
+ * records: capacity cfg.max_sweeps; profiles: max_sweeps*(n-1); trace and
+ * visits: max_sweeps*2(n-1) (each may be NULL). */
+int achi_chain_run(achi_chain* chain, achi_dmrg_result* result,
+                   achi_sweep_record* records, int32_t* chi_profiles,
+                   double* entropy_profiles, achi_trace_row* trace,
+                   achi_visit_record* visits);
+/* bond dimensions chi_1..chi_{n-1} (MatrixProductState::bond_dims, mps.cpp:24-29) */
+int achi_chain_bond_dims(const achi_chain* chain, int32_t* dims);
+/* copy site tensor k (row-major (l,d,r)) to host; size = l*d*r doubles */
+int achi_chain_get_site(const achi_chain* chain, int k, double* out, size_t capacity);
+/* copy environment block (row-major (bra,mpo,ket)); which = 0 left, 1 right */
+int achi_chain_get_env(const achi_chain* chain, int which, int k, int64_t* shape3,
+                       double* out, size_t capacity);
+/* per-bond controller states (n-1 entries) */
+int achi_chain_get_states(const achi_chain* chain, achi_bond_state* out);
+/* replace bond states (test hook for replaying the reference's states) */
+int achi_chain_set_states(achi_chain* chain, const achi_bond_state* in);
+/* load an MPS (host, row-major sites with the given bond dims) into the chain
+ * and rebuild environments at centre 0 (Environment::rebuild, dmrg.cpp:51-56).
+ * The state must be right-canonical with centre 0. */
+int achi_chain_load_state(achi_chain* chain, const int32_t* bond_dims,
+                          const double* const* sites);
+
+/* ---- local kernels, host buffers (for parity tests and API-level calls) ---- */
+/* apply_effective_hamiltonian (dmrg.cpp:58-71): out(bl,s1',s2',br).
+ * L: (chl, D1, chl) ; W1: (D1, d, d, D2); W2: (D2, d, d, D3); R: (chr, D3, chr);
+ * theta/out: (chl, d, d, chr). */
+int achi_heff_apply(achi_ctx* ctx, int chl, int chr, int d, int D1, int D2, int D3,
+                    const double* L, const double* W1, const double* W2,
+                    const double* R, const double* theta, double* out);
+/* Environment::update_left (dmrg.cpp:26-37): Lnew(b',a',j') from L (chl,Dl,chl),
+ * A (chl,d,chn), W (Dl,d,d,Dr) -> Lnew (chn, Dr, chn) */
+int achi_env_update_left(achi_ctx* ctx, int chl, int chn, int d, int Dl, int Dr,
+                         const double* L, const double* A, const double* W,
+                         double* Lnew);
+/* Environment::update_right (dmrg.cpp:39-49): Rnew(b',a,j) from R (chr,Dr,chr),
+ * B (chn,d,chr), W (Dl,d,d,Dr) -> Rnew (chn, Dl, chn) */
+int achi_env_update_right(achi_ctx* ctx, int chr, int chn, int d, int Dl, int Dr,
+                          const double* R, const double* B, const double* W,
+                          double* Rnew);
+
+/* svd_full (linalg.cpp:67-70) + fix_phases (linalg.cpp:19-35) on the GPU
+ * Jacobi kernel.  a: m x n ROW-major.  r = min(m,n).  Outputs (any may be
+ * NULL): sigma[r] non-increasing; u: m x r row-major; vt: r x n row-major.
+ * sweeps_out: Jacobi sweeps used. */
+int achi_svd(achi_ctx* ctx, int m, int n, const double* a, double* sigma,
+             double* u, double* vt, int* sweeps_out);
+/* Batched SVD of `batch` m x n row-major matrices stored back to back; only
+ * singular values are returned (batch x r).  Device-resident timing hook for
+ * config C2 (bench.cpp:635-668). */
+int achi_svd_batched(achi_ctx* ctx, int batch, int m, int n, const double* a,
+                     double* sigma);
+
+/* Fused bond-select kernel (K7) on a host spectrum: entropy_from_spectrum
+ * (mps.cpp:97-113), rank_for_discarded_weight (controller.cpp:134-148),
+ * kept-rank logic (dmrg.cpp:113-136), controller_update
+ * (controller.cpp:150-190) and truncation_error (mps.cpp:115-122), executed
+ * on the device.  state is updated in place. */
+int achi_bond_select(achi_ctx* ctx, const achi_dmrg_config* cfg, int n_sigma,
+                     const double* sigma, achi_bond_state* state, int sweep,
+                     int bond, achi_trace_row* row, achi_visit_record* visit);
+
+/* eigs_lowest (linalg.cpp:107-178) with a dense symmetric operator (test
+ * hook for the device Lanczos): h is dim x dim row-major. */
+int achi_eigs_lowest_dense(achi_ctx* ctx, int dim, const double* h,
+                           const double* v0, double tol, int max_iter,
+                           double* eigenvalue, double* eigenvector,
+                           int* matvecs, double* residual);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADAPTCHI_B200_H */
