@@ -1,0 +1,234 @@
+"""Python front-end over the C-ABI (include/adaptchi_b200.h).
+
+Names follow the reference API (proj/include/adaptchi/*.hpp): ``run_dmrg``,
+``two_site_sweep`` (Chain.sweep), ``apply_effective_hamiltonian``,
+``Environment.update_left/update_right``, ``svd_full``, ``eigs_lowest``,
+``controller_update``.  Errors are raised as :class:`AchiError` carrying the
+reference exception name (errors.hpp:8-59).  Every call runs on the GPU; there
+is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import abi
+
+
+class AchiError(RuntimeError):
+    def __init__(self, code, msg, residual=None):
+        self.code = code
+        self.name = abi.ERROR_NAMES.get(code, str(code))
+        self.residual = residual
+        super().__init__(f"{self.name}: {msg}")
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _ip(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Context:
+    """One device + one CUDA stream (achi_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = abi.load()
+        self.h = C.c_void_p()
+        rc = self.lib.achi_ctx_create(device, C.byref(self.h))
+        if rc != 0:
+            raise AchiError(rc, f"achi_ctx_create(device={device}) failed")
+
+    def close(self):
+        if self.h:
+            self.lib.achi_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != 0:
+            buf = C.create_string_buffer(1024)
+            self.lib.achi_last_error(self.h, buf, 1024)
+            raise AchiError(rc, buf.value.decode(), self.lib.achi_last_residual(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.achi_launch_count(self.h))
+
+    def synchronize(self):
+        self._check(self.lib.achi_synchronize(self.h))
+
+    # ---- local kernels (host buffers) ----
+    def apply_effective_hamiltonian(self, L, W1, W2, R, theta):
+        """dmrg.cpp:58-71; L (chl,D1,chl), W (D,d,d,D'), R (chr,D3,chr), theta (chl,d,d,chr)."""
+        L, W1, W2, R, theta = map(_f64, (L, W1, W2, R, theta))
+        chl, D1 = L.shape[0], L.shape[1]
+        chr_, D3 = R.shape[0], R.shape[1]
+        d, D2 = W1.shape[1], W1.shape[3]
+        out = np.zeros((chl, d, d, chr_))
+        self._check(self.lib.achi_heff_apply(self.h, chl, chr_, d, D1, D2, D3, _dp(L), _dp(W1),
+                                             _dp(W2), _dp(R), _dp(theta), _dp(out)))
+        return out
+
+    def env_update_left(self, L, A, W):
+        """Environment::update_left (dmrg.cpp:26-37)."""
+        L, A, W = map(_f64, (L, A, W))
+        chl, Dl = L.shape[0], L.shape[1]
+        d, chn, Dr = A.shape[1], A.shape[2], W.shape[3]
+        out = np.zeros((chn, Dr, chn))
+        self._check(self.lib.achi_env_update_left(self.h, chl, chn, d, Dl, Dr, _dp(L), _dp(A),
+                                                  _dp(W), _dp(out)))
+        return out
+
+    def env_update_right(self, R, B, W):
+        """Environment::update_right (dmrg.cpp:39-49)."""
+        R, B, W = map(_f64, (R, B, W))
+        chr_, Dr = R.shape[0], R.shape[1]
+        chn, d, Dl = B.shape[0], B.shape[1], W.shape[0]
+        out = np.zeros((chn, Dl, chn))
+        self._check(self.lib.achi_env_update_right(self.h, chr_, chn, d, Dl, Dr, _dp(R), _dp(B),
+                                                   _dp(W), _dp(out)))
+        return out
+
+    def svd_full(self, a):
+        """linalg.cpp:67-70 on the GPU Jacobi kernel: returns (u, sigma, vt, sweeps)."""
+        a = _f64(a)
+        m, n = a.shape
+        k = min(m, n)
+        s, u, vt = np.zeros(k), np.zeros((m, k)), np.zeros((k, n))
+        sw = C.c_int()
+        self._check(self.lib.achi_svd(self.h, m, n, _dp(a), _dp(s), _dp(u), _dp(vt), C.byref(sw)))
+        return u, s, vt, sw.value
+
+    def svd_batched(self, a):
+        a = _f64(a)
+        b, m, n = a.shape
+        s = np.zeros((b, min(m, n)))
+        self._check(self.lib.achi_svd_batched(self.h, b, m, n, _dp(a), _dp(s)))
+        return s
+
+    def bond_select(self, cfg, sigma, state, sweep=0, bond=0):
+        """Fused entropy / floor-rank / kept / controller_update kernel on one spectrum."""
+        s = _f64(sigma)
+        row, visit = abi.TraceRow(), abi.VisitRecord()
+        self._check(self.lib.achi_bond_select(self.h, C.byref(cfg), len(s), _dp(s), C.byref(state),
+                                              sweep, bond, C.byref(row), C.byref(visit)))
+        return row, visit
+
+    def eigs_lowest_dense(self, h, v0, tol=1e-10, max_iter=200):
+        h, v0 = _f64(h), _f64(v0)
+        dim = h.shape[0]
+        ev, mv, res = C.c_double(), C.c_int(), C.c_double()
+        vec = np.zeros(dim)
+        self._check(self.lib.achi_eigs_lowest_dense(self.h, dim, _dp(h), _dp(v0), C.c_double(tol),
+                                                    max_iter, C.byref(ev), _dp(vec), C.byref(mv),
+                                                    C.byref(res)))
+        return ev.value, vec, mv.value, res.value
+
+    # ---- DMRG ----
+    def chain(self, spec, cfg) -> "Chain":
+        return Chain(self, spec, cfg)
+
+    def run_dmrg(self, spec, cfg):
+        """run_dmrg (dmrg.cpp:216-282) on a device-resident chain."""
+        ch = Chain(self, spec, cfg)
+        try:
+            return ch.run()
+        finally:
+            ch.close()
+
+
+class Chain:
+    """Device-resident MPS + environments + controller states (achi_chain)."""
+
+    def __init__(self, ctx: Context, spec, cfg):
+        self.ctx, self.spec, self.cfg = ctx, spec, cfg
+        self.n = spec.n
+        self.h = C.c_void_p()
+        ctx._check(ctx.lib.achi_chain_create(ctx.h, C.byref(spec), C.byref(cfg), C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            self.ctx.lib.achi_chain_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sweep(self, index):
+        """two_site_sweep (dmrg.cpp:175-214)."""
+        n = self.n
+        rec = abi.SweepRecord()
+        chi = np.zeros(n - 1, np.int32)
+        ent = np.zeros(n - 1)
+        trace = (abi.TraceRow * (2 * (n - 1)))()
+        visits = (abi.VisitRecord * (2 * (n - 1)))()
+        self.ctx._check(self.ctx.lib.achi_chain_sweep(self.h, index, C.byref(rec), _ip(chi), _dp(ent),
+                                                      trace, visits))
+        return dict(record=rec, energy=rec.energy, chi_profile=chi, entropy_profile=ent,
+                    trace=list(trace), visits=list(visits))
+
+    def run(self):
+        n, ms = self.n, self.cfg.max_sweeps
+        res = abi.DmrgResult()
+        recs = (abi.SweepRecord * ms)()
+        chi = np.zeros(ms * (n - 1), np.int32)
+        ent = np.zeros(ms * (n - 1))
+        trace = (abi.TraceRow * (ms * 2 * (n - 1)))()
+        visits = (abi.VisitRecord * (ms * 2 * (n - 1)))()
+        self.ctx._check(self.ctx.lib.achi_chain_run(self.h, C.byref(res), recs, _ip(chi), _dp(ent),
+                                                    trace, visits))
+        ns = res.n_sweeps
+        return dict(
+            energy=res.energy, converged=bool(res.converged), max_chi_used=res.max_chi_used,
+            max_monotonicity_violation=res.max_monotonicity_violation, n_sweeps=ns,
+            records=[recs[i] for i in range(ns)], energies=[recs[i].energy for i in range(ns)],
+            chi_profiles=chi[: ns * (n - 1)].reshape(ns, n - 1).copy(),
+            entropy_profiles=ent[: ns * (n - 1)].reshape(ns, n - 1).copy(),
+            trace=[trace[i] for i in range(ns * 2 * (n - 1))],
+            visits=[visits[i] for i in range(ns * 2 * (n - 1))],
+            bond_dims=self.bond_dims())
+
+    def bond_dims(self):
+        d = np.zeros(self.n - 1, np.int32)
+        self.ctx.lib.achi_chain_bond_dims(self.h, _ip(d))
+        return d
+
+    def site(self, k):
+        dims = [1] + list(self.bond_dims()) + [1]
+        out = np.zeros((dims[k], 2, dims[k + 1]))
+        self.ctx._check(self.ctx.lib.achi_chain_get_site(self.h, k, _dp(out), out.size))
+        return out
+
+    def env(self, which, k):
+        shape = (C.c_int64 * 3)()
+        self.ctx._check(self.ctx.lib.achi_chain_get_env(self.h, which, k, shape, None, 0))
+        out = np.zeros(tuple(shape))
+        self.ctx._check(self.ctx.lib.achi_chain_get_env(self.h, which, k, shape, _dp(out), out.size))
+        return out
+
+    def states(self):
+        arr = (abi.BondState * (self.n - 1))()
+        self.ctx._check(self.ctx.lib.achi_chain_get_states(self.h, arr))
+        return list(arr)
+
+    def load_state(self, sites):
+        dims = np.array([s.shape[2] for s in sites[:-1]], np.int32)
+        flat = [np.ascontiguousarray(s, dtype=np.float64) for s in sites]
+        ptrs = (C.POINTER(C.c_double) * len(flat))(*[_dp(a) for a in flat])
+        self.ctx._check(self.ctx.lib.achi_chain_load_state(self.h, _ip(dims), ptrs))

@@ -1,0 +1,399 @@
+// extern "C" boundary (include/adaptchi_b200.h): typed errors -> int codes.
+#include <cstring>
+#include <memory>
+
+#include "chain.cuh"
+
+using namespace achi;
+
+namespace {
+
+int guard(achi_ctx* ctx, const std::function<void()>& f) {
+  try {
+    f();
+    if (ctx) ctx->c.last_error.clear();
+    return ACHI_OK;
+  } catch (const Error& e) {
+    if (ctx) {
+      ctx->c.last_error = e.what();
+      ctx->c.last_residual = e.residual;
+    }
+    return e.code;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->c.last_error = e.what();
+    return ACHI_E_ERROR;
+  }
+}
+
+__global__ void dense_gemv_kernel(const double* __restrict__ h, int dim, const double* __restrict__ x,
+                                  double* __restrict__ y) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= dim) return;
+  double s = 0.0;
+  for (int j = lane; j < dim; j += 32) s += h[static_cast<long>(row) * dim + j] * x[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) y[row] = s;
+}
+
+HostMpo host_mpo(const double* w, int l, int d, int r) {
+  HostMpo m{l, d, r, std::vector<double>(w, w + static_cast<size_t>(l) * d * d * r)};
+  return m;
+}
+
+void h2d(Ctx& c, double* dst, const double* src, size_t n) {
+  ACHI_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+}
+void d2h(Ctx& c, double* dst, const double* src, size_t n) {
+  ACHI_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+int achi_ctx_create(int device, achi_ctx** out) {
+  return guard(nullptr, [&] {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device)
+      fail(ACHI_E_NO_DEVICE, "no CUDA device");
+    cudaDeviceProp prop;
+    ACHI_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) fail(ACHI_E_NO_DEVICE, "device is not sm_100 (B200)");
+    ACHI_CUDA(cudaSetDevice(device));
+    auto ctx = std::make_unique<achi_ctx>();
+    ctx->c.device = device;
+    ctx->c.num_sms = prop.multiProcessorCount;
+    ACHI_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+    *out = ctx.release();
+  });
+}
+
+int achi_ctx_destroy(achi_ctx* ctx) {
+  if (!ctx) return ACHI_OK;
+  cudaSetDevice(ctx->c.device);
+  cudaStreamSynchronize(ctx->c.stream);
+  cudaStream_t s = ctx->c.stream;
+  delete ctx;
+  cudaStreamDestroy(s);
+  return ACHI_OK;
+}
+
+int achi_last_error(const achi_ctx* ctx, char* buf, size_t len) {
+  if (!ctx || !buf || !len) return ACHI_OK;
+  std::snprintf(buf, len, "%s", ctx->c.last_error.c_str());
+  return ACHI_OK;
+}
+
+double achi_last_residual(const achi_ctx* ctx) { return ctx ? ctx->c.last_residual : 0.0; }
+int64_t achi_launch_count(const achi_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+int achi_synchronize(achi_ctx* ctx) {
+  return guard(ctx, [&] { ctx->c.sync(); });
+}
+
+// ---- chain ----
+int achi_chain_create(achi_ctx* ctx, const achi_model_spec* spec, const achi_dmrg_config* cfg,
+                      achi_chain** out) {
+  return guard(ctx, [&] {
+    auto ch = std::make_unique<achi_chain>();
+    ch->ch.owner = ctx;
+    ch->ch.create(ctx->c, *spec, *cfg);
+    *out = ch.release();
+  });
+}
+
+int achi_chain_destroy(achi_chain* chain) {
+  if (chain) {
+    chain->ch.ctx->sync();
+    delete chain;
+  }
+  return ACHI_OK;
+}
+
+int achi_chain_sweep(achi_chain* chain, int sweep_index, achi_sweep_record* rec,
+                     int32_t* chi_profile, double* entropy_profile, achi_trace_row* trace,
+                     achi_visit_record* visits) {
+  achi_ctx* ctx = chain->ch.owner;
+  return guard(ctx, [&] {
+    chain->ch.sweep(sweep_index, rec, chi_profile, entropy_profile, trace, visits);
+  });
+}
+
+// run_dmrg sweep loop + convergence (dmrg.cpp:255-281)
+int achi_chain_run(achi_chain* chain, achi_dmrg_result* result, achi_sweep_record* records,
+                   int32_t* chi_profiles, double* entropy_profiles, achi_trace_row* trace,
+                   achi_visit_record* visits) {
+  Chain& ch = chain->ch;
+  achi_ctx* ctx = ch.owner;
+  return guard(ctx, [&] {
+    const int nb = ch.n - 1, nv = 2 * (ch.n - 1);
+    achi_dmrg_result res{};
+    double prev = 0;
+    bool have_prev = false;
+    for (int s = 0; s < ch.cfg.max_sweeps; ++s) {
+      achi_sweep_record rec{};
+      ch.sweep(s, &rec, chi_profiles ? chi_profiles + static_cast<long>(s) * nb : nullptr,
+               entropy_profiles ? entropy_profiles + static_cast<long>(s) * nb : nullptr,
+               trace ? trace + static_cast<long>(s) * nv : nullptr,
+               visits ? visits + static_cast<long>(s) * nv : nullptr);
+      res.max_chi_used = std::max(res.max_chi_used, rec.max_chi_used);
+      if (have_prev) {
+        const double delta = rec.energy - prev;
+        rec.delta_e_rel = std::fabs(delta) / std::max(std::fabs(rec.energy), 1e-300);
+        if (delta > 0) res.max_monotonicity_violation = std::max(res.max_monotonicity_violation, delta);
+      } else {
+        rec.delta_e_rel = std::numeric_limits<double>::infinity();
+      }
+      if (records) records[s] = rec;
+      res.n_sweeps = s + 1;
+      if (have_prev && rec.delta_e_rel < ch.cfg.eps_conv) {
+        res.converged = 1;
+        prev = rec.energy;
+        break;
+      }
+      prev = rec.energy;
+      have_prev = true;
+    }
+    res.energy = prev;
+    if (result) *result = res;
+  });
+}
+
+int achi_chain_bond_dims(const achi_chain* chain, int32_t* dims) {
+  for (int k = 1; k < chain->ch.n; ++k) dims[k - 1] = chain->ch.chi[k];
+  return ACHI_OK;
+}
+
+int achi_chain_get_site(const achi_chain* chain, int k, double* out, size_t capacity) {
+  const Chain& ch = chain->ch;
+  achi_ctx* ctx = ch.owner;
+  return guard(ctx, [&] {
+    if (k < 0 || k >= ch.n) fail(ACHI_E_INVALID_RANK, "site index out of range");
+    const int l = ch.chi[k], r = ch.chi[k + 1];
+    if (capacity < static_cast<size_t>(l) * ch.d * r) fail(ACHI_E_SIZE_GUARD, "capacity");
+    download_padded3(*ch.ctx, ch.site[k].p, l, ch.d, r, out);
+  });
+}
+
+int achi_chain_get_env(const achi_chain* chain, int which, int k, int64_t* shape3, double* out,
+                       size_t capacity) {
+  const Chain& ch = chain->ch;
+  achi_ctx* ctx = ch.owner;
+  return guard(ctx, [&] {
+    if (k < 0 || k >= ch.n) fail(ACHI_E_INVALID_RANK, "env index out of range");
+    const int chi = which == 0 ? ch.chi[k] : ch.chi[k + 1];
+    const int D = which == 0 ? ch.mpo[k].l : ch.mpo[k].r;
+    shape3[0] = chi;
+    shape3[1] = D;
+    shape3[2] = chi;
+    if (out) {
+      if (capacity < static_cast<size_t>(chi) * D * chi) fail(ACHI_E_SIZE_GUARD, "capacity");
+      download_padded3(*ch.ctx, which == 0 ? ch.L[k].p : ch.R[k].p, chi, D, chi, out);
+    }
+  });
+}
+
+int achi_chain_get_states(const achi_chain* chain, achi_bond_state* out) {
+  const Chain& ch = chain->ch;
+  achi_ctx* ctx = ch.owner;
+  return guard(ctx, [&] {
+    ACHI_CUDA(cudaMemcpyAsync(out, ch.states.p, sizeof(achi_bond_state) * (ch.n - 1),
+                              cudaMemcpyDeviceToHost, ch.ctx->stream));
+    ch.ctx->sync();
+  });
+}
+
+int achi_chain_set_states(achi_chain* chain, const achi_bond_state* in) {
+  Chain& ch = chain->ch;
+  achi_ctx* ctx = ch.owner;
+  return guard(ctx, [&] {
+    ACHI_CUDA(cudaMemcpyAsync(ch.states.p, in, sizeof(achi_bond_state) * (ch.n - 1),
+                              cudaMemcpyHostToDevice, ch.ctx->stream));
+    ch.ctx->sync();
+  });
+}
+
+int achi_chain_load_state(achi_chain* chain, const int32_t* bond_dims, const double* const* sites) {
+  Chain& ch = chain->ch;
+  achi_ctx* ctx = ch.owner;
+  return guard(ctx, [&] {
+    for (int k = 1; k < ch.n; ++k) {
+      if (bond_dims[k - 1] < 1 || bond_dims[k - 1] > ch.cap[k])
+        fail(ACHI_E_INVALID_RANK, "load_state: bond dimension exceeds capacity");
+      ch.chi[k] = bond_dims[k - 1];
+    }
+    std::vector<std::vector<double>> hs(ch.n);
+    for (int k = 0; k < ch.n; ++k) {
+      const size_t sz = static_cast<size_t>(ch.chi[k]) * ch.d * ch.chi[k + 1];
+      hs[k].assign(sites[k], sites[k] + sz);
+    }
+    ch.upload_sites(hs);
+    ch.rebuild_envs();
+    ch.ctx->sync();
+  });
+}
+
+// ---- local kernels on host buffers ----
+int achi_heff_apply(achi_ctx* ctx, int chl, int chr, int d, int D1, int D2, int D3,
+                    const double* L, const double* W1, const double* W2, const double* R,
+                    const double* theta, double* out) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    const int lp = pad2i(chl), rp = pad2i(chr);
+    DevBuf dL, dR, dT, dO;
+    dL.reserve(static_cast<size_t>(lp) * D1 * lp);
+    dR.reserve(static_cast<size_t>(rp) * D3 * rp);
+    dT.reserve(static_cast<size_t>(lp) * d * d * rp);
+    dO.reserve(static_cast<size_t>(lp) * d * d * rp);
+    upload_padded3(c, L, chl, D1, chl, dL.p);
+    upload_padded3(c, R, chr, D3, chr, dR.p);
+    upload_padded3(c, theta, chl, d * d, chr, dT.p);
+    MixStore ms;
+    auto mix = ms.upload(c, {mix_heff(host_mpo(W1, D1, d, D2), host_mpo(W2, D2, d, D3))});
+    HeffOps op{dL.p, dR.p, lp, rp, d, D1, D3, mix[0]};
+    heff_apply(c, op, dT.p, dO.p);
+    download_padded3(c, dO.p, chl, d * d, chr, out);
+  });
+}
+
+int achi_env_update_left(achi_ctx* ctx, int chl, int chn, int d, int Dl, int Dr, const double* L,
+                         const double* A, const double* W, double* Lnew) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    const int lp = pad2i(chl), np = pad2i(chn);
+    DevBuf dL, dA, dO;
+    dL.reserve(static_cast<size_t>(lp) * Dl * lp);
+    dA.reserve(static_cast<size_t>(lp) * d * np);
+    dO.reserve(static_cast<size_t>(np) * Dr * np);
+    upload_padded3(c, L, chl, Dl, chl, dL.p);
+    upload_padded3(c, A, chl, d, chn, dA.p);
+    MixStore ms;
+    auto mix = ms.upload(c, {mix_env_left(host_mpo(W, Dl, d, Dr))});
+    env_left(c, dL.p, dA.p, lp, np, d, Dl, Dr, mix[0], dO.p);
+    download_padded3(c, dO.p, chn, Dr, chn, Lnew);
+  });
+}
+
+int achi_env_update_right(achi_ctx* ctx, int chr, int chn, int d, int Dl, int Dr, const double* R,
+                          const double* B, const double* W, double* Rnew) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    const int rp = pad2i(chr), np = pad2i(chn);
+    DevBuf dR, dB, dO;
+    dR.reserve(static_cast<size_t>(rp) * Dr * rp);
+    dB.reserve(static_cast<size_t>(np) * d * rp);
+    dO.reserve(static_cast<size_t>(np) * Dl * np);
+    upload_padded3(c, R, chr, Dr, chr, dR.p);
+    upload_padded3(c, B, chn, d, chr, dB.p);
+    MixStore ms;
+    auto mix = ms.upload(c, {mix_env_right(host_mpo(W, Dl, d, Dr))});
+    env_right(c, dR.p, dB.p, rp, np, d, Dl, Dr, mix[0], dO.p);
+    download_padded3(c, dO.p, chn, Dl, chn, Rnew);
+  });
+}
+
+int achi_svd(achi_ctx* ctx, int m, int n, const double* a, double* sigma, double* u, double* vt,
+             int* sweeps_out) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    if (m < 1 || n < 1) fail(ACHI_E_INVALID_MATRIX, "svd: matrix must be at least 1x1");
+    for (long i = 0; i < static_cast<long>(m) * n; ++i)
+      if (!std::isfinite(a[i])) fail(ACHI_E_INVALID_MATRIX, "svd: non-finite entries");
+    DevBuf dA, dS, dU, dV;
+    dA.reserve(static_cast<size_t>(m) * n);
+    h2d(c, dA.p, a, static_cast<size_t>(m) * n);
+    SvdWs ws;
+    const SvdSide side = m <= n ? SvdSide::kRows : SvdSide::kCols;
+    SvdResultDev r = svd_device(c, ws, dA.p, m, n, m, n, side);
+    const int k = r.r_true;
+    svd_phase_signs(c, ws, r, k);
+    dU.reserve(static_cast<size_t>(m) * k);
+    dV.reserve(static_cast<size_t>(k) * n);
+    svd_gather(c, ws, r, k, dU.p, dV.p);
+    if (sigma) d2h(c, sigma, r.sigma, k);
+    if (u) d2h(c, u, dU.p, static_cast<size_t>(m) * k);
+    if (vt) d2h(c, vt, dV.p, static_cast<size_t>(k) * n);
+    c.sync();
+    if (sweeps_out) *sweeps_out = r.sweeps;
+  });
+}
+
+int achi_svd_batched(achi_ctx* ctx, int batch, int m, int n, const double* a, double* sigma) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    const long mn = static_cast<long>(m) * n;
+    DevBuf dA, dS;
+    dA.reserve(static_cast<size_t>(mn) * batch);
+    const int k = std::min(m, n);
+    dS.reserve(static_cast<size_t>(k) * batch);
+    h2d(c, dA.p, a, static_cast<size_t>(mn) * batch);
+    SvdWs ws;
+    svd_device(c, ws, dA.p, m, n, m, n, m <= n ? SvdSide::kRows : SvdSide::kCols, batch, mn, dS.p);
+    d2h(c, sigma, dS.p, static_cast<size_t>(k) * batch);
+    c.sync();
+  });
+}
+
+int achi_bond_select(achi_ctx* ctx, const achi_dmrg_config* cfg, int n_sigma, const double* sigma,
+                     achi_bond_state* state, int sweep, int bond, achi_trace_row* row,
+                     achi_visit_record* visit) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    if (n_sigma < 1) fail(ACHI_E_DEGENERATE_SPECTRUM, "entropy: empty spectrum");
+    DevBuf dS;
+    DevArr<achi_bond_state> dst;
+    DevArr<achi_trace_row> dtr;
+    DevArr<achi_visit_record> dvr;
+    DevArr<BondOut> dbo;
+    dS.reserve(n_sigma);
+    dst.reserve(1);
+    dtr.reserve(1);
+    dvr.reserve(1);
+    dbo.reserve(1);
+    h2d(c, dS.p, sigma, n_sigma);
+    ACHI_CUDA(cudaMemcpyAsync(dst.p, state, sizeof(achi_bond_state), cudaMemcpyHostToDevice, c.stream));
+    ACHI_CUDA(cudaMemsetAsync(dbo.p, 0, sizeof(BondOut), c.stream));
+    bond_select(c, dS.p, n_sigma, *cfg, dst.p, 0, sweep, 0, dtr.p, dvr.p, dbo.p);
+    BondOut bo;
+    ACHI_CUDA(cudaMemcpyAsync(&bo, dbo.p, sizeof(BondOut), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (bo.err == ACHI_E_DEGENERATE_SPECTRUM) fail(bo.err, "entropy: all-zero spectrum");
+    if (bo.err) fail(bo.err, "controller_update: invalid state or config");
+    ACHI_CUDA(cudaMemcpyAsync(state, dst.p, sizeof(achi_bond_state), cudaMemcpyDeviceToHost, c.stream));
+    if (row) ACHI_CUDA(cudaMemcpyAsync(row, dtr.p, sizeof(achi_trace_row), cudaMemcpyDeviceToHost, c.stream));
+    if (visit)
+      ACHI_CUDA(cudaMemcpyAsync(visit, dvr.p, sizeof(achi_visit_record), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (row) row->bond = bond;
+    if (visit) visit->bond = bond;
+  });
+}
+
+int achi_eigs_lowest_dense(achi_ctx* ctx, int dim, const double* h, const double* v0, double tol,
+                           int max_iter, double* eigenvalue, double* eigenvector, int* matvecs,
+                           double* residual) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    DevBuf dH, dV, dO;
+    dH.reserve(static_cast<size_t>(dim) * dim);
+    dV.reserve(dim);
+    dO.reserve(dim);
+    h2d(c, dH.p, h, static_cast<size_t>(dim) * dim);
+    h2d(c, dV.p, v0, dim);
+    LanczosWs ws;
+    EigsOut e = eigs_lowest(
+        c, ws,
+        [&](const double* in, double* out) {
+          dense_gemv_kernel<<<cdiv(dim, 8), 256, 0, c.stream>>>(dH.p, dim, in, out);
+          ACHI_LAUNCHED(c);
+        },
+        dim, dim, dV.p, tol, max_iter, dO.p);
+    d2h(c, eigenvector, dO.p, dim);
+    c.sync();
+    *eigenvalue = e.eigenvalue;
+    *matvecs = e.matvecs;
+    *residual = e.residual;
+  });
+}
+
+}  // extern "C"

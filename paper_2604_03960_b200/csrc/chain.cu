@@ -1,0 +1,297 @@
+// DMRG chain driver on device-resident state (see chain.cuh).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <limits>
+
+#include "chain.cuh"
+
+namespace achi {
+
+void validate_spec(const achi_model_spec& s) {  // models.cpp:11-17
+  if (s.n < 2) fail(ACHI_E_INVALID_CONFIG, "model: n must be >= 2");
+  if (!std::isfinite(s.jx) || !std::isfinite(s.jy) || !std::isfinite(s.jz) || !std::isfinite(s.h))
+    fail(ACHI_E_INVALID_CONFIG, "model: couplings must be finite");
+  if (s.family != ACHI_HEISENBERG_XXZ && s.family != ACHI_TRANSVERSE_ISING)
+    fail(ACHI_E_UNSUPPORTED_MODEL, "build_mpo: unknown model family");
+}
+
+void validate_config(const achi_dmrg_config& g) {  // dmrg.cpp:8-16, controller.cpp:17-33
+  const auto& c = g.controller;
+  if (g.max_sweeps < 1) fail(ACHI_E_INVALID_CONFIG, "dmrg: max_sweeps must be >= 1");
+  if (!(g.eps_conv > 0)) fail(ACHI_E_INVALID_CONFIG, "dmrg: eps_conv must be > 0");
+  if (!(g.eig_tol > 0)) fail(ACHI_E_INVALID_CONFIG, "dmrg: eig_tol must be > 0");
+  if (g.eig_max_iter < 1) fail(ACHI_E_INVALID_CONFIG, "dmrg: eig_max_iter must be >= 1");
+  if (c.chi_min < 1) fail(ACHI_E_INVALID_CONFIG, "controller: chi_min must be >= 1");
+  if (c.chi_min > c.chi_max) fail(ACHI_E_INVALID_CONFIG, "controller: chi_min must be <= chi_max");
+  if (!(c.alpha_ema > 0.0) || c.alpha_ema > 1.0)
+    fail(ACHI_E_INVALID_CONFIG, "controller: alpha_ema must lie in (0, 1]");
+  if (c.gamma_margin < 1.0) fail(ACHI_E_INVALID_CONFIG, "controller: gamma_margin must be >= 1");
+  if (c.beta_predict < 0.0) fail(ACHI_E_INVALID_CONFIG, "controller: beta_predict must be >= 0");
+  if (!(c.eps_trunc >= 0.0)) fail(ACHI_E_INVALID_CONFIG, "controller: eps_trunc must be >= 0");
+  if (c.kp < 0 || c.ki < 0 || c.kd < 0 || !std::isfinite(c.kp) || !std::isfinite(c.ki) ||
+      !std::isfinite(c.kd))
+    fail(ACHI_E_INVALID_CONFIG, "controller: gains must be finite and >= 0");
+}
+
+std::vector<HostMpo> build_mpo_real(const achi_model_spec& s) {
+  validate_spec(s);
+  const double sc = s.convention == ACHI_SPIN_HALF ? 0.5 : 1.0;
+  const double id[4] = {1, 0, 0, 1}, x[4] = {0, sc, sc, 0}, z[4] = {sc, 0, 0, -sc};
+  const double iy[4] = {0, sc, -sc, 0};  // i*sigma^y (scaled): real
+  int w;
+  HostMpo bulk;
+  auto put = [&](int row, int col, const double* op, double f) {
+    for (int so = 0; so < 2; ++so)
+      for (int si = 0; si < 2; ++si)
+        bulk.w[((static_cast<size_t>(row) * 2 + so) * 2 + si) * w + col] = f * op[so * 2 + si];
+  };
+  if (s.family == ACHI_HEISENBERG_XXZ) {
+    w = 5;
+    bulk = HostMpo{w, 2, w, std::vector<double>(static_cast<size_t>(w) * 4 * w, 0.0)};
+    put(0, 0, id, 1.0);
+    put(1, 0, x, 1.0);
+    put(2, 0, iy, 1.0);
+    put(3, 0, z, 1.0);
+    put(4, 0, z, -s.h);
+    put(4, 1, x, s.jx);
+    put(4, 2, iy, -s.jy);
+    put(4, 3, z, s.jz);
+    put(4, 4, id, 1.0);
+  } else {
+    w = 3;
+    bulk = HostMpo{w, 2, w, std::vector<double>(static_cast<size_t>(w) * 4 * w, 0.0)};
+    put(0, 0, id, 1.0);
+    put(1, 0, z, 1.0);
+    put(2, 0, x, -s.h);
+    put(2, 1, z, -s.jz);
+    put(2, 2, id, 1.0);
+  }
+  HostMpo first{1, 2, w, std::vector<double>(4 * w, 0.0)}, last{w, 2, 1, std::vector<double>(4 * w, 0.0)};
+  for (int so = 0; so < 2; ++so)
+    for (int si = 0; si < 2; ++si) {
+      for (int c = 0; c < w; ++c) first.w[(so * 2 + si) * w + c] = bulk.at(w - 1, so, si, c);
+      for (int r = 0; r < w; ++r) last.w[(static_cast<size_t>(r) * 2 + so) * 2 + si] = bulk.at(r, so, si, 0);
+    }
+  std::vector<HostMpo> out;
+  out.push_back(first);
+  for (int i = 1; i < s.n - 1; ++i) out.push_back(bulk);
+  out.push_back(last);
+  return out;
+}
+
+namespace {
+
+// Neel product state (dmrg.cpp:222-232) followed by canonicalize(psi, 0)
+// (mps.cpp:186-210): Householder QR of each 2x1 column, signs as dlarfg.
+std::vector<std::vector<double>> neel_canonical(int n, int d) {
+  std::vector<std::vector<double>> s(n, std::vector<double>(d, 0.0));
+  for (int i = 0; i < n; ++i) s[i][i % 2] = 1.0;
+  for (int i = n - 1; i >= 1; --i) {
+    const double alpha = s[i][0], xnorm = std::fabs(s[i][1]);
+    double beta, q0, q1;
+    if (xnorm == 0.0) {
+      beta = alpha;
+      q0 = 1.0;
+      q1 = 0.0;
+    } else {
+      const double nrm = std::hypot(alpha, xnorm);
+      beta = alpha >= 0 ? -nrm : nrm;
+      const double tau = (beta - alpha) / beta;
+      const double v1 = s[i][1] / (alpha - beta);
+      q0 = 1.0 - tau;
+      q1 = -tau * v1;
+    }
+    s[i][0] = q0;
+    s[i][1] = q1;
+    for (double& v : s[i - 1]) v *= beta;
+  }
+  return s;
+}
+
+__global__ void set_boundary_kernel(double* p) { p[0] = 1.0; }
+
+}  // namespace
+
+void Chain::create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g) {
+  ctx = &c;
+  spec = s;
+  cfg = g;
+  validate_spec(s);
+  validate_config(g);
+  n = s.n;
+  mpo = build_mpo_real(s);
+  int init = g.initial_state;
+  if (init == ACHI_INIT_AUTOMATIC) init = s.family == ACHI_HEISENBERG_XXZ ? ACHI_INIT_NEEL : ACHI_INIT_RANDOM;
+  if (init != ACHI_INIT_NEEL)
+    fail(ACHI_E_UNSUPPORTED_MODEL,
+         "random complex initial state (random_mps, mps.cpp:75-95) is not on the real FP64 path");
+  // mixing matrices
+  std::vector<MixMatrix> all;
+  for (int b = 0; b + 1 < n; ++b) all.push_back(mix_heff(mpo[b], mpo[b + 1]));
+  for (int k = 0; k < n; ++k) all.push_back(mix_env_left(mpo[k]));
+  for (int k = 0; k < n; ++k) all.push_back(mix_env_right(mpo[k]));
+  auto dm = mixes.upload(c, all);
+  mheff.assign(dm.begin(), dm.begin() + (n - 1));
+  mleft.assign(dm.begin() + (n - 1), dm.begin() + (2 * n - 1));
+  mright.assign(dm.begin() + (2 * n - 1), dm.end());
+  // capacities chi_k <= min(chi_max, d^k, d^(n-k))
+  cap.assign(n + 1, 1);
+  chi.assign(n + 1, 1);
+  for (int k = 1; k < n; ++k) {
+    long v = g.controller.chi_max;
+    long gl = 1, gr = 1;
+    for (int i = 0; i < k && gl < v; ++i) gl *= d;
+    for (int i = 0; i < n - k && gr < v; ++i) gr *= d;
+    cap[k] = static_cast<int>(std::min({v, gl, gr}));
+  }
+  site.resize(n);
+  L.resize(n);
+  R.resize(n);
+  size_t max_vec = 0, max_ws = 0;
+  for (int k = 0; k < n; ++k) {
+    const size_t cl = pad2i(cap[k]), cr = pad2i(cap[k + 1]);
+    site[k].reserve(cl * d * cr);
+    L[k].reserve(cl * cl * mpo[k].l);
+    R[k].reserve(cr * cr * mpo[k].r);
+    ACHI_CUDA(cudaMemsetAsync(L[k].p, 0, sizeof(double) * L[k].cap, c.stream));
+    ACHI_CUDA(cudaMemsetAsync(R[k].p, 0, sizeof(double) * R[k].cap, c.stream));
+    if (k + 1 < n) {
+      const size_t c2 = pad2i(cap[k + 2]);
+      max_vec = std::max(max_vec, cl * d * d * c2);
+      max_ws = std::max(max_ws, cl * d * d * c2 * std::max(mpo[k].l, mpo[k + 1].r));
+    }
+    max_ws = std::max(max_ws, cl * cr * d * std::max(mpo[k].l, mpo[k].r));
+  }
+  theta.reserve(max_vec);
+  vec.reserve(max_vec);
+  c.ws_a.reserve(max_ws);
+  c.ws_b.reserve(max_ws);
+  lz.reserve(static_cast<long>(max_vec));
+  states.reserve(n);
+  trace.reserve(2 * (n - 1));
+  visits.reserve(2 * (n - 1));
+  bout.reserve(1);
+  bout_h.reserve(1);
+  vh.assign(2 * (n - 1), VisitHost{0, 0, 0});
+  // boundary environments (dmrg.cpp:18-24)
+  set_boundary_kernel<<<1, 1, 0, c.stream>>>(L[0].p);
+  ACHI_LAUNCHED(c);
+  set_boundary_kernel<<<1, 1, 0, c.stream>>>(R[n - 1].p);
+  ACHI_LAUNCHED(c);
+  // Neel + canonicalize, environments, controller cold start (dmrg.cpp:222-250)
+  upload_sites(neel_canonical(n, d));
+  std::vector<achi_bond_state> st(n - 1);
+  for (auto& b : st) {
+    b = achi_bond_state{};
+    b.chi = g.controller.chi_min;
+    b.ema = 0.0;
+    b.initialized = 1;
+    b.history[0] = 0.0;
+    b.history_len = 1;
+  }
+  ACHI_CUDA(cudaMemcpyAsync(states.p, st.data(), sizeof(achi_bond_state) * (n - 1),
+                            cudaMemcpyHostToDevice, c.stream));
+  rebuild_envs();
+  c.sync();
+}
+
+void Chain::upload_sites(const std::vector<std::vector<double>>& hs) {
+  for (int k = 0; k < n; ++k) {
+    const int l = chi[k], r = chi[k + 1];
+    if (static_cast<long>(hs[k].size()) != static_cast<long>(l) * d * r)
+      fail(ACHI_E_INTERNAL, "upload_sites: size mismatch");
+    upload_padded3(*ctx, hs[k].data(), l, d, r, site[k].p);
+  }
+  ctx->sync();
+}
+
+void Chain::rebuild_envs() {  // Environment::rebuild(psi, mpo, 0), dmrg.cpp:51-56
+  for (int k = n - 2; k >= 0; --k)
+    env_right(*ctx, R[k + 1].p, site[k + 1].p, pad2i(chi[k + 2]), pad2i(chi[k + 1]), d,
+              mpo[k + 1].l, mpo[k + 1].r, mright[k + 1], R[k].p);
+}
+
+// visit_bond (dmrg.cpp:84-171)
+void Chain::visit(int b, bool right, int sweep_index, int slot) {
+  Ctx& c = *ctx;
+  const int chl = chi[b], chm = chi[b + 1], chr = chi[b + 2];
+  const int chlp = pad2i(chl), chmp = pad2i(chm), chrp = pad2i(chr);
+  const long nvec = static_cast<long>(chlp) * d * d * chrp;
+  const long dim = static_cast<long>(chl) * d * d * chr;
+  theta_merge(c, site[b].p, site[b + 1].p, chlp, chmp, chrp, d, theta.p);
+  HeffOps op{L[b].p, R[b + 1].p, chlp, chrp, d, mpo[b].l, mpo[b + 1].r, mheff[b]};
+  EigsOut eig = eigs_lowest(
+      c, lz, [&](const double* in, double* out) { heff_apply(c, op, in, out); }, nvec, dim,
+      theta.p, cfg.eig_tol, cfg.eig_max_iter, vec.p);
+  const SvdSide side = right ? SvdSide::kRows : SvdSide::kCols;
+  SvdResultDev sr = svd_device(c, svd, vec.p, chlp * d, d * chrp, chl * d, d * chr, side);
+  bond_select(c, sr.sigma, sr.r_true, cfg, states.p, b, sweep_index, right ? 1 : 0,
+              trace.p + slot, visits.p + slot, bout.p);
+  ACHI_CUDA(cudaMemcpyAsync(bout_h.p, bout.p, sizeof(BondOut), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  const BondOut bo = *bout_h.p;
+  if (bo.err == ACHI_E_DEGENERATE_SPECTRUM) fail(bo.err, "dmrg: zero two-site block");
+  if (bo.err) fail(bo.err, "controller_update: invalid controller state or config");
+  const int kept = bo.kept;
+  if (!(bo.lam_norm > 0)) fail(ACHI_E_DEGENERATE_SPECTRUM, "dmrg: empty truncation");
+  svd_phase_signs(c, svd, sr, kept);
+  absorb(c, sr, svd.sign.p, kept, bout.p, chl, chr, d, right, site[b].p, site[b + 1].p);
+  chi[b + 1] = kept;
+  const int kp = pad2i(kept);
+  if (right)
+    env_left(c, L[b].p, site[b].p, chlp, kp, d, mpo[b].l, mpo[b].r, mleft[b], L[b + 1].p);
+  else
+    env_right(c, R[b + 1].p, site[b + 1].p, chrp, kp, d, mpo[b + 1].l, mpo[b + 1].r,
+              mright[b + 1], R[b].p);
+  vh[slot] = VisitHost{eig.eigenvalue, eig.residual, eig.matvecs};
+}
+
+// two_site_sweep (dmrg.cpp:175-214)
+void Chain::sweep(int sweep_index, achi_sweep_record* rec, int32_t* chi_profile, double* entropy,
+                  achi_trace_row* trace_out, achi_visit_record* visits_out) {
+  Ctx& c = *ctx;
+  c.sync();
+  auto t0 = std::chrono::steady_clock::now();
+  int slot = 0;
+  for (int b = 0; b <= n - 2; ++b) visit(b, true, sweep_index, slot++);
+  for (int b = n - 2; b >= 0; --b) visit(b, false, sweep_index, slot++);
+  c.sync();
+  auto t1 = std::chrono::steady_clock::now();
+  const int nv = 2 * (n - 1);
+  std::vector<achi_visit_record> vr(nv);
+  ACHI_CUDA(cudaMemcpyAsync(vr.data(), visits.p, sizeof(achi_visit_record) * nv,
+                            cudaMemcpyDeviceToHost, c.stream));
+  if (trace_out)
+    ACHI_CUDA(cudaMemcpyAsync(trace_out, trace.p, sizeof(achi_trace_row) * nv,
+                              cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  achi_sweep_record r{};
+  r.sweep_index = sweep_index;
+  std::vector<double> ent(n - 1, 0.0);
+  for (int i = 0; i < nv; ++i) {
+    vr[i].energy = vh[i].energy;
+    vr[i].matvecs = vh[i].matvecs;
+    vr[i].lanczos_residual = vh[i].residual;
+    r.max_chi_used = std::max(r.max_chi_used, vr[i].kept);
+    r.max_trunc_error = std::max(r.max_trunc_error, vr[i].trunc_error);
+    ent[vr[i].bond] = vr[i].entropy;
+  }
+  r.energy = vh[nv - 1].energy;
+  r.wall_time = std::chrono::duration<double>(t1 - t0).count();
+  long pc = 0;
+  double avg = 0;
+  for (int k = 0; k < n; ++k) pc += static_cast<long>(chi[k]) * d * chi[k + 1];
+  for (int k = 1; k < n; ++k) avg += chi[k];
+  r.parameter_count = pc;
+  r.average_chi = avg / static_cast<double>(n - 1);
+  if (rec) *rec = r;
+  if (chi_profile)
+    for (int k = 1; k < n; ++k) chi_profile[k - 1] = chi[k];
+  if (entropy)
+    for (int k = 0; k < n - 1; ++k) entropy[k] = ent[k];
+  if (visits_out)
+    for (int i = 0; i < nv; ++i) visits_out[i] = vr[i];
+}
+
+}  // namespace achi

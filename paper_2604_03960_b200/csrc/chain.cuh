@@ -1,0 +1,67 @@
+// Device-resident DMRG chain: MPS sites, left/right environment blocks and
+// per-bond controller states live in HBM; the host drives the sweep
+// (two_site_sweep, dmrg.cpp:175-214) and reads back only the kept rank per
+// visit plus Lanczos convergence scalars.
+#pragma once
+
+#include <vector>
+
+#include "bond.cuh"
+#include "contract.cuh"
+#include "lanczos.cuh"
+#include "svd_jacobi.cuh"
+
+struct achi_ctx {
+  achi::Ctx c;
+};
+
+namespace achi {
+
+// models.cpp:49-97 with the sigma^y channel in the real gauge (iY, -jy*iY)
+std::vector<HostMpo> build_mpo_real(const achi_model_spec& spec);
+void validate_spec(const achi_model_spec& spec);
+void validate_config(const achi_dmrg_config& cfg);
+
+struct VisitHost {
+  double energy, residual;
+  int matvecs;
+};
+
+struct Chain {
+  Ctx* ctx = nullptr;
+  achi_ctx* owner = nullptr;
+  achi_model_spec spec{};
+  achi_dmrg_config cfg{};
+  int n = 0, d = 2;
+  std::vector<HostMpo> mpo;
+  MixStore mixes;
+  std::vector<DevMix> mheff, mleft, mright;
+  std::vector<int> chi, cap;  // chi[k]: bond between sites k-1 and k (chi[0] = chi[n] = 1)
+  std::vector<DevBuf> site, L, R;
+  DevArr<achi_bond_state> states;
+  DevArr<achi_trace_row> trace;
+  DevArr<achi_visit_record> visits;
+  DevArr<BondOut> bout;
+  PinnedArr<BondOut> bout_h;
+  DevBuf theta, vec;
+  LanczosWs lz;
+  SvdWs svd;
+  std::vector<VisitHost> vh;
+  // run-level bookkeeping (dmrg.cpp:255-281)
+  double prev_energy = 0;
+  bool have_prev = false;
+
+  void create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g);
+  void rebuild_envs();
+  void upload_sites(const std::vector<std::vector<double>>& host_sites);
+  void visit(int bond, bool moving_right, int sweep, int slot);
+  void sweep(int sweep_index, achi_sweep_record* rec, int32_t* chi_profile, double* entropy,
+             achi_trace_row* trace_out, achi_visit_record* visits_out);
+  long site_size(int k) const { return static_cast<long>(pad2i(chi[k])) * d * pad2i(chi[k + 1]); }
+};
+
+}  // namespace achi
+
+struct achi_chain {
+  achi::Chain ch;
+};

@@ -1,0 +1,139 @@
+// Common infrastructure for the B200-native DMRG hot path: error handling,
+// device buffers, the context (device + stream + launch counter).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/adaptchi_b200.h"
+
+namespace achi {
+
+// Typed error carrying an ACHI_E_* code (one per reference exception type,
+// errors.hpp:8-59).
+struct Error : std::runtime_error {
+  int code;
+  double residual = 0;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& m) { throw Error(code, m); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    std::snprintf(buf, sizeof(buf), "%s failed at %s:%d: %s", what, file, line,
+                  cudaGetErrorString(e));
+    fail(ACHI_E_CUDA, buf);
+  }
+}
+#define ACHI_CUDA(x) ::achi::cuda_check((x), #x, __FILE__, __LINE__)
+#define ACHI_LAUNCHED(ctx)                                            \
+  do {                                                                \
+    ::achi::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
+    ++(ctx).launches;                                                 \
+  } while (0)
+
+// Owning device allocation (capacity-based, grows but never shrinks).
+struct DevBuf {
+  double* p = nullptr;
+  size_t cap = 0;  // elements
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), cap(o.cap) { o.p = nullptr; o.cap = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; cap = o.cap; o.p = nullptr; o.cap = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  // ensure capacity (contents not preserved on growth)
+  double* reserve(size_t n) {
+    if (n > cap) {
+      release();
+      size_t bytes = (n == 0 ? 1 : n) * sizeof(double);
+      ACHI_CUDA(cudaMalloc(&p, bytes));
+      cap = n;
+    }
+    return p;
+  }
+};
+
+template <class T>
+struct DevArr {
+  T* p = nullptr;
+  size_t cap = 0;
+  DevArr() = default;
+  DevArr(const DevArr&) = delete;
+  DevArr& operator=(const DevArr&) = delete;
+  ~DevArr() { if (p) cudaFree(p); }
+  T* reserve(size_t n) {
+    if (n > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      ACHI_CUDA(cudaMalloc(&p, (n == 0 ? 1 : n) * sizeof(T)));
+      cap = n;
+    }
+    return p;
+  }
+};
+
+// Pinned host scratch for small device->host status reads.
+template <class T>
+struct PinnedArr {
+  T* p = nullptr;
+  size_t cap = 0;
+  ~PinnedArr() { if (p) cudaFreeHost(p); }
+  T* reserve(size_t n) {
+    if (n > cap) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      ACHI_CUDA(cudaMallocHost(&p, (n == 0 ? 1 : n) * sizeof(T)));
+      cap = n;
+    }
+    return p;
+  }
+};
+
+// Lanczos step status written by the device (read by the host driver loop).
+struct LanczosStatus {
+  double theta;      // lowest Ritz value of the current tridiagonal
+  double res_bound;  // beta_j * |s_{k-1}|
+  double bnorm;      // ||w|| after reorthogonalisation
+  double alpha;      // q_j . H q_j
+  double ev;         // Rayleigh quotient of the Ritz vector (after explicit check)
+  double res;        // ||H r - ev r||
+  double aux;
+  int32_t flags, pad;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  int num_sms = 148;
+  std::string last_error;
+  double last_residual = 0;
+  // scratch
+  DevBuf ws_a, ws_b, ws_c, ws_split;  // GEMM / contraction intermediates
+  DevBuf red;                          // reduction partials
+  DevBuf small;                        // small device scalars (h coefficients, s vector, ...)
+  PinnedArr<double> host_small;
+  PinnedArr<LanczosStatus> status;
+  void sync() { ACHI_CUDA(cudaStreamSynchronize(stream)); }
+};
+
+inline size_t pad2(size_t x) { return x + (x & 1); }
+inline int pad2i(int x) { return x + (x & 1); }
+inline int cdiv(long a, long b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace achi

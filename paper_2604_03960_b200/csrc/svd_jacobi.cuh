@@ -1,0 +1,56 @@
+// Blocked one-sided Jacobi SVD (replaces reference_svd = Eigen BDCSVD +
+// fix_phases, linalg.cpp:19-48, on the DMRG path svd_full at dmrg.cpp:117).
+//
+// The working matrix G (mg x ng, column-major) has its columns orthogonalised
+// by cyclic block-pair rotations: columns are grouped in blocks of 16; each
+// round pairs blocks by the circle method; one CTA per pair forms the 32x32
+// Gram matrix with DMMA, diagonalises it by two-sided Jacobi in shared memory
+// and applies the accumulated rotation to G and to V (ng x ng) with DMMA.
+// After convergence sigma_c = ||G[:,c]||, columns are sorted non-increasing
+// and the phase convention of fix_phases is applied to the kept vectors.
+#pragma once
+
+#include "common.cuh"
+
+namespace achi {
+
+struct SvdWs {
+  DevBuf G, V, sig, sorted;
+  DevArr<int> perm;
+  DevArr<double> sign;
+  DevArr<unsigned long long> conv;
+  PinnedArr<unsigned long long> conv_host;
+};
+
+// Orientation: kRows -> columns of G are the rows of theta (G = theta^T, V
+// accumulates the left singular vectors U); kCols -> columns of G are the
+// columns of theta (G = theta, V accumulates the right singular vectors).
+enum class SvdSide { kRows = 0, kCols = 1 };
+
+struct SvdResultDev {
+  SvdSide side;
+  int m, n;          // padded rows/cols of theta
+  int m_true, n_true;
+  int ng, mg;        // working matrix columns/rows (ng padded to a multiple of 32)
+  int r_true;        // min(m_true, n_true)
+  int sweeps;
+  const double* G;   // mg x ng col-major (ld = mg)
+  const double* V;   // ng x ng col-major (ld = ng)
+  const double* sigma;  // sorted, r_true entries valid (device)
+  const int* perm;      // perm[k] = working column of the k-th singular value
+};
+
+// SVD of theta (m x n row-major, ld = n, padded; true dims m_true x n_true).
+// Batched over `batch` matrices at stride `bstride` (sigma only for batch > 1).
+SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, int m_true,
+                        int n_true, SvdSide side, int batch = 1, long bstride = 0,
+                        double* sigma_out = nullptr);
+
+// fix_phases signs for the first `kept` vectors on the accurate side (U for
+// kRows, computed from G for kCols): writes ws.sign[0..kept).
+void svd_phase_signs(Ctx& ctx, SvdWs& ws, const SvdResultDev& r, int kept);
+
+// Gather thin factors to device row-major buffers: U (m_true x r) and VT (r x n_true).
+void svd_gather(Ctx& ctx, SvdWs& ws, const SvdResultDev& r, int k, double* U, double* VT);
+
+}  // namespace achi

@@ -1,0 +1,291 @@
+"""GPU parity: every CUDA kernel of the hot path against the CPU oracle.
+
+All calls go through the C-ABI (libadaptchi_b200.so).  Tolerances are written
+in each test: bit-exact for integer decisions (kept rank, floor rank, chi
+profiles), FP64 rounding-level for contractions, and the north_star's
+1e-10 relative energy / 1e-11 relative (to sigma_1) singular values.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2604_03960_b200 import abi
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2604_03960_b200.api import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def rand_env(rng, chi, D):
+    e = rng.standard_normal((chi, D, chi))
+    return e
+
+
+# ---------------- K1: effective Hamiltonian ----------------
+
+@pytest.mark.parametrize("chl,chr_", [(1, 1), (1, 2), (3, 5), (8, 8), (17, 13), (64, 64), (130, 96)])
+def test_heff_matches_oracle(ctx, oracle, chl, chr_):
+    rng = np.random.default_rng(chl * 1000 + chr_)
+    w = oracle.build_mpo(abi.model_spec(6, jz=1.3, h=0.4))
+    W1, W2 = w[2], w[3]
+    L, R = rand_env(rng, chl, 5), rand_env(rng, chr_, 5)
+    th = rng.standard_normal((chl, 2, 2, chr_))
+    got = ctx.apply_effective_hamiltonian(L, W1, W2, R, th)
+    ref = oracle.heff_apply(L, W1, W2, R, th)
+    scale = np.abs(ref).max()
+    assert np.abs(got - ref).max() <= 1e-13 * scale * max(1, math.sqrt(chl * chr_))
+
+
+def test_heff_boundary_and_dense(ctx, oracle):  # test_dmrg.cpp:64-82
+    spec = abi.model_spec(2, convention=abi.SPIN_HALF)
+    w = oracle.build_mpo(spec)
+    from tests.test_oracle_golden import dense_from_mpo
+    h = dense_from_mpo(w)
+    one = np.ones((1, 1, 1))
+    th = np.random.default_rng(2).standard_normal((1, 2, 2, 1))
+    out = ctx.apply_effective_hamiltonian(one, w[0], w[1], one, th)
+    assert np.abs(out.ravel() - h @ th.ravel()).max() <= 1e-12
+
+
+def test_heff_linear(ctx, oracle):  # test_dmrg.cpp:84-109
+    rng = np.random.default_rng(6)
+    w = oracle.build_mpo(abi.model_spec(6))
+    L, R = rand_env(rng, 6, 5), rand_env(rng, 6, 5)
+    t1, t2 = rng.standard_normal((2, 6, 2, 2, 6))
+    a, b = 1.3, -0.2
+    hc = ctx.apply_effective_hamiltonian(L, w[2], w[3], R, a * t1 + b * t2)
+    ha = ctx.apply_effective_hamiltonian(L, w[2], w[3], R, t1)
+    hb = ctx.apply_effective_hamiltonian(L, w[2], w[3], R, t2)
+    assert np.abs(hc - (a * ha + b * hb)).max() <= 1e-10
+
+
+@pytest.mark.parametrize("chi", [256, 300])
+def test_heff_large_vs_einsum(ctx, oracle, chi):
+    """Large shapes exercise the 128x128 tile config and split-K."""
+    rng = np.random.default_rng(chi)
+    w = oracle.build_mpo(abi.model_spec(6))
+    L, R = rand_env(rng, chi, 5), rand_env(rng, chi, 5)
+    th = rng.standard_normal((chi, 2, 2, chi))
+    got = ctx.apply_effective_hamiltonian(L, w[2], w[3], R, th)
+    ref = np.einsum("bal,lstr,aSsc,cTte,Rer->bSTR", L, th, w[2], w[3], R, optimize=True)
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+# ---------------- K2/K3: environments ----------------
+
+@pytest.mark.parametrize("chl,chn", [(1, 2), (2, 4), (5, 7), (33, 64), (128, 200)])
+def test_env_updates_match_oracle(ctx, oracle, chl, chn):
+    rng = np.random.default_rng(chl + 7 * chn)
+    w = oracle.build_mpo(abi.model_spec(6, jz=0.7, h=0.3))
+    for W in (w[0], w[2], w[5]):
+        Dl, Dr = W.shape[0], W.shape[3]
+        L = rand_env(rng, chl, Dl)
+        A = rng.standard_normal((chl, 2, chn))
+        got = ctx.env_update_left(L, A, W)
+        ref = oracle.env_update_left(L, A, W)
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+        R = rand_env(rng, chl, Dr)
+        B = rng.standard_normal((chn, 2, chl))
+        got = ctx.env_update_right(R, B, W)
+        ref = oracle.env_update_right(R, B, W)
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+# ---------------- K6: SVD ----------------
+
+@pytest.mark.parametrize("shape", [(2, 2), (8, 8), (6, 3), (3, 6), (1, 5), (5, 1), (12, 9),
+                                   (64, 64), (100, 37), (96, 256), (512, 512)])
+def test_svd_matches_oracle(ctx, oracle, shape):
+    rng = np.random.default_rng(sum(shape))
+    m = rng.standard_normal(shape)
+    u, s, vt, sweeps = ctx.svd_full(m)
+    uo, so, vto = oracle.svd(m)
+    k = min(shape)
+    assert np.abs(s - so).max() <= 1e-11 * so[0]           # north_star: 1e-11 relative
+    assert np.abs(u.T @ u - np.eye(k)).max() <= 1e-10      # test_linalg.cpp:25-34
+    assert np.abs(vt @ vt.T - np.eye(k)).max() <= 1e-10
+    assert np.linalg.norm(m - (u * s) @ vt) / np.linalg.norm(m) <= 1e-10
+    assert np.all(np.diff(s) <= 0)
+    for j in range(k):  # fix_phases convention
+        i = int(np.argmax(np.abs(u[:, j])))
+        assert u[i, j] > 0
+    # same phase-fixed factors as the oracle where sigma is non-degenerate
+    gap = np.minimum(np.abs(np.diff(so, prepend=np.inf)), np.abs(np.diff(so, append=-np.inf)))
+    ok = gap > 1e-6 * so[0]
+    assert np.abs(u[:, ok] - uo[:, ok]).max() <= 1e-8
+
+
+def test_svd_known_answers(ctx):  # test_linalg.cpp:38-55
+    u, s, vt, _ = ctx.svd_full(np.eye(2))
+    assert np.allclose(s, 1, atol=1e-12)
+    assert np.abs(u - np.eye(2)).max() <= 1e-12 and np.abs(vt - np.eye(2)).max() <= 1e-12
+    _, s, _, _ = ctx.svd_full(np.diag([3.0, 2.0]))
+    assert abs(s[0] - 3) <= 3e-13 and abs(s[1] - 2) <= 2e-13
+    bad = np.zeros((2, 2))
+    bad[0, 0] = np.nan
+    with pytest.raises(Exception, match="InvalidMatrix"):
+        ctx.svd_full(bad)
+
+
+def test_svd_batched(ctx, oracle):
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((4, 128, 128))
+    s = ctx.svd_batched(a)
+    for i in range(4):
+        so = oracle.svd(a[i])[1]
+        assert np.abs(s[i] - so).max() <= 1e-11 * so[0]
+
+
+# ---------------- K7: fused bond select / controller ----------------
+
+def test_bond_select_matches_oracle_controller(ctx, oracle):
+    rng = np.random.default_rng(8)
+    for mode in (abi.MODE_PID, abi.MODE_THRESHOLD, abi.MODE_DIRECT, abi.MODE_FIXED):
+        cfg = abi.dmrg_config(abi.controller_config(mode=mode, chi_min=2, chi_max=40, eps_trunc=1e-6))
+        st_g = oracle.state(chi=2, initialized=1, history=[0.0], history_len=1)
+        st_o = oracle.state(chi=2, initialized=1, history=[0.0], history_len=1)
+        for t in range(60):
+            r = int(rng.integers(1, 200))
+            v = np.sort(np.exp(-rng.uniform(0, 12, r)))[::-1]
+            v /= np.linalg.norm(v)
+            request = st_o.chi
+            row, visit = ctx.bond_select(cfg, v, st_g, 0, 3)
+            rowo = oracle.controller_update(st_o, v, cfg.controller)
+            floor, _ = oracle.rank_for_discarded_weight(v, cfg.controller.eps_trunc)
+            assert visit.floor_rank == floor
+            assert row.chi == rowo.chi and st_g.chi == st_o.chi
+            assert abs(row.s_raw - rowo.s_raw) <= 1e-13
+            assert abs(st_g.ema - st_o.ema) <= 1e-13 and abs(st_g.integral - st_o.integral) <= 1e-13
+            # kept rule (dmrg.cpp:113-136)
+            c = cfg.controller
+            if mode == abi.MODE_FIXED:
+                kept = c.chi_max
+            else:
+                kept = min(max(max(request, floor), c.chi_min), c.chi_max)
+                sig = int((v > 1e-14 * v[0]).sum())
+                kept = min(kept, max(sig, 1))
+            kept = max(min(kept, len(v)), 1)
+            assert visit.kept == kept
+            assert abs(visit.trunc_error - oracle.truncation_error(v, kept)) <= 1e-14
+            assert abs(visit.entropy - oracle.entropy(v)) <= 1e-13
+
+
+def test_bond_select_rejects_zero_spectrum(ctx):
+    cfg = abi.adaptive_config(16)
+    with pytest.raises(Exception, match="DegenerateSpectrum"):
+        ctx.bond_select(cfg, np.zeros(4), abi.BondState(chi=2, initialized=1, history_len=1))
+
+
+# ---------------- K5: Lanczos ----------------
+
+def test_eigs_known_answers(ctx):  # test_linalg.cpp:170-193
+    ev, vec, _, _ = ctx.eigs_lowest_dense(np.diag([-1.0, 0.0, 1.0]), np.ones(3), 1e-12, 100)
+    assert abs(ev + 1) <= 1e-10 and abs(abs(vec[0]) - 1) <= 1e-8
+    h = np.array([[0.25, 0, 0, 0], [0, -0.25, 0.5, 0], [0, 0.5, -0.25, 0], [0, 0, 0, 0.25]])
+    ev, *_ = ctx.eigs_lowest_dense(h, np.random.default_rng(0).standard_normal(4), 1e-12, 100)
+    assert abs(ev + 0.75) <= 1e-10
+
+
+def test_eigs_dense_64_vs_oracle(ctx, oracle):  # test_linalg.cpp:195-206
+    rng = np.random.default_rng(777)
+    a = rng.standard_normal((64, 64))
+    h = 0.5 * (a + a.T)
+    v0 = rng.standard_normal(64)
+    ev, vec, mv, res = ctx.eigs_lowest_dense(h, v0, 1e-11, 400)
+    evo, _, mvo, _ = oracle.eigs_lowest_dense(h, v0, 1e-11, 400)
+    assert abs(ev - np.linalg.eigvalsh(h)[0]) <= 1e-9 and abs(ev - evo) <= 1e-12
+    assert np.linalg.norm(h @ vec - ev * vec) <= 1e-11 * max(1, abs(ev))
+    assert abs(mv - mvo) <= 2
+
+
+def test_eigs_nonconvergence(ctx):  # test_linalg.cpp:208-226
+    rng = np.random.default_rng(12)
+    a = rng.standard_normal((32, 32))
+    h = 0.5 * (a + a.T)
+    with pytest.raises(Exception) as ei:
+        ctx.eigs_lowest_dense(h, np.ones(32), 1e-14, 3)
+    assert ei.value.name == "EigenNonConvergence" and ei.value.residual > 0
+    with pytest.raises(Exception, match="InvalidMatrix"):
+        ctx.eigs_lowest_dense(np.eye(4), np.zeros(4), 1e-10, 10)
+
+
+# ---------------- full local update: DMRG parity ----------------
+
+def compare_runs(g, o, e_rel=1e-10):
+    assert g["n_sweeps"] == o["n_sweeps"]
+    for a, b in zip(g["energies"], o["energies"]):
+        assert abs(a - b) <= e_rel * abs(b), (a, b)
+    assert np.array_equal(g["chi_profiles"], o["chi_profiles"])
+    assert np.abs(g["entropy_profiles"] - o["entropy_profiles"]).max() <= 1e-8
+    assert [v.kept for v in g["visits"]] == [v.kept for v in o["visits"]]
+
+
+def test_dmrg_c1_parity(ctx, oracle):
+    """Config C1: Heisenberg N=20 fixed chi=32, 5 sweeps (BASELINE.json configs[0])."""
+    spec = abi.model_spec(20)
+    cfg = abi.fixed_config(32, max_sweeps=5)
+    g = ctx.run_dmrg(spec, cfg)
+    o = oracle.run_dmrg(spec, cfg)
+    compare_runs(g, o)
+    assert abs(g["energy"] / 20 + 1.736494666879792) <= 1e-8
+
+
+def test_dmrg_pid_parity_criterion2(ctx, oracle):  # acceptance_main.cpp:106-126
+    spec = abi.model_spec(20)
+    cfg = abi.adaptive_config(64, 1e-5)
+    g = ctx.run_dmrg(spec, cfg)
+    o = oracle.run_dmrg(spec, cfg)
+    compare_runs(g, o)
+    assert g["records"][-1].average_chi <= 10.0 and g["max_chi_used"] <= 14
+    gt = [(t.chi, t.delta_chi, t.clamped) for t in g["trace"]]
+    ot = [(t.chi, t.delta_chi, t.clamped) for t in o["trace"]]
+    assert gt == ot
+
+
+def test_dmrg_small_known_answers(ctx, oracle):  # test_dmrg.cpp:111-126,179-186
+    r = ctx.run_dmrg(abi.model_spec(2, convention=abi.SPIN_HALF), abi.fixed_config(4))
+    assert abs(r["energy"] + 0.75) <= 1e-9 * 0.75
+    spec = abi.model_spec(8)
+    r = ctx.run_dmrg(spec, abi.fixed_config(16, eps_conv=1e-10))
+    assert r["converged"] and r["n_sweeps"] <= 5
+    assert abs(r["energy"] - oracle.exact_ground_energy(spec)) <= 1e-8
+    f = ctx.run_dmrg(spec, abi.fixed_config(12))
+    pinned = abi.adaptive_config(12)
+    pinned.controller.chi_min = 12
+    a = ctx.run_dmrg(spec, pinned)
+    assert abs(f["energy"] - a["energy"]) <= 1e-10
+
+
+def test_env_cache_equals_rebuild(ctx):  # test_dmrg.cpp:151-177 (Neel start)
+    from paper_2604_03960_b200.api import Chain
+    spec = abi.model_spec(8)
+    ch = Chain(ctx, spec, abi.fixed_config(8))
+    ch.sweep(0)
+    cached = [ch.env(1, k) for k in range(8)]
+    sites = [ch.site(k) for k in range(8)]
+    fresh = Chain(ctx, spec, abi.fixed_config(8))
+    fresh.load_state(sites)
+    for k in range(8):
+        b = fresh.env(1, k)
+        assert cached[k].shape == b.shape
+        assert np.abs(cached[k] - b).max() <= 1e-10
+
+
+def test_trace_rows_per_visit(ctx):  # test_dmrg.cpp:270-279
+    cfg = abi.adaptive_config(16, max_sweeps=3, eps_conv=1e-16)
+    r = ctx.run_dmrg(abi.model_spec(6), cfg)
+    assert r["n_sweeps"] == 3 and len(r["trace"]) == 3 * 2 * 5
+
+
+def test_launch_counter_moves(ctx):
+    before = ctx.launches
+    ctx.apply_effective_hamiltonian(np.ones((2, 5, 2)), *[np.ones((5, 2, 2, 5))] * 2,
+                                    np.ones((2, 5, 2)), np.ones((2, 2, 2, 2)))
+    assert ctx.launches > before
