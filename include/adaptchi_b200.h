@@ -226,6 +226,14 @@ int achi_bond_select(achi_ctx* ctx, const achi_dmrg_config* cfg, int n_sigma,
                      const double* sigma, achi_bond_state* state, int sweep,
                      int bond, achi_trace_row* row, achi_visit_record* visit);
 
+/* The contraction engine behind K1-K4 (TMA-fed DMMA GEMM), exposed for unit
+ * tests: C (M x N, row-major, ldc) = A * B.  a_kmajor: A stored M x K
+ * row-major (else K x M); b_kmajor: B stored N x K row-major (else K x N).
+ * Leading dimensions must be even (16-byte TMA strides).  Replaces the GEMM
+ * inside Tensor::contract (tensor.hpp:195-196). */
+int achi_dgemm(achi_ctx* ctx, int M, int N, int K, int a_kmajor, const double* a, long lda,
+               int b_kmajor, const double* b, long ldb, double* c, long ldc);
+
 /* eigs_lowest (linalg.cpp:107-178) with a dense symmetric operator (test
  * hook for the device Lanczos): h is dim x dim row-major. */
 int achi_eigs_lowest_dense(achi_ctx* ctx, int dim, const double* h,

@@ -166,6 +166,8 @@ def load():
                                        C.c_int, C.c_int, P(TraceRow), P(VisitRecord)]),
         "achi_eigs_lowest_dense": (C.c_int, [vp, C.c_int, dp, dp, d, C.c_int, dp, dp,
                                              P(C.c_int), dp]),
+        "achi_dgemm": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, dp, C.c_long, C.c_int,
+                                 dp, C.c_long, dp, C.c_long]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -137,6 +137,17 @@ class Context:
                                                     C.byref(res)))
         return ev.value, vec, mv.value, res.value
 
+    def dgemm(self, a, b, a_kmajor=True, b_kmajor=False):
+        """C = A @ B on the TMA/DMMA engine.  a: (M,K) if a_kmajor else (K,M) stored;
+        b: (N,K) if b_kmajor else (K,N) stored."""
+        a, b = _f64(a), _f64(b)
+        M, K = (a.shape[0], a.shape[1]) if a_kmajor else (a.shape[1], a.shape[0])
+        N = b.shape[0] if b_kmajor else b.shape[1]
+        c = np.zeros((M, N + (N & 1)))
+        self._check(self.lib.achi_dgemm(self.h, M, N, K, int(a_kmajor), _dp(a), a.shape[1],
+                                        int(b_kmajor), _dp(b), b.shape[1], _dp(c), c.shape[1]))
+        return c[:, :N]
+
     # ---- DMRG ----
     def chain(self, spec, cfg) -> "Chain":
         return Chain(self, spec, cfg)

@@ -369,6 +369,27 @@ int achi_bond_select(achi_ctx* ctx, const achi_dmrg_config* cfg, int n_sigma, co
   });
 }
 
+int achi_dgemm(achi_ctx* ctx, int M, int N, int K, int a_kmajor, const double* a, long lda,
+               int b_kmajor, const double* b, long ldb, double* c, long ldc) {
+  return guard(ctx, [&] {
+    Ctx& cx = ctx->c;
+    const size_t na = static_cast<size_t>(a_kmajor ? M : K) * lda;
+    const size_t nb = static_cast<size_t>(b_kmajor ? N : K) * ldb;
+    const size_t nc = static_cast<size_t>(M) * ldc;
+    DevBuf dA, dB, dC;
+    dA.reserve(na);
+    dB.reserve(nb);
+    dC.reserve(nc);
+    h2d(cx, dA.p, a, na);
+    h2d(cx, dB.p, b, nb);
+    ACHI_CUDA(cudaMemsetAsync(dC.p, 0, nc * sizeof(double), cx.stream));
+    gemm(cx, M, N, K, Operand{dA.p, lda, a_kmajor ? Major::kK : Major::kMN},
+         Operand{dB.p, ldb, b_kmajor ? Major::kK : Major::kMN}, dC.p, ldc);
+    d2h(cx, c, dC.p, nc);
+    cx.sync();
+  });
+}
+
 int achi_eigs_lowest_dense(achi_ctx* ctx, int dim, const double* h, const double* v0, double tol,
                            int max_iter, double* eigenvalue, double* eigenvector, int* matvecs,
                            double* residual) {

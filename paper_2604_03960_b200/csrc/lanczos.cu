@@ -152,7 +152,8 @@ __device__ void tridiag_lowest_dev(const double* a, const double* b, int k, doub
   double dd[LANCZOS_BLOCK], du[LANCZOS_BLOCK], dl[LANCZOS_BLOCK], x[LANCZOS_BLOCK];
   const double tiny = (scale > 0 ? scale : 1.0) * 1e-300 + 1e-300;
   const double pivmin = (scale > 0 ? scale : 1.0) * 2.3e-16;
-  for (int i = 0; i < k; ++i) x[i] = 1.0;
+  // generic deterministic start (a symmetric start can be an exact eigenvector)
+  for (int i = 0; i < k; ++i) x[i] = 1.0 + 0.5 * sin(1.0 + 2.3 * i);
   for (int iter = 0; iter < 3; ++iter) {
     for (int i = 0; i < k; ++i) dd[i] = a[i] - theta;
     for (int i = 0; i + 1 < k; ++i) dl[i] = du[i] = b[i];

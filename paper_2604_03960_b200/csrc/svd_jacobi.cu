@@ -50,6 +50,7 @@ struct RoundArgs {
   int vrows;
   int nb, round;
   double tol;
+  const double* zero2;  // per batch: columns with ||g||^2 <= zero2 are numerically zero
   unsigned long long* conv;
 };
 
@@ -115,6 +116,7 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(RoundArgs a) {
   __shared__ JacobiSmem sm;
   double* G = a.G + blockIdx.y * a.gstride;
   double* V = a.V + blockIdx.y * a.vstride;
+  const double z2 = a.zero2[blockIdx.y];
   int ba, bb;
   circle_pair(a.nb, a.round, blockIdx.x, ba, bb);
   const int ca = ba * JB, cb = bb * JB;
@@ -151,10 +153,8 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(RoundArgs a) {
   double meas = 0.0;
   for (int idx = threadIdx.x; idx < JW * JW; idx += JT) {
     const int i = idx / JW, j = idx - i * JW;
-    if (i < j) {
-      const double d = sm.S[i][i] * sm.S[j][j];
-      if (d > 0) meas = fmax(meas, fabs(sm.S[i][j]) / sqrt(d));
-    }
+    if (i < j && sm.S[i][i] > z2 && sm.S[j][j] > z2)
+      meas = fmax(meas, fabs(sm.S[i][j]) / sqrt(sm.S[i][i] * sm.S[j][j]));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) meas = fmax(meas, __shfl_xor_sync(0xffffffffu, meas, o));
@@ -179,8 +179,7 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(RoundArgs a) {
         circle_pair(JW, step, threadIdx.x, i, j);
         const double app = sm.S[i][i], aqq = sm.S[j][j], apq = sm.S[i][j];
         double c = 1.0, s = 0.0;
-        const double d = app * aqq;
-        if (d > 0 && fabs(apq) > a.tol * sqrt(d)) {
+        if (app > z2 && aqq > z2 && fabs(apq) > a.tol * sqrt(app * aqq)) {
           const double tau = (aqq - app) / (2.0 * apq);
           const double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
           c = 1.0 / sqrt(1.0 + t * t);
@@ -264,6 +263,25 @@ __global__ void load_g_kernel(const double* __restrict__ theta, long tstride, in
       const int c = c0 + dy, r = r0 + threadIdx.x;
       if (c < ng && r < mg) Gb[static_cast<long>(c) * mg + r] = tile[threadIdx.x][dy];
     }
+  }
+}
+
+// zero2[b] = (sqrt(mg) * eps * ||G_b||_F)^2: the rounding floor of a column norm
+__global__ void zero_floor_kernel(const double* __restrict__ G, long gstride, long len, int mg,
+                                  double* __restrict__ zero2) {
+  __shared__ double sh[32];
+  const double* g = G + blockIdx.x * gstride;
+  double s = 0.0;
+  for (long i = threadIdx.x; i < len; i += blockDim.x) s += g[i] * g[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (blockDim.x >> 5); ++w) t += sh[w];
+    const double f = sqrt(static_cast<double>(mg)) * EPS;
+    zero2[blockIdx.x] = f * f * t;
   }
 }
 
@@ -370,6 +388,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   double* sorted = ws.sorted.reserve(static_cast<size_t>(ng) * batch);
   int* perm = ws.perm.reserve(static_cast<size_t>(ng) * batch);
   unsigned long long* conv = ws.conv.reserve(4);
+  double* zero2 = ws.zero2.reserve(static_cast<size_t>(batch));
   unsigned long long* conv_h = ws.conv_host.reserve(4);
 
   {
@@ -379,6 +398,8 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     dim3 g2(static_cast<unsigned>(std::min<long>(cdiv(vstride, 256), 4L * ctx.num_sms)), batch);
     identity_kernel<<<g2, 256, 0, ctx.stream>>>(V, ng, ng, vstride);
     ACHI_LAUNCHED(ctx);
+    zero_floor_kernel<<<batch, 1024, 0, ctx.stream>>>(G, gstride, gstride, mg, zero2);
+    ACHI_LAUNCHED(ctx);
   }
   const int nb = ng / JB;  // even (ng multiple of 32)
   const double tol = std::max(1e-15, 2.0 * std::sqrt(static_cast<double>(mg)) * EPS);
@@ -386,7 +407,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   for (; sweeps < 40; ++sweeps) {
     ACHI_CUDA(cudaMemsetAsync(conv, 0, sizeof(unsigned long long), ctx.stream));
     for (int r = 0; r < nb - 1; ++r) {
-      RoundArgs a{G, mg, gstride, mg, V, ng, vstride, ng, nb, r, tol, conv};
+      RoundArgs a{G, mg, gstride, mg, V, ng, vstride, ng, nb, r, tol, zero2, conv};
       jacobi_round_kernel<<<dim3(nb / 2, batch), JT, 0, ctx.stream>>>(a);
       ACHI_LAUNCHED(ctx);
     }

@@ -15,7 +15,7 @@
 namespace achi {
 
 struct SvdWs {
-  DevBuf G, V, sig, sorted;
+  DevBuf G, V, sig, sorted, zero2;
   DevArr<int> perm;
   DevArr<double> sign;
   DevArr<unsigned long long> conv;

@@ -74,7 +74,10 @@ def test_heff_large_vs_einsum(ctx, oracle, chi):
     L, R = rand_env(rng, chi, 5), rand_env(rng, chi, 5)
     th = rng.standard_normal((chi, 2, 2, chi))
     got = ctx.apply_effective_hamiltonian(L, w[2], w[3], R, th)
-    ref = np.einsum("bal,lstr,aSsc,cTte,Rer->bSTR", L, th, w[2], w[3], R, optimize=True)
+    x = np.einsum("bal,lstr->bastr", L, th)
+    y = np.einsum("bastr,aSsc->bStrc", x, w[2])
+    z = np.einsum("bStrc,cTte->bSTre", y, w[3])
+    ref = np.einsum("bSTre,Rer->bSTR", z, R)
     assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
