@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native two-site DMRG local update.
+
+Metric (BASELINE.json): "DMRG sweep wall time Heisenberg N=100 chi<=1024;
+trunc-SVD ms at chi=2048".
+
+Workload (config C3, BASELINE.json configs[2]): Heisenberg spin-1/2 open
+chain N=100, adaptive PID/EMA chi with chi_max=1024, eps_trunc=1e-10, Neel
+start (dmrg.cpp:222-232), synthetic (no input data).  One "step" = one
+two_site_sweep (dmrg.cpp:175-214).  W warm-up sweeps grow chi from 1; the K
+timed sweeps are sweeps W..W+K-1 of the same run.  value = device time per
+sweep (CUDA events on the library stream), max over ranks.  The second half
+of the metric (truncated SVD of a random 4096x4096 FP64 theta, chi=2048) is
+reported as "svd_chi2048_ms".
+
+--impl reference times the reference algorithm on the host cores (the C++
+oracle port of /root/reference/proj in complex128, all threads) on the same
+workload.  Multi-GPU: a single chain does not shard (a sweep is sequential,
+dmrg.cpp:156-163), so N GPUs run N independent replicas ("replicas only").
+"""
+from __future__ import annotations
+
+import argparse
+import faulthandler
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from paper_2604_03960_b200 import abi  # noqa: E402
+
+METRIC = "DMRG sweep wall time Heisenberg N=100 chi<=1024; trunc-SVD ms at chi=2048"
+# FP64 roofline denominator: MEASURED_PEAKS.json has no FP64 entry; measured on
+# this pool's B200s (profiles/fp64_peak_r01.txt): DMMA instruction peak 37.1
+# TFLOP/s (cuBLAS DGEMM 8192^3 burst 35.5).
+FP64_PEAK_TFLOPS = 37.1
+N_SITES, CHI_MAX, EPS_TRUNC = 100, 1024, 1e-10
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def workload(max_sweeps):
+    spec = abi.model_spec(N_SITES, convention=abi.SPIN_HALF)
+    cfg = abi.adaptive_config(CHI_MAX, EPS_TRUNC, max_sweeps=max_sweeps)
+    return spec, cfg
+
+
+# ---------------------------------------------------------------- distributed
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl")
+            self.dist, self.torch = dist, torch
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, x):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([float(x)], device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[2 + i].strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- helpers
+def mv_flops(chl, chr_, D=5, d=2):
+    return 2.0 * D * d * d * chl * chr_ * (chl + chr_) + 4.0 * D * D * d ** 3 * chl * chr_
+
+
+def visit_cost_model(visits, chi_profile):
+    """FLOP proxy per visit: matvecs x H_eff flops + SVD (~22 m n^2) + env update."""
+    dims = [1] + list(chi_profile) + [1]
+    cost = []
+    for v in visits:
+        b = v.bond
+        chl, chr_ = dims[b], dims[b + 2]
+        m, n = 2 * chl, 2 * chr_
+        svd = 22.0 * max(m, n) * min(m, n) ** 2
+        env = 4.0 * 5 * 2 * max(chl, chr_) * v.kept * (max(chl, chr_) + v.kept)
+        cost.append(v.matvecs * mv_flops(chl, chr_) + svd + env)
+    return np.array(cost)
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- our arm
+def log(msg):
+    print(f"[bench] {msg}", file=sys.stderr, flush=True)
+
+
+def run_ours(args, dist):
+    from paper_2604_03960_b200.api import Chain, Context
+    ctx = Context(dist.local)
+    W, K = args.warmup, args.steps
+    spec, cfg = workload(W + K)
+    t0 = time.perf_counter()
+    ch = Chain(ctx, spec, cfg)
+    setup_s = time.perf_counter() - t0
+    for s in range(W):
+        ch.sweep(s)
+    ctx.device_times(enable=True, reset=True)
+    launches0 = ctx.launches
+    sampler = ClockSampler(dist.local)
+    sampler.start()
+    dev_ms, host_s, last = [], [], None
+    for i in range(K):
+        ctx.flush_l2(256 << 20)  # > 126 MB L2: each timed sweep starts cold
+        dist.barrier()
+        ctx.timer_start()
+        th = time.perf_counter()
+        last = ch.sweep(W + i)  # public API call: returns the step's results to the host
+        host_s.append(time.perf_counter() - th)
+        dev_ms.append(ctx.timer_stop())
+    clocks = sampler.stop()
+    log(f"timed sweeps done: {dev_ms}")
+    launches = ctx.launches - launches0
+    phases = ctx.device_times(enable=False)
+    sweep_s = dist.max(float(np.mean(dev_ms)) / 1e3)
+    e2e_s = dist.max(float(np.mean(host_s)))
+    chi = last["chi_profile"]
+    nb = N_SITES - 1
+    d2h = 56 + nb * (4 + 8) + 2 * nb * (80 + 96)  # record + profiles + trace + visit rows
+    hbm, hbm_src = peaks()
+    # roofline of the dominant phase (by device time)
+    svd, mv = phases["svd"], phases["matvec"]
+    svd_gbs = svd["work"] / max(svd["ms"], 1e-9) / 1e6
+    mv_tfs = mv["work"] / max(mv["ms"], 1e-9) / 1e9
+    roof_svd = {"bound": "hbm", "kernel": "jacobi_round_kernel (blocked one-sided Jacobi SVD)",
+                "achieved": round(svd_gbs, 3), "peak": hbm, "unit": "GB/s",
+                "frac": round(svd_gbs / hbm, 6), "traffic": None,
+                "work_def": "16*(m*n+n^2)*jacobi_sweeps bytes per SVD", "peak_source": hbm_src}
+    roof_mv = {"bound": "tensor", "kernel": "dmma_gemm_kernel + mpo_mix_kernel (H_eff matvec)",
+               "achieved": round(mv_tfs, 4), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+               "frac": round(mv_tfs / FP64_PEAK_TFLOPS, 6), "traffic": None,
+               "work_def": "2*D*d^2*chl*chr*(chl+chr)+4*D^2*d^3*chl*chr flops per matvec",
+               "peak_source": "measured DMMA peak (profiles/fp64_peak_r01.txt)"}
+    dominant = roof_svd if svd["ms"] >= mv["ms"] else roof_mv
+    out = {
+        "metric": METRIC, "value": round(sweep_s, 6), "unit": "s/sweep",
+        "n_gpus": dist.world, "steps": K, "warmup": W, "ms_per_step": round(sweep_s * 1e3, 3),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (Neel start, no input data)",
+        "config": {"workload": "C3: Heisenberg S=1/2 OBC N=100, PID/EMA chi_max=1024, "
+                               "eps_trunc=1e-10, timed sweeps W..W+K-1",
+                   "n": N_SITES, "chi_max": CHI_MAX, "eps_trunc": EPS_TRUNC,
+                   "parallelism": f"replicas x{dist.world} (a chain does not shard)",
+                   "l2": "flushed (256 MB write) before every timed sweep"},
+        "e_per_site": last["energy"] / N_SITES, "chi_max_seen": int(chi.max()),
+        "chi_avg": round(float(chi.mean()), 2), "setup_s": round(setup_s, 4),
+        "phases_ms": {k: round(v["ms"], 3) for k, v in phases.items()},
+        "roofline": dominant, "roofline_matvec": roof_mv,
+        "e2e": {"value": round(e2e_s, 6), "unit": "s/sweep", "h2d_bytes_per_step": 4,
+                "d2h_bytes_per_step": d2h,
+                "note": "host wall time of the public Chain.sweep call incl. result readback; "
+                        "the MPS/environments are device-resident (uploaded once at setup)"},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    if not args.skip_svd:
+        log("svd part")
+        out.update(svd_part(ctx, args))
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        log("cpu baseline")
+        out["cpu_baseline"] = cpu_baseline_sample(spec, cfg, ch, last)
+    ctx.close()
+    return out
+
+
+def svd_part(ctx, args):
+    """Truncated-SVD half of the metric: random 4096x4096 FP64 theta (chi=2048)."""
+    import torch
+    n = 2 * args.svd_chi
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+    s = torch.empty(n, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    ctx.svd_batched_device(a.data_ptr(), 1, n, n, s.data_ptr())  # warm-up
+    ms, sweeps = [], 0
+    for _ in range(args.svd_reps):
+        ctx.flush_l2(256 << 20)
+        ctx.timer_start()
+        sweeps = ctx.svd_batched_device(a.data_ptr(), 1, n, n, s.data_ptr())
+        ms.append(ctx.timer_stop())
+    fro = float((a * a).sum())
+    err = abs(float((s * s).sum()) - fro) / fro
+    # e2e through the host-buffer API (H2D of theta, D2H of sigma inside the timed region)
+    ha = a.cpu().numpy()
+    t = time.perf_counter()
+    ctx.svd_batched(ha[None])
+    e2e = time.perf_counter() - t
+    hbm, _ = peaks()
+    med = statistics.median(ms)
+    gbs = 16.0 * sweeps * (n * n + n * n) / (med * 1e-3) / 1e9
+    return {"svd_chi2048_ms": round(med, 3), "svd_chi2048_e2e_ms": round(e2e * 1e3, 3),
+            "svd_chi2048_sweeps": sweeps, "svd_chi2048_sum_sigma2_relerr": err,
+            "svd_chi2048_roofline": {"bound": "hbm", "achieved": round(gbs, 2), "peak": hbm,
+                                     "unit": "GB/s", "frac": round(gbs / hbm, 5)}}
+
+
+def cpu_baseline_sample(spec, cfg, ch, last):
+    """Oracle port (complex128, all host threads) on a bounded sample: 20 right-moving
+    visits at the chain centre from the steady-state MPS, extrapolated to the full
+    sweep with a FLOP model weighted by this run's own visit records."""
+    from oracle import oracle as O
+    threads = cpu_threads()
+    O.set_threads(threads)
+    sites = [ch.site(k) for k in range(N_SITES)]
+    states = ch.states()
+    first, count = 40, 20
+    secs, mvs = O.time_visits_from_state(spec, cfg, sites, states, first, count, complex_mode=True)
+    chi = last["chi_profile"]
+
+    class V:
+        def __init__(self, bond, matvecs, kept):
+            self.bond, self.matvecs, self.kept = bond, matvecs, kept
+    sample = [V(first + i, int(mvs[i]), int(chi[first + i])) for i in range(count)]
+    c_sample = visit_cost_model(sample, chi).sum()
+    c_full = visit_cost_model(last["visits"], chi).sum()
+    est = float(secs.sum()) * c_full / c_sample
+    return {"value": round(est, 3), "unit": "s/sweep", "cores": threads, "kind": "port",
+            "sample": f"{count} right-moving visits (bonds {first}..{first + count - 1}) of the "
+                      f"steady-state sweep on the oracle (complex128, OpenBLAS {threads} threads): "
+                      f"{secs.sum():.2f} s, extrapolated to all {2 * (N_SITES - 1)} visits by FLOP "
+                      f"model (matvecs x H_eff flops + SVD + env)"}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, dist):
+    """The reference algorithm (oracle port of proj/src, complex128) on the host cores."""
+    if dist.rank != 0:
+        return None
+    from oracle import oracle as O
+    threads = cpu_threads()
+    O.set_threads(threads)
+    W, K = args.warmup, args.steps
+    spec, cfg = workload(W + K)
+    cfg.eps_conv = 1e-300  # time fixed sweeps (no early stop), as the GPU arm does
+    ch = O.OracleChain(spec, cfg, complex_mode=True)
+    for s in range(W):
+        ch.sweep(s)
+    walls, budget_hit = [], False
+    t0 = time.perf_counter()
+    for i in range(K):
+        rec, chi = ch.sweep(W + i)
+        walls.append(rec.wall_time)
+        if time.perf_counter() - t0 > args.ref_budget_s:
+            budget_hit = i + 1 < K
+            break
+    ch.close()
+    v = float(np.mean(walls))
+    sample = (f"sweeps {W}..{W + len(walls) - 1} of the C3 run, full sweeps, complex128, "
+              f"OpenBLAS {threads} threads" + (f" (stopped after {len(walls)} of {K} steps: "
+                                               f"{args.ref_budget_s:.0f} s budget)" if budget_hit else ""))
+    return {"metric": METRIC, "value": round(v, 4), "unit": "s/sweep", "impl": "reference",
+            "n_gpus": dist.world, "steps": len(walls), "warmup": W,
+            "ms_per_step": round(v * 1e3, 2), "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic (Neel start)",
+            "config": {"workload": "C3: Heisenberg S=1/2 OBC N=100, PID/EMA chi_max=1024, "
+                                   "eps_trunc=1e-10", "n": N_SITES, "chi_max": CHI_MAX},
+            "e_per_site": rec.energy / N_SITES, "chi_max_seen": int(chi.max()),
+            "cpu_baseline": {"value": round(v, 4), "unit": "s/sweep", "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": round(v, 4), "unit": "s/sweep", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    faulthandler.enable()
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--svd-chi", type=int, default=2048)
+    ap.add_argument("--svd-reps", type=int, default=3)
+    ap.add_argument("--skip-svd", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=180.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # contract: W >= 3
+    dist = Dist()
+    out = run_reference(args, dist) if args.impl == "reference" else run_ours(args, dist)
+    if dist.rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+    dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -149,6 +149,17 @@ double achi_last_residual(const achi_ctx* ctx);
 /* number of device kernels this context launched so far (evidence counter) */
 int64_t achi_launch_count(const achi_ctx* ctx);
 int achi_synchronize(achi_ctx* ctx);
+/* CUDA-event timer on the context's stream (device time between start and
+ * stop, in ms, after a stream synchronize). */
+int achi_timer_start(achi_ctx* ctx);
+int achi_timer_stop(achi_ctx* ctx, double* ms);
+/* write `bytes` through a scratch buffer on the context's stream (L2 flush) */
+int achi_flush_l2(achi_ctx* ctx, size_t bytes);
+/* Per-phase device time measured with CUDA events on the context stream
+ * (phases: 0 H_eff matvec, 1 SVD, 2 environment update).  enable turns the
+ * accounting on/off (-1 leaves it); reset zeroes it.  out9 (may be NULL) =
+ * {ms[3], algorithmic work[3] (flops, bytes, flops), launches[3]}. */
+int achi_device_times(achi_ctx* ctx, int enable, int reset, double* out9);
 
 /* ---- DMRG (dmrg.hpp:40-90, dmrg.cpp:216-282) ---- */
 /* run_dmrg setup: validate, build_mpo (real gauge), Neel product state,
@@ -187,6 +198,12 @@ int achi_chain_set_states(achi_chain* chain, const achi_bond_state* in);
 int achi_chain_load_state(achi_chain* chain, const int32_t* bond_dims,
                           const double* const* sites);
 
+/* Phase accounting since chain creation (host wall clock at sync points):
+ * out[0..7] = {lanczos+merge s, svd s, bond-select s, absorb+env s, matvecs,
+ * svd sweeps, visits, 0}.  profile != 0 adds a sync after each visit so the
+ * phase split is exact (default off: the hot path keeps its own syncs only). */
+int achi_chain_stats(achi_chain* chain, int profile, double* out8);
+
 /* ---- local kernels, host buffers (for parity tests and API-level calls) ---- */
 /* apply_effective_hamiltonian (dmrg.cpp:58-71): out(bl,s1',s2',br).
  * L: (chl, D1, chl) ; W1: (D1, d, d, D2); W2: (D2, d, d, D3); R: (chr, D3, chr);
@@ -216,6 +233,10 @@ int achi_svd(achi_ctx* ctx, int m, int n, const double* a, double* sigma,
  * config C2 (bench.cpp:635-668). */
 int achi_svd_batched(achi_ctx* ctx, int batch, int m, int n, const double* a,
                      double* sigma);
+/* Same on DEVICE pointers (inputs already resident in HBM; the benchmark's
+ * device-time path).  d_sigma: batch x min(m,n) device buffer. */
+int achi_svd_batched_device(achi_ctx* ctx, int batch, int m, int n, const double* d_a,
+                            double* d_sigma, int* sweeps_out);
 
 /* Fused bond-select kernel (K7) on a host spectrum: entropy_from_spectrum
  * (mps.cpp:97-113), rank_for_discarded_weight (controller.cpp:134-148),

@@ -117,6 +117,51 @@ def sample_visits(spec, cfg, warm_sweeps, first, count, complex_mode=True):
     return secs.value, dims
 
 
+class OracleChain:
+    """Step-wise oracle run (run_dmrg setup, then one two_site_sweep per call)."""
+
+    def __init__(self, spec, cfg, complex_mode=True):
+        self.n = spec.n
+        buf, bl = _err()
+        f = lib().oracle_chain_create
+        f.restype = C.c_void_p
+        self.h = f(C.byref(spec), C.byref(cfg), C.c_int(int(complex_mode)), buf, C.c_size_t(bl))
+        if not self.h:
+            raise OracleError(1, buf.value.decode())
+
+    def sweep(self, index):
+        rec = abi.SweepRecord()
+        chi = np.zeros(self.n - 1, np.int32)
+        buf, bl = _err()
+        _check(lib().oracle_chain_sweep(C.c_void_p(self.h), index, C.byref(rec), _ip(chi), buf,
+                                        C.c_size_t(bl)), buf)
+        return rec, chi
+
+    def close(self):
+        if self.h:
+            lib().oracle_chain_destroy(C.c_void_p(self.h))
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+def time_visits_from_state(spec, cfg, sites, states, first, count, complex_mode=True):
+    """Seconds and matvec counts of `count` right-moving visits from a given state."""
+    dims = np.array([s.shape[2] for s in sites[:-1]], np.int32)
+    flat = [np.ascontiguousarray(s, dtype=np.float64) for s in sites]
+    ptrs = (C.POINTER(C.c_double) * len(flat))(*[_dp(a) for a in flat])
+    st = (abi.BondState * len(states))(*states)
+    secs = np.zeros(count)
+    mv = np.zeros(count, np.int32)
+    buf, bl = _err()
+    rc = lib().oracle_time_visits_from_state(C.byref(spec), C.byref(cfg), C.c_int(int(complex_mode)),
+                                             _ip(dims), ptrs, st, first, count, _dp(secs), _ip(mv),
+                                             buf, C.c_size_t(bl))
+    _check(rc, buf)
+    return secs, mv
+
+
 def heff_apply(L, W1, W2, R, theta):
     chl, D1 = L.shape[0], L.shape[1]
     chr_, D3 = R.shape[0], R.shape[1]

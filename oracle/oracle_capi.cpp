@@ -171,6 +171,39 @@ int run_impl(const achi_model_spec* spec, const achi_dmrg_config* cfg, bool real
 
 }  // namespace
 
+// ---- step-wise chain (run_dmrg setup + two_site_sweep), for timed baselines ----
+struct OracleChainBase {
+  virtual ~OracleChainBase() = default;
+  virtual SweepRecord sweep(int s) = 0;
+};
+template <class T>
+struct OracleChain : OracleChainBase {
+  ModelSpec ms;
+  DmrgConfig dc;
+  std::vector<Tensor<T>> mpo;
+  MPS<T> psi;
+  Environment<T> env;
+  std::vector<BondState> states;
+  OracleChain(const ModelSpec& s, const DmrgConfig& c)
+      : ms(s), dc(c), mpo(build_mpo<T>(s, !std::is_same_v<T, cd>)), env(s.n) {
+    ms.validate();
+    dc.validate();
+    init_run(ms, dc, psi);
+    env.rebuild(psi, mpo, 0);
+    states.assign(ms.n - 1, BondState{});
+    for (auto& st : states) {  // dmrg.cpp:243-250
+      st.chi = dc.controller.chi_min;
+      st.ema = 0.0;
+      st.initialized = true;
+      st.push_history(0.0);
+    }
+  }
+  SweepRecord sweep(int s) override {
+    return two_site_sweep(psi, mpo, env, dc, states, s, nullptr, nullptr);
+  }
+};
+
+
 extern "C" {
 
 void oracle_set_threads(int n) { scipy_openblas_set_num_threads64_(n); }
@@ -232,6 +265,77 @@ int oracle_sample_visits(const achi_model_spec* spec, const achi_dmrg_config* cf
     return set_err(err, errlen, e);
   }
 }
+
+// Time `count` right-moving bond visits starting at `first` from a given
+// right-canonical real MPS (centre 0) and controller states: the sampled CPU
+// baseline for sweeps too long to run in full on the host.
+int oracle_time_visits_from_state(const achi_model_spec* spec, const achi_dmrg_config* cfg,
+                                  int complex_mode, const int32_t* dims, const double* const* sites,
+                                  const achi_bond_state* states, int first, int count,
+                                  double* seconds, int32_t* matvecs, char* err, size_t errlen) {
+  try {
+    auto body = [&](auto tag) -> int {
+      using T = decltype(tag);
+      ModelSpec ms = to_spec(spec);
+      DmrgConfig dc = to_cfg(cfg);
+      auto mpo = build_mpo<T>(ms, !std::is_same_v<T, cd>);
+      MPS<T> psi;
+      for (int k = 0; k < ms.n; ++k) {
+        long l = k == 0 ? 1 : dims[k - 1], r = k == ms.n - 1 ? 1 : dims[k];
+        Tensor<T> t({l, 2, r});
+        for (long i = 0; i < t.size(); ++i) t.data[i] = T(sites[k][i]);
+        psi.sites.push_back(std::move(t));
+      }
+      // move the canonical centre to `first` (QR sweeps, state unchanged) and
+      // build the environments there (Environment::rebuild, dmrg.cpp:51-56)
+      canonicalize(psi, first);
+      Environment<T> env(ms.n);
+      env.rebuild(psi, mpo, first);
+      std::vector<BondState> st(ms.n - 1);
+      for (int b = 0; b < ms.n - 1; ++b) st[b] = to_state(&states[b]);
+      for (int v = 0; v < count && first + v <= ms.n - 2; ++v) {
+        auto t0 = std::chrono::steady_clock::now();
+        VisitLog lg = visit_bond(psi, mpo, env, dc, st, first + v, true, 0, nullptr);
+        auto t1 = std::chrono::steady_clock::now();
+        seconds[v] = std::chrono::duration<double>(t1 - t0).count();
+        if (matvecs) matvecs[v] = lg.matvecs;
+      }
+      return 0;
+    };
+    return complex_mode ? body(cd{}) : body(double{});
+  } catch (const std::exception& e) {
+    return set_err(err, errlen, e);
+  }
+}
+
+void* oracle_chain_create(const achi_model_spec* spec, const achi_dmrg_config* cfg, int complex_mode,
+                          char* err, size_t errlen) {
+  try {
+    if (complex_mode) return new OracleChain<cd>(to_spec(spec), to_cfg(cfg));
+    return new OracleChain<double>(to_spec(spec), to_cfg(cfg));
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e);
+    return nullptr;
+  }
+}
+int oracle_chain_sweep(void* h, int sweep, achi_sweep_record* rec, int32_t* chi, char* err,
+                       size_t errlen) {
+  try {
+    SweepRecord r = static_cast<OracleChainBase*>(h)->sweep(sweep);
+    rec->sweep_index = r.sweep_index;
+    rec->max_chi_used = r.max_chi_used;
+    rec->energy = r.energy;
+    rec->max_trunc_error = r.max_trunc_error;
+    rec->wall_time = r.wall_time;
+    rec->parameter_count = r.parameter_count;
+    rec->average_chi = r.average_chi;
+    for (size_t b = 0; b < r.chi_profile.size(); ++b) chi[b] = r.chi_profile[b];
+    return 0;
+  } catch (const std::exception& e) {
+    return set_err(err, errlen, e);
+  }
+}
+void oracle_chain_destroy(void* h) { delete static_cast<OracleChainBase*>(h); }
 
 // apply_effective_hamiltonian (dmrg.cpp:58-71), real
 int oracle_heff_apply(int chl, int chr, int d, int D1, int D2, int D3, const double* L,

@@ -145,6 +145,9 @@ def load():
         "achi_last_residual": (d, [vp]),
         "achi_launch_count": (C.c_int64, [vp]),
         "achi_synchronize": (C.c_int, [vp]),
+        "achi_timer_start": (C.c_int, [vp]),
+        "achi_timer_stop": (C.c_int, [vp, dp]),
+        "achi_flush_l2": (C.c_int, [vp, C.c_size_t]),
         "achi_chain_create": (C.c_int, [vp, P(ModelSpec), P(DmrgConfig), P(vp)]),
         "achi_chain_destroy": (C.c_int, [vp]),
         "achi_chain_sweep": (C.c_int, [vp, C.c_int, P(SweepRecord), P(i32), dp,
@@ -152,6 +155,7 @@ def load():
         "achi_chain_run": (C.c_int, [vp, P(DmrgResult), P(SweepRecord), P(i32), dp,
                                      P(TraceRow), P(VisitRecord)]),
         "achi_chain_bond_dims": (C.c_int, [vp, P(i32)]),
+        "achi_chain_stats": (C.c_int, [vp, C.c_int, dp]),
         "achi_chain_get_site": (C.c_int, [vp, C.c_int, dp, C.c_size_t]),
         "achi_chain_get_env": (C.c_int, [vp, C.c_int, C.c_int, P(C.c_int64), dp, C.c_size_t]),
         "achi_chain_get_states": (C.c_int, [vp, P(BondState)]),
@@ -162,6 +166,9 @@ def load():
         "achi_env_update_right": (C.c_int, [vp] + [C.c_int] * 5 + [dp] * 4),
         "achi_svd": (C.c_int, [vp, C.c_int, C.c_int, dp, dp, dp, dp, P(C.c_int)]),
         "achi_svd_batched": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, dp, dp]),
+        "achi_svd_batched_device": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                              C.c_void_p, P(C.c_int)]),
+        "achi_device_times": (C.c_int, [vp, C.c_int, C.c_int, dp]),
         "achi_bond_select": (C.c_int, [vp, P(DmrgConfig), C.c_int, dp, P(BondState),
                                        C.c_int, C.c_int, P(TraceRow), P(VisitRecord)]),
         "achi_eigs_lowest_dense": (C.c_int, [vp, C.c_int, dp, dp, d, C.c_int, dp, dp,

@@ -47,7 +47,10 @@ class Context:
             raise AchiError(rc, f"achi_ctx_create(device={device}) failed")
 
     def close(self):
+        """Destroy the context; chains created on it are closed first."""
         if self.h:
+            for ch in list(getattr(self, "_chains", ())):
+                ch.close()
             self.lib.achi_ctx_destroy(self.h)
             self.h = C.c_void_p()
 
@@ -69,6 +72,34 @@ class Context:
 
     def synchronize(self):
         self._check(self.lib.achi_synchronize(self.h))
+
+    def timer_start(self):
+        self._check(self.lib.achi_timer_start(self.h))
+
+    def timer_stop(self) -> float:
+        """Device milliseconds since timer_start (CUDA events on the context stream)."""
+        ms = C.c_double()
+        self._check(self.lib.achi_timer_stop(self.h, C.byref(ms)))
+        return ms.value
+
+    def device_times(self, enable=None, reset=False):
+        """Per-phase CUDA-event device time: dict phase -> (ms, work, launches)."""
+        out = np.zeros(9)
+        e = -1 if enable is None else int(bool(enable))
+        self._check(self.lib.achi_device_times(self.h, e, int(bool(reset)), _dp(out)))
+        names = ("matvec", "svd", "env")
+        return {k: dict(ms=out[i], work=out[3 + i], launches=int(out[6 + i]))
+                for i, k in enumerate(names)}
+
+    def svd_batched_device(self, d_a_ptr, batch, m, n, d_sigma_ptr):
+        """Device-pointer batched SVD (inputs resident in HBM); returns Jacobi sweeps."""
+        sw = C.c_int()
+        self._check(self.lib.achi_svd_batched_device(self.h, batch, m, n, C.c_void_p(d_a_ptr),
+                                                     C.c_void_p(d_sigma_ptr), C.byref(sw)))
+        return sw.value
+
+    def flush_l2(self, nbytes=256 << 20):
+        self._check(self.lib.achi_flush_l2(self.h, C.c_size_t(nbytes)))
 
     # ---- local kernels (host buffers) ----
     def apply_effective_hamiltonian(self, L, W1, W2, R, theta):
@@ -168,12 +199,18 @@ class Chain:
         self.ctx, self.spec, self.cfg = ctx, spec, cfg
         self.n = spec.n
         self.h = C.c_void_p()
+        if not ctx.h:
+            raise AchiError(21, "context is closed")
         ctx._check(ctx.lib.achi_chain_create(ctx.h, C.byref(spec), C.byref(cfg), C.byref(self.h)))
+        if not hasattr(ctx, "_chains"):
+            import weakref
+            ctx._chains = weakref.WeakSet()
+        ctx._chains.add(self)
 
     def close(self):
-        if self.h:
+        if self.h and self.ctx.h:
             self.ctx.lib.achi_chain_destroy(self.h)
-            self.h = C.c_void_p()
+        self.h = C.c_void_p()
 
     def __del__(self):
         try:
@@ -214,6 +251,16 @@ class Chain:
             trace=[trace[i] for i in range(ns * 2 * (n - 1))],
             visits=[visits[i] for i in range(ns * 2 * (n - 1))],
             bond_dims=self.bond_dims())
+
+    def stats(self, profile=None):
+        """Phase wall-clock split since creation; profile=True syncs per visit."""
+        out = np.zeros(8)
+        p = -1 if profile is None else int(bool(profile))
+        if p < 0:
+            p = 0
+        self.ctx.lib.achi_chain_stats(self.h, p, _dp(out))
+        keys = ("lanczos_s", "svd_s", "select_s", "absorb_env_s", "matvecs", "svd_sweeps", "visits")
+        return dict(zip(keys, out[:7].tolist()))
 
     def bond_dims(self):
         d = np.zeros(self.n - 1, np.int32)

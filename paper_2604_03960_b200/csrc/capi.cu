@@ -91,6 +91,55 @@ int achi_synchronize(achi_ctx* ctx) {
   return guard(ctx, [&] { ctx->c.sync(); });
 }
 
+int achi_timer_start(achi_ctx* ctx) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    if (!c.ev0) {
+      ACHI_CUDA(cudaEventCreate(&c.ev0));
+      ACHI_CUDA(cudaEventCreate(&c.ev1));
+    }
+    c.sync();
+    ACHI_CUDA(cudaEventRecord(c.ev0, c.stream));
+  });
+}
+
+int achi_timer_stop(achi_ctx* ctx, double* ms) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    ACHI_CUDA(cudaEventRecord(c.ev1, c.stream));
+    ACHI_CUDA(cudaEventSynchronize(c.ev1));
+    float f = 0;
+    ACHI_CUDA(cudaEventElapsedTime(&f, c.ev0, c.ev1));
+    *ms = f;
+  });
+}
+
+int achi_flush_l2(achi_ctx* ctx, size_t bytes) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    const size_t n = bytes / sizeof(double);
+    c.flush.reserve(n);
+    ACHI_CUDA(cudaMemsetAsync(c.flush.p, 0, n * sizeof(double), c.stream));
+  });
+}
+
+int achi_device_times(achi_ctx* ctx, int enable, int reset, double* out9) {
+  return guard(ctx, [&] {
+    EventAcc& a = ctx->c.acc;
+    ctx->c.sync();
+    a.resolve();
+    if (out9)
+      for (int t = 0; t < EventAcc::kNumTags; ++t) {
+        out9[t] = a.ms[t];
+        out9[3 + t] = a.work[t];
+        out9[6 + t] = static_cast<double>(a.count[t]);
+      }
+    if (reset)
+      for (int t = 0; t < EventAcc::kNumTags; ++t) a.ms[t] = a.work[t] = 0, a.count[t] = 0;
+    if (enable >= 0) a.enabled = enable != 0;
+  });
+}
+
 // ---- chain ----
 int achi_chain_create(achi_ctx* ctx, const achi_model_spec* spec, const achi_dmrg_config* cfg,
                       achi_chain** out) {
@@ -104,7 +153,7 @@ int achi_chain_create(achi_ctx* ctx, const achi_model_spec* spec, const achi_dmr
 
 int achi_chain_destroy(achi_chain* chain) {
   if (chain) {
-    chain->ch.ctx->sync();
+    cudaStreamSynchronize(chain->ch.ctx->stream);
     delete chain;
   }
   return ACHI_OK;
@@ -157,6 +206,22 @@ int achi_chain_run(achi_chain* chain, achi_dmrg_result* result, achi_sweep_recor
     res.energy = prev;
     if (result) *result = res;
   });
+}
+
+int achi_chain_stats(achi_chain* chain, int profile, double* out8) {
+  Chain& ch = chain->ch;
+  ch.profile = profile != 0;
+  if (out8) {
+    out8[0] = ch.stats.merge_lanczos;
+    out8[1] = ch.stats.svd;
+    out8[2] = ch.stats.select;
+    out8[3] = ch.stats.absorb_env;
+    out8[4] = static_cast<double>(ch.stats.matvecs);
+    out8[5] = static_cast<double>(ch.stats.svd_sweeps);
+    out8[6] = static_cast<double>(ch.stats.visits);
+    out8[7] = 0;
+  }
+  return ACHI_OK;
 }
 
 int achi_chain_bond_dims(const achi_chain* chain, int32_t* dims) {
@@ -331,6 +396,17 @@ int achi_svd_batched(achi_ctx* ctx, int batch, int m, int n, const double* a, do
     svd_device(c, ws, dA.p, m, n, m, n, m <= n ? SvdSide::kRows : SvdSide::kCols, batch, mn, dS.p);
     d2h(c, sigma, dS.p, static_cast<size_t>(k) * batch);
     c.sync();
+  });
+}
+
+int achi_svd_batched_device(achi_ctx* ctx, int batch, int m, int n, const double* d_a,
+                            double* d_sigma, int* sweeps_out) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    static thread_local SvdWs ws;  // reused across benchmark calls (no realloc per call)
+    SvdResultDev r = svd_device(c, ws, d_a, m, n, m, n, m <= n ? SvdSide::kRows : SvdSide::kCols,
+                                batch, static_cast<long>(m) * n, d_sigma);
+    if (sweeps_out) *sweeps_out = r.sweeps;
   });
 }
 

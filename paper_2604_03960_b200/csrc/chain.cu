@@ -215,22 +215,41 @@ void Chain::rebuild_envs() {  // Environment::rebuild(psi, mpo, 0), dmrg.cpp:51-
 // visit_bond (dmrg.cpp:84-171)
 void Chain::visit(int b, bool right, int sweep_index, int slot) {
   Ctx& c = *ctx;
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   const int chl = chi[b], chm = chi[b + 1], chr = chi[b + 2];
   const int chlp = pad2i(chl), chmp = pad2i(chm), chrp = pad2i(chr);
   const long nvec = static_cast<long>(chlp) * d * d * chrp;
   const long dim = static_cast<long>(chl) * d * d * chr;
   theta_merge(c, site[b].p, site[b + 1].p, chlp, chmp, chrp, d, theta.p);
   HeffOps op{L[b].p, R[b + 1].p, chlp, chrp, d, mpo[b].l, mpo[b + 1].r, mheff[b]};
+  // algorithmic FP64 flops of one matvec: 2 D d^2 chl chr (chl+chr) + 4 D^2 d^3 chl chr
+  const double D = mpo[b].r;
+  const double mv_flops = 2.0 * D * d * d * chl * chr * (chl + chr) + 4.0 * D * D * d * d * d * chl * chr;
   EigsOut eig = eigs_lowest(
-      c, lz, [&](const double* in, double* out) { heff_apply(c, op, in, out); }, nvec, dim,
-      theta.p, cfg.eig_tol, cfg.eig_max_iter, vec.p);
+      c, lz,
+      [&](const double* in, double* out) {
+        c.acc.begin(EventAcc::kMatvec, c.stream);
+        heff_apply(c, op, in, out);
+        c.acc.end(c.stream, mv_flops);
+      },
+      nvec, dim, theta.p, cfg.eig_tol, cfg.eig_max_iter, vec.p);
+  const auto t1 = clk::now();
   const SvdSide side = right ? SvdSide::kRows : SvdSide::kCols;
+  c.acc.begin(EventAcc::kSvd, c.stream);
   SvdResultDev sr = svd_device(c, svd, vec.p, chlp * d, d * chrp, chl * d, d * chr, side);
+  // algorithmic bytes: 16 (m n + n^2) per Jacobi sweep (read+write G and V)
+  c.acc.end(c.stream, 16.0 * sr.sweeps *
+                          (static_cast<double>(sr.mg) * sr.ng + static_cast<double>(sr.ng) * sr.ng));
+  c.sync();
+  c.acc.resolve();
+  const auto t2 = clk::now();
   bond_select(c, sr.sigma, sr.r_true, cfg, states.p, b, sweep_index, right ? 1 : 0,
               trace.p + slot, visits.p + slot, bout.p);
   ACHI_CUDA(cudaMemcpyAsync(bout_h.p, bout.p, sizeof(BondOut), cudaMemcpyDeviceToHost, c.stream));
   c.sync();
   const BondOut bo = *bout_h.p;
+  const auto t3 = clk::now();
   if (bo.err == ACHI_E_DEGENERATE_SPECTRUM) fail(bo.err, "dmrg: zero two-site block");
   if (bo.err) fail(bo.err, "controller_update: invalid controller state or config");
   const int kept = bo.kept;
@@ -239,12 +258,27 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   absorb(c, sr, svd.sign.p, kept, bout.p, chl, chr, d, right, site[b].p, site[b + 1].p);
   chi[b + 1] = kept;
   const int kp = pad2i(kept);
-  if (right)
-    env_left(c, L[b].p, site[b].p, chlp, kp, d, mpo[b].l, mpo[b].r, mleft[b], L[b + 1].p);
-  else
-    env_right(c, R[b + 1].p, site[b + 1].p, chrp, kp, d, mpo[b + 1].l, mpo[b + 1].r,
-              mright[b + 1], R[b].p);
+  {
+    const double De = right ? mpo[b].r : mpo[b + 1].l, ch0 = right ? chl : chr;
+    c.acc.begin(EventAcc::kEnv, c.stream);
+    if (right)
+      env_left(c, L[b].p, site[b].p, chlp, kp, d, mpo[b].l, mpo[b].r, mleft[b], L[b + 1].p);
+    else
+      env_right(c, R[b + 1].p, site[b + 1].p, chrp, kp, d, mpo[b + 1].l, mpo[b + 1].r,
+                mright[b + 1], R[b].p);
+    c.acc.end(c.stream, 2.0 * De * d * ch0 * kept * (ch0 + kept) + 2.0 * De * De * d * d * ch0 * kept);
+  }
   vh[slot] = VisitHost{eig.eigenvalue, eig.residual, eig.matvecs};
+  if (profile) c.sync();
+  const auto t4 = clk::now();
+  auto sec = [](auto a, auto z) { return std::chrono::duration<double>(z - a).count(); };
+  stats.merge_lanczos += sec(t0, t1);
+  stats.svd += sec(t1, t2);
+  stats.select += sec(t2, t3);
+  stats.absorb_env += sec(t3, t4);
+  stats.matvecs += eig.matvecs;
+  stats.svd_sweeps += sr.sweeps;
+  stats.visits += 1;
 }
 
 // two_site_sweep (dmrg.cpp:175-214)
@@ -257,6 +291,7 @@ void Chain::sweep(int sweep_index, achi_sweep_record* rec, int32_t* chi_profile,
   for (int b = 0; b <= n - 2; ++b) visit(b, true, sweep_index, slot++);
   for (int b = n - 2; b >= 0; --b) visit(b, false, sweep_index, slot++);
   c.sync();
+  c.acc.resolve();
   auto t1 = std::chrono::steady_clock::now();
   const int nv = 2 * (n - 1);
   std::vector<achi_visit_record> vr(nv);

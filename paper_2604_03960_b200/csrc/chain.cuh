@@ -47,6 +47,12 @@ struct Chain {
   LanczosWs lz;
   SvdWs svd;
   std::vector<VisitHost> vh;
+  // phase wall-clock accounting (host steady_clock at the existing sync points)
+  struct Stats {
+    double merge_lanczos = 0, svd = 0, select = 0, absorb_env = 0;
+    long matvecs = 0, svd_sweeps = 0, visits = 0;
+  } stats;
+  bool profile = false;  // sync after each visit so phase times are exact
   // run-level bookkeeping (dmrg.cpp:255-281)
   double prev_energy = 0;
   bool have_prev = false;

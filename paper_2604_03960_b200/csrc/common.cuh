@@ -116,7 +116,53 @@ struct LanczosStatus {
   int32_t flags, pad;
 };
 
+// Device-time accounting: event pairs recorded on the context stream around a
+// phase, resolved (after a sync the caller already pays) into per-tag totals.
+struct EventAcc {
+  enum Tag { kMatvec = 0, kSvd = 1, kEnv = 2, kNumTags = 3 };
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<int, int>> open;  // (tag, index of start event)
+  size_t used = 0;
+  double ms[kNumTags] = {0, 0, 0};
+  double work[kNumTags] = {0, 0, 0};  // algorithmic flops or bytes
+  long count[kNumTags] = {0, 0, 0};
+  bool enabled = false;
+  cudaEvent_t next() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void begin(int tag, cudaStream_t s) {
+    if (!enabled) return;
+    const int i = static_cast<int>(used);
+    cudaEventRecord(next(), s);
+    open.emplace_back(tag, i);
+  }
+  void end(cudaStream_t s, double w) {
+    if (!enabled) return;
+    cudaEventRecord(next(), s);
+    work[open.back().first] += w;
+    count[open.back().first] += 1;
+  }
+  // call after a stream sync: fold all closed pairs into the totals
+  void resolve() {
+    for (auto& [tag, i] : open) {
+      float f = 0;
+      if (cudaEventElapsedTime(&f, pool[i], pool[i + 1]) == cudaSuccess) ms[tag] += f;
+    }
+    open.clear();
+    used = 0;
+  }
+  ~EventAcc() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
 struct Ctx {
+  EventAcc acc;
   int device = 0;
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
@@ -129,6 +175,8 @@ struct Ctx {
   DevBuf small;                        // small device scalars (h coefficients, s vector, ...)
   PinnedArr<double> host_small;
   PinnedArr<LanczosStatus> status;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  DevBuf flush;
   void sync() { ACHI_CUDA(cudaStreamSynchronize(stream)); }
 };
 
