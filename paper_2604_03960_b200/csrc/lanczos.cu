@@ -33,51 +33,67 @@ __device__ double block_sum(double v, double* sh) {
   return r;
 }
 
-__device__ __forceinline__ void chunk_of(long n, long& begin, long& end) {
-  const long chunk = (n + gridDim.x - 1) / gridDim.x;
-  begin = blockIdx.x * chunk;
-  end = min(n, begin + chunk);
-}
+constexpr int EPT = 4;                      // elements per thread
+constexpr int CHUNK = RED_THREADS * EPT;    // elements per block (fixed: deterministic)
 
-// partials[b * ld + v] = sum_{x in chunk b} Q_v[x] * w[x] for v < nv; plus w.w at v = nv if self
+// partials[b * ld + v] = sum_{x in chunk b} Q_v[x] * w[x] for v < nv; plus w.w at v = nv if self.
+// One warp-shuffle reduction per vector and a single __syncthreads per block.
 __global__ void __launch_bounds__(RED_THREADS) multi_dot_kernel(const double* __restrict__ Q, long stride,
                                                                 int nv, const double* __restrict__ w,
                                                                 long n, double* __restrict__ partials,
                                                                 int ld, int self) {
-  __shared__ double sh[32];
-  long b0, b1;
-  chunk_of(n, b0, b1);
-  for (int v0 = 0; v0 < nv + self; v0 += DOT_GROUP) {
+  __shared__ double sh[RED_THREADS / 32][65];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long base = static_cast<long>(blockIdx.x) * CHUNK + threadIdx.x;
+  double wx[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const long x = base + e * RED_THREADS;
+    wx[e] = x < n ? w[x] : 0.0;
+  }
+  const int nt = nv + self;
+  for (int v0 = 0; v0 < nt; v0 += DOT_GROUP) {
     double acc[DOT_GROUP];
-#pragma unroll
-    for (int g = 0; g < DOT_GROUP; ++g) acc[g] = 0.0;
-    for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
-      const double wx = w[x];
-#pragma unroll
-      for (int g = 0; g < DOT_GROUP; ++g) {
-        const int v = v0 + g;
-        if (v < nv) acc[g] += Q[v * stride + x] * wx;
-        else if (v == nv && self) acc[g] += wx * wx;
-      }
-    }
 #pragma unroll
     for (int g = 0; g < DOT_GROUP; ++g) {
       const int v = v0 + g;
-      if (v >= nv + self) break;
-      const double s = block_sum(acc[g], sh);
-      if (threadIdx.x == 0) partials[static_cast<long>(blockIdx.x) * ld + v] = s;
+      double a = 0.0;
+      if (v < nv) {
+        const double* q = Q + v * stride;
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          const long x = base + e * RED_THREADS;
+          if (x < n) a += q[x] * wx[e];
+        }
+      } else if (v == nv && self) {
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) a += wx[e] * wx[e];
+      }
+      acc[g] = warp_sum(a);
     }
+    if (lane == 0)
+#pragma unroll
+      for (int g = 0; g < DOT_GROUP; ++g)
+        if (v0 + g < nt) sh[warp][v0 + g] = acc[g];
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < nt; v += blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int w8 = 0; w8 < RED_THREADS / 32; ++w8) s += sh[w8][v];
+    partials[static_cast<long>(blockIdx.x) * ld + v] = s;
   }
 }
 
-// out[v] = sum_b partials[b * ld + v], fixed order, for v < nv
-__global__ void reduce_partials_kernel(const double* __restrict__ partials, int nblocks, int ld,
-                                       int nv, double* __restrict__ out) {
-  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nblocks; ++b) s += partials[static_cast<long>(b) * ld + v];
-    out[v] = s;
-  }
+// out[v] = sum_b partials[b * ld + v] (one block per v, fixed-order tree)
+__global__ void __launch_bounds__(RED_THREADS) reduce_partials_kernel(
+    const double* __restrict__ partials, int nblocks, int ld, int nv, double* __restrict__ out) {
+  __shared__ double sh[32];
+  const int v = blockIdx.x;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) s += partials[static_cast<long>(b) * ld + v];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) out[v] = s;
 }
 
 // dst[x] = src[x] + sign * sum_v coef[v] * Q_v[x]; partials[b] = sum_chunk dst^2
@@ -88,14 +104,30 @@ __global__ void __launch_bounds__(RED_THREADS) multi_axpy_kernel(
   __shared__ double sh[32];
   for (int v = threadIdx.x; v < nv; v += blockDim.x) c[v] = sign * coef[v];
   __syncthreads();
-  long b0, b1;
-  chunk_of(n, b0, b1);
+  const long base = static_cast<long>(blockIdx.x) * CHUNK + threadIdx.x;
+  double acc[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const long x = base + e * RED_THREADS;
+    acc[e] = (src && x < n) ? src[x] : 0.0;
+  }
+  for (int i = 0; i < nv; ++i) {
+    const double ci = c[i];
+    const double* q = Q + i * stride;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const long x = base + e * RED_THREADS;
+      if (x < n) acc[e] += ci * q[x];
+    }
+  }
   double nrm = 0.0;
-  for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
-    double v = src ? src[x] : 0.0;
-    for (int i = 0; i < nv; ++i) v += c[i] * Q[i * stride + x];
-    dst[x] = v;
-    nrm += v * v;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const long x = base + e * RED_THREADS;
+    if (x < n) {
+      dst[x] = acc[e];
+      nrm += acc[e] * acc[e];
+    }
   }
   if (partials) {
     const double s = block_sum(nrm, sh);
@@ -127,34 +159,17 @@ __device__ int sturm_count(const double* a, const double* b, int k, double x) {
   return cnt;
 }
 
-__device__ void tridiag_lowest_dev(const double* a, const double* b, int k, double* theta_out,
-                                   double* s) {
-  if (k == 1) {
-    *theta_out = a[0];
-    s[0] = 1.0;
-    return;
-  }
-  double lo = a[0], hi = a[0], scale = 0;
-  for (int i = 0; i < k; ++i) {
-    const double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i + 1 < k ? fabs(b[i]) : 0.0);
-    lo = fmin(lo, a[i] - r);
-    hi = fmax(hi, a[i] + r);
-    scale = fmax(scale, fabs(a[i]) + r);
-  }
-  for (int it = 0; it < 256; ++it) {
-    const double mid = 0.5 * (lo + hi);
-    if (mid <= lo || mid >= hi) break;
-    if (sturm_count(a, b, k, mid) >= 1) hi = mid; else lo = mid;
-  }
-  const double theta = hi;
-  *theta_out = theta;
-  // inverse iteration
+// Eigenvector of the k x k tridiagonal for the eigenvalue theta by inverse
+// iteration (partially pivoted elimination, dgtsv scheme), unit norm, first
+// nonzero component positive.
+__device__ void tridiag_vector_from_theta(const double* a, const double* b, int k, double theta,
+                                          double scale, double* s) {
   double dd[LANCZOS_BLOCK], du[LANCZOS_BLOCK], dl[LANCZOS_BLOCK], x[LANCZOS_BLOCK];
   const double tiny = (scale > 0 ? scale : 1.0) * 1e-300 + 1e-300;
   const double pivmin = (scale > 0 ? scale : 1.0) * 2.3e-16;
   // generic deterministic start (a symmetric start can be an exact eigenvector)
   for (int i = 0; i < k; ++i) x[i] = 1.0 + 0.5 * sin(1.0 + 2.3 * i);
-  for (int iter = 0; iter < 3; ++iter) {
+  for (int iter = 0; iter < 2; ++iter) {
     for (int i = 0; i < k; ++i) dd[i] = a[i] - theta;
     for (int i = 0; i + 1 < k; ++i) dl[i] = du[i] = b[i];
     for (int i = 0; i + 1 < k; ++i) {
@@ -198,24 +213,74 @@ __device__ void tridiag_lowest_dev(const double* a, const double* b, int k, doub
   for (int i = 0; i < k; ++i) s[i] = sg * x[i];
 }
 
+// Warp version: 32-point multisection on Sturm counts (one point per lane,
+// ~11 rounds to machine precision instead of ~60 serial bisection steps),
+// then inverse iteration on lane 0.  Called by all 32 lanes of one warp.
+__device__ void tridiag_lowest_warp(const double* a, const double* b, int k, double* theta_out,
+                                    double* s) {
+  const int lane = threadIdx.x & 31;
+  if (k == 1) {
+    if (lane == 0) {
+      *theta_out = a[0];
+      s[0] = 1.0;
+    }
+    return;
+  }
+  double lo = INFINITY, hi = -INFINITY, scale = 0.0;
+  for (int i = lane; i < k; i += 32) {
+    const double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i + 1 < k ? fabs(b[i]) : 0.0);
+    lo = fmin(lo, a[i] - r);
+    hi = fmax(hi, a[i] + r);
+    scale = fmax(scale, fabs(a[i]) + r);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
+  }
+  for (int round = 0; round < 40; ++round) {
+    const double w = hi - lo;
+    if (!(w > 2.3e-16 * fmax(fabs(lo), fabs(hi)))) break;
+    const double x = lo + (lane + 1) * (w / 33.0);
+    const unsigned has = __ballot_sync(0xffffffffu, sturm_count(a, b, k, x) >= 1);
+    const double nlo = has == 0u ? __shfl_sync(0xffffffffu, x, 31)
+                                 : (__ffs(has) >= 2 ? __shfl_sync(0xffffffffu, x, __ffs(has) - 2) : lo);
+    const double nhi = has == 0u ? hi : __shfl_sync(0xffffffffu, x, __ffs(has) - 1);
+    if (nlo == lo && nhi == hi) break;
+    lo = nlo;
+    hi = nhi;
+  }
+  if (lane == 0) {
+    tridiag_vector_from_theta(a, b, k, hi, scale, s);
+    *theta_out = hi;
+  }
+}
+
 // After CGS2: alpha[j] = h1[j]; beta[j] = sqrt(sum partials); tridiagonal solve.
 __global__ void __launch_bounds__(RED_THREADS) finish_step_kernel(
     const double* __restrict__ partials, int nblocks, double* alpha, double* beta,
     const double* h1, double* s, int j, LanczosStatus* st) {
   __shared__ double sh[32];
+  __shared__ double bn_s;
   double v = 0.0;
   for (int b = threadIdx.x; b < nblocks; b += blockDim.x) v += partials[b];
   v = block_sum(v, sh);
   if (threadIdx.x == 0) {
-    const double bn = sqrt(v);
+    bn_s = sqrt(v);
     alpha[j] = h1[j];
-    beta[j] = bn;
+    beta[j] = bn_s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
     double theta;
-    tridiag_lowest_dev(alpha, beta, j + 1, &theta, s);
-    st->theta = theta;
-    st->bnorm = bn;
-    st->alpha = alpha[j];
-    st->res_bound = bn * fabs(s[j]);
+    tridiag_lowest_warp(alpha, beta, j + 1, &theta, s);
+    if (threadIdx.x == 0) {
+      st->theta = theta;
+      st->bnorm = bn_s;
+      st->alpha = alpha[j];
+      st->res_bound = bn_s * fabs(s[j]);
+    }
   }
 }
 
@@ -245,9 +310,7 @@ __global__ void __launch_bounds__(RED_THREADS) residual_kernel(const double* __r
   }
 }
 
-int red_blocks(const Ctx& ctx, long n) {
-  return static_cast<int>(std::max<long>(1, std::min<long>(cdiv(n, RED_THREADS * 4), 2L * ctx.num_sms)));
-}
+int red_blocks(const Ctx&, long n) { return std::max(1, cdiv(n, CHUNK)); }
 
 struct Kernels {
   Ctx& ctx;
@@ -258,7 +321,7 @@ struct Kernels {
   void dots(const double* Q, int nv, const double* w, double* h) {
     multi_dot_kernel<<<nb, RED_THREADS, 0, ctx.stream>>>(Q, ws.stride, nv, w, n, ws.partials.p, 64, 0);
     ACHI_LAUNCHED(ctx);
-    reduce_partials_kernel<<<1, 64, 0, ctx.stream>>>(ws.partials.p, nb, 64, nv, h);
+    reduce_partials_kernel<<<nv, RED_THREADS, 0, ctx.stream>>>(ws.partials.p, nb, 64, nv, h);
     ACHI_LAUNCHED(ctx);
   }
   // dst = src + sign * Q c ; norm partials -> ws.partials (first nb entries)
@@ -298,7 +361,7 @@ void LanczosWs::reserve(long n) {
     ritz.reserve(s);
     tmp.reserve(s);
   }
-  partials.reserve(64L * 2 * 148 * 4 + 1024);
+  partials.reserve(64L * cdiv(s, CHUNK) + 1024);
   scal.reserve(512);
 }
 
@@ -307,7 +370,7 @@ void device_norm2(Ctx& ctx, const double* x, long n, double* result) {
   double* part = ctx.red.reserve(static_cast<size_t>(nb) * 2 + 8);
   multi_dot_kernel<<<nb, RED_THREADS, 0, ctx.stream>>>(x, 0, 0, x, n, part, 1, 1);
   ACHI_LAUNCHED(ctx);
-  reduce_partials_kernel<<<1, 32, 0, ctx.stream>>>(part, nb, 1, 1, result);
+  reduce_partials_kernel<<<1, RED_THREADS, 0, ctx.stream>>>(part, nb, 1, 1, result);
   ACHI_LAUNCHED(ctx);
 }
 

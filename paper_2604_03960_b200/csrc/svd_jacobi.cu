@@ -60,6 +60,7 @@ struct JacobiSmem {
   double J[JW][SLD];
   double cs[16][2];
   double red[JT / 32];
+  double ath;
   int changed;
 };
 
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(RoundArgs a) {
   if (!(sm.red[0] > a.tol)) return;  // pair already orthogonal
 
   // ---- two-sided cyclic Jacobi on S, accumulating J ----
-  for (int sweep = 0; sweep < 12; ++sweep) {
+  for (int sweep = 0; sweep < 6; ++sweep) {
     if (threadIdx.x == 0) sm.changed = 0;
     __syncthreads();
     for (int step = 0; step < JW - 1; ++step) {
@@ -280,7 +281,10 @@ __global__ void zero_floor_kernel(const double* __restrict__ G, long gstride, lo
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < (blockDim.x >> 5); ++w) t += sh[w];
-    const double f = sqrt(static_cast<double>(mg)) * EPS;
+    // columns below 64 sqrt(mg) eps ||G||_F are rounding noise (a rank-deficient
+    // theta leaves such columns; their direction is undefined and their norm is
+    // below the reference's own normwise accuracy): they are not rotated
+    const double f = 64.0 * sqrt(static_cast<double>(mg)) * EPS;
     zero2[blockIdx.x] = f * f * t;
   }
 }
