@@ -379,7 +379,7 @@ int achi_svd(achi_ctx* ctx, int m, int n, const double* a, double* sigma, double
     if (u) d2h(c, u, dU.p, static_cast<size_t>(m) * k);
     if (vt) d2h(c, vt, dV.p, static_cast<size_t>(k) * n);
     c.sync();
-    if (sweeps_out) *sweeps_out = r.sweeps;
+    if (sweeps_out) *sweeps_out = r.sweeps();
   });
 }
 
@@ -406,7 +406,8 @@ int achi_svd_batched_device(achi_ctx* ctx, int batch, int m, int n, const double
     static thread_local SvdWs ws;  // reused across benchmark calls (no realloc per call)
     SvdResultDev r = svd_device(c, ws, d_a, m, n, m, n, m <= n ? SvdSide::kRows : SvdSide::kCols,
                                 batch, static_cast<long>(m) * n, d_sigma);
-    if (sweeps_out) *sweeps_out = r.sweeps;
+    c.sync();
+    if (sweeps_out) *sweeps_out = r.sweeps();
   });
 }
 

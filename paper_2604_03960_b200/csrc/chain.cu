@@ -238,11 +238,14 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   const SvdSide side = right ? SvdSide::kRows : SvdSide::kCols;
   c.acc.begin(EventAcc::kSvd, c.stream);
   SvdResultDev sr = svd_device(c, svd, vec.p, chlp * d, d * chrp, chl * d, d * chr, side);
-  // algorithmic bytes (SURVEY.md §8d): 16 (m n + n^2) per Jacobi sweep (read+write G and V)
-  c.acc.end(c.stream, 16.0 * sr.sweeps *
-                          (static_cast<double>(sr.mg) * sr.ng + static_cast<double>(sr.ng) * sr.ng));
+  c.acc.end(c.stream, 0.0);
   c.sync();
   c.acc.resolve();
+  const int svd_sweeps = sr.sweeps();
+  // algorithmic bytes (SURVEY.md §8d): 16 (m n + n^2) per Jacobi sweep (read+write G and V)
+  if (c.acc.enabled)
+    c.acc.work[EventAcc::kSvd] +=
+        16.0 * svd_sweeps * (static_cast<double>(sr.mg) * sr.ng + static_cast<double>(sr.ng) * sr.ng);
   const auto t2 = clk::now();
   bond_select(c, sr.sigma, sr.r_true, cfg, states.p, b, sweep_index, right ? 1 : 0,
               trace.p + slot, visits.p + slot, bout.p);
@@ -277,7 +280,7 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   stats.select += sec(t2, t3);
   stats.absorb_env += sec(t3, t4);
   stats.matvecs += eig.matvecs;
-  stats.svd_sweeps += sr.sweeps;
+  stats.svd_sweeps += svd_sweeps;
   stats.visits += 1;
 }
 

@@ -19,7 +19,8 @@ struct SvdWs {
   DevArr<int> perm;
   DevArr<double> sign;
   DevArr<unsigned long long> conv;
-  PinnedArr<unsigned long long> conv_host;
+  DevArr<int> sweeps;
+  PinnedArr<int> sweeps_host;
 };
 
 // Orientation: kRows -> columns of G are the rows of theta (G = theta^T, V
@@ -33,11 +34,15 @@ struct SvdResultDev {
   int m_true, n_true;
   int ng, mg;        // working matrix columns/rows (ng padded to a multiple of 32)
   int r_true;        // min(m_true, n_true)
-  int sweeps;
-  const double* G;   // mg x ng col-major (ld = mg)
+  const int* sweeps_host;  // per cooperative launch; valid after the next stream sync
+  int n_launches;
+  const double* G;   // mg x ng col-major (ld = mg, rows >= the true row count are zero)
   const double* V;   // ng x ng col-major (ld = ng)
   const double* sigma;  // sorted, r_true entries valid (device)
   const int* perm;      // perm[k] = working column of the k-th singular value
+  // Jacobi sweeps used (max over launches); call after a stream sync.  Throws
+  // NumericalFailure if the iteration hit its sweep cap (linalg.cpp:39-40).
+  int sweeps() const;
 };
 
 // SVD of theta (m x n row-major, ld = n, padded; true dims m_true x n_true).
