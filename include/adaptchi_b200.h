@@ -255,6 +255,12 @@ int achi_bond_select(achi_ctx* ctx, const achi_dmrg_config* cfg, int n_sigma,
 int achi_dgemm(achi_ctx* ctx, int M, int N, int K, int a_kmajor, const double* a, long lda,
                int b_kmajor, const double* b, long ldb, double* c, long ldc);
 
+/* Device-resident timing hook for K1: `reps` applications of the effective
+ * Hamiltonian at chl = chr = chi (XXZ bulk MPO, D = 5) on pseudo-random
+ * device data; returns the average device ms per matvec and the achieved
+ * algorithmic TFLOP/s (2 D d^2 chi^2 (2 chi) + 4 D^2 d^3 chi^2 flops). */
+int achi_heff_bench(achi_ctx* ctx, int chi, int reps, double* ms_per_matvec, double* tflops);
+
 /* eigs_lowest (linalg.cpp:107-178) with a dense symmetric operator (test
  * hook for the device Lanczos): h is dim x dim row-major. */
 int achi_eigs_lowest_dense(achi_ctx* ctx, int dim, const double* h,

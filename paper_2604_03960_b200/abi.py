@@ -179,5 +179,12 @@ def load():
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
         f.restype, f.argtypes = res, args
+    _late_signatures(lib)
     _lib = lib
     return lib
+
+
+def _late_signatures(lib):
+    P = C.POINTER
+    lib.achi_heff_bench.restype = C.c_int
+    lib.achi_heff_bench.argtypes = [C.c_void_p, C.c_int, C.c_int, P(C.c_double), P(C.c_double)]

@@ -290,3 +290,10 @@ class Chain:
         flat = [np.ascontiguousarray(s, dtype=np.float64) for s in sites]
         ptrs = (C.POINTER(C.c_double) * len(flat))(*[_dp(a) for a in flat])
         self.ctx._check(self.ctx.lib.achi_chain_load_state(self.h, _ip(dims), ptrs))
+
+
+def heff_bench(ctx: Context, chi: int, reps: int = 20):
+    """Device-resident H_eff timing at chl = chr = chi: (ms per matvec, TFLOP/s)."""
+    ms, tf = C.c_double(), C.c_double()
+    ctx._check(ctx.lib.achi_heff_bench(ctx.h, chi, reps, C.byref(ms), C.byref(tf)))
+    return ms.value, tf.value

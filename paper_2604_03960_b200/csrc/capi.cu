@@ -36,6 +36,23 @@ __global__ void dense_gemv_kernel(const double* __restrict__ h, int dim, const d
   if (lane == 0) y[row] = s;
 }
 
+// deterministic pseudo-random fill in [-1, 1) (splitmix64), for timing hooks
+__global__ void fill_random_kernel(double* p, size_t n, unsigned long long seed) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    unsigned long long z = (i + 1) * 0x9E3779B97F4A7C15ull + seed * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    p[i] = static_cast<double>(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+  }
+}
+
+void fill_random(Ctx& c, double* p, size_t n, unsigned long long seed) {
+  fill_random_kernel<<<4 * c.num_sms, 256, 0, c.stream>>>(p, n, seed);
+  ACHI_LAUNCHED(c);
+}
+
 HostMpo host_mpo(const double* w, int l, int d, int r) {
   HostMpo m{l, d, r, std::vector<double>(w, w + static_cast<size_t>(l) * d * d * r)};
   return m;
@@ -464,6 +481,39 @@ int achi_dgemm(achi_ctx* ctx, int M, int N, int K, int a_kmajor, const double* a
          Operand{dB.p, ldb, b_kmajor ? Major::kK : Major::kMN}, dC.p, ldc);
     d2h(cx, c, dC.p, nc);
     cx.sync();
+  });
+}
+
+int achi_heff_bench(achi_ctx* ctx, int chi, int reps, double* ms_per_matvec, double* tflops) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    const int cp = pad2i(chi), d = 2, D = 5;
+    achi_model_spec spec{ACHI_HEISENBERG_XXZ, 4, 1.0, 1.0, 1.0, 0.0, ACHI_SPIN_HALF, 0};
+    auto mpo = build_mpo_real(spec);
+    MixStore ms;
+    auto mix = ms.upload(c, {mix_heff(mpo[1], mpo[2])});
+    DevBuf dL, dR, dT, dO;
+    const size_t nenv = static_cast<size_t>(cp) * D * cp, nvec = static_cast<size_t>(cp) * d * d * cp;
+    fill_random(c, dL.reserve(nenv), nenv, 1);
+    fill_random(c, dR.reserve(nenv), nenv, 2);
+    fill_random(c, dT.reserve(nvec), nvec, 3);
+    dO.reserve(nvec);
+    HeffOps op{dL.p, dR.p, cp, cp, d, D, D, mix[0]};
+    heff_apply(c, op, dT.p, dO.p);  // warm-up (tensor maps, attributes)
+    cudaEvent_t e0, e1;
+    ACHI_CUDA(cudaEventCreate(&e0));
+    ACHI_CUDA(cudaEventCreate(&e1));
+    ACHI_CUDA(cudaEventRecord(e0, c.stream));
+    for (int r = 0; r < reps; ++r) heff_apply(c, op, dT.p, dO.p);
+    ACHI_CUDA(cudaEventRecord(e1, c.stream));
+    ACHI_CUDA(cudaEventSynchronize(e1));
+    float f = 0;
+    ACHI_CUDA(cudaEventElapsedTime(&f, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double x = chi, flops = 2.0 * D * d * d * x * x * (2 * x) + 4.0 * D * D * d * d * d * x * x;
+    *ms_per_matvec = f / reps;
+    *tflops = flops / (*ms_per_matvec * 1e-3) / 1e12;
   });
 }
 
