@@ -239,6 +239,15 @@ def run_ours(args, dist):
     if not args.skip_svd:
         log("svd part")
         out.update(svd_part(ctx, args))
+    # K1 at the large-chi end of the metric's range (chi_max = 1024): device-resident H_eff
+    from paper_2604_03960_b200.api import heff_bench
+    ms, tf = heff_bench(ctx, 1024, 10)
+    out["roofline_heff_chi1024"] = {
+        "bound": "tensor", "kernel": "H_eff matvec (dmma_gemm_kernel x2 + mpo_mix_kernel)",
+        "achieved": round(tf, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+        "frac": round(tf / FP64_PEAK_TFLOPS, 4), "ms_per_matvec": round(ms, 4),
+        "work_def": "2*D*d^2*chi^2*(2*chi)+4*D^2*d^3*chi^2 flops, chi=1024, D=5, d=2",
+        "peak_source": "measured DMMA peak (profiles/fp64_peak_r01.txt)"}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         log("cpu baseline")
         out["cpu_baseline"] = cpu_baseline_sample(spec, cfg, ch, last)

@@ -1,0 +1,77 @@
+"""CPU tests of the multi-GPU sharding host logic (world_size 2, gloo backend).
+
+The GPU work of each unit is replaced by a deterministic CPU function; what is
+tested is the plan (every unit exactly once, deterministic, cost balanced) and
+the single end-of-job gather to rank 0.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2604_03960_b200 import ensemble
+
+
+def test_plans_cover_every_unit_once():
+    costs = [ensemble.chain_cost(j) for j in ensemble.xxz_ensemble(64)]
+    for world in (1, 2, 4, 8):
+        plan = ensemble.lpt_plan(costs, world)
+        flat = sorted(u for p in plan for u in p)
+        assert flat == list(range(64))
+        loads = [sum(costs[u] for u in p) for p in plan]
+        assert max(loads) <= 1.35 * (sum(costs) / world) + max(costs)
+        assert plan == ensemble.lpt_plan(costs, world)  # deterministic
+        rr = ensemble.round_robin_plan(64, world)
+        assert sorted(u for p in rr for u in p) == list(range(64))
+
+
+def test_critical_chains_cost_more():
+    assert ensemble.chain_cost(1.0) >= ensemble.chain_cost(0.5) > 0
+    assert ensemble.chain_cost(1.0) > ensemble.chain_cost(1.5) > ensemble.chain_cost(2.0)
+
+
+def fake_work(u):
+    return np.array([u * 0.5, u ** 2, -u])
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    costs = [ensemble.chain_cost(j) for j in ensemble.xxz_ensemble(10)]
+    out, plan = ensemble.run_sharded(10, costs, fake_work, 3, rank, world)
+    out2, _ = ensemble.run_sharded(7, None, fake_work, 3, rank, world)
+    if rank == 0:
+        q.put((out.tolist(), out2.tolist(), plan))
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_sharded_gather_world2_gloo():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out, out2, plan = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out, out2 = np.array(out), np.array(out2)
+    assert out.shape == (10, 3) and out2.shape == (7, 3)
+    for u in range(10):
+        assert np.array_equal(out[u], fake_work(u))
+    for u in range(7):
+        assert np.array_equal(out2[u], fake_work(u))
+    assert sorted(plan[0] + plan[1]) == list(range(10))
