@@ -1,9 +1,13 @@
 // Device Lanczos (see lanczos.cuh).  All reductions are deterministic: each
 // block owns a fixed contiguous chunk and partials are summed in fixed order.
+#include <cooperative_groups.h>
+
 #include <cmath>
 #include <limits>
 
 #include "lanczos.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace achi {
 
@@ -312,6 +316,136 @@ __global__ void __launch_bounds__(RED_THREADS) residual_kernel(const double* __r
 
 int red_blocks(const Ctx&, long n) { return std::max(1, cdiv(n, CHUNK)); }
 
+// ---- fused Lanczos step (one cooperative launch) --------------------------
+// After w = H q_j:  h1 = Q^T w (alpha_j = h1[j]);  w <- w - Q h1;  h2 = Q^T w;
+// w <- w - Q h2;  beta_j = ||w||;  tridiagonal lowest pair (warp 0 of block 0);
+// q_{j+1} = w / beta_j.  Classical Gram-Schmidt twice, equal to the reference's
+// MGS (linalg.cpp:131-135) to rounding.  Each block owns a fixed contiguous
+// chunk and every block reduces the per-block partials in the same fixed order,
+// so all blocks see bit-identical coefficients (deterministic).
+struct OrthArgs {
+  const double* Q;
+  long stride;
+  int nv;  // j + 1
+  double* w;
+  long n;
+  double* pa;  // [grid][64] partials of h1
+  double* pb;  // [grid][64] partials of h2
+  double* pc;  // [grid]     partials of ||w||^2
+  double* alpha;
+  double* beta;
+  double* s;
+  double* qnext;
+  LanczosStatus* st;
+  int j;
+};
+
+constexpr int ORTH_THREADS = 256;
+
+__device__ void orth_partials(const double* Q, long stride, int nv, const double* w, long b0,
+                              long b1, double* part, double (*sh)[65]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int v0 = 0; v0 < nv; v0 += DOT_GROUP) {
+    double acc[DOT_GROUP];
+#pragma unroll
+    for (int g = 0; g < DOT_GROUP; ++g) acc[g] = 0.0;
+    for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
+      const double wx = w[x];
+#pragma unroll
+      for (int g = 0; g < DOT_GROUP; ++g)
+        if (v0 + g < nv) acc[g] += Q[(v0 + g) * stride + x] * wx;
+    }
+#pragma unroll
+    for (int g = 0; g < DOT_GROUP; ++g) {
+      const double r = warp_sum(acc[g]);
+      if (lane == 0 && v0 + g < nv) sh[warp][v0 + g] = r;
+    }
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    double t = 0.0;
+#pragma unroll
+    for (int w8 = 0; w8 < ORTH_THREADS / 32; ++w8) t += sh[w8][v];
+    part[static_cast<long>(blockIdx.x) * 64 + v] = t;
+  }
+  __syncthreads();
+}
+
+// every block: coef[v] = sum_b part[b][v] in fixed order
+__device__ void orth_reduce(const double* part, int nv, double* coef) {
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    double t = 0.0;
+    for (int b = 0; b < static_cast<int>(gridDim.x); ++b) t += part[static_cast<long>(b) * 64 + v];
+    coef[v] = t;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) {
+  __shared__ double sh[ORTH_THREADS / 32][65];
+  __shared__ double coef[64];
+  __shared__ double red[32];
+  cg::grid_group grid = cg::this_grid();
+  const long chunk = (a.n + gridDim.x - 1) / gridDim.x;
+  const long b0 = static_cast<long>(blockIdx.x) * chunk, b1 = min(a.n, b0 + chunk);
+  // pass 1: h1 = Q^T w
+  orth_partials(a.Q, a.stride, a.nv, a.w, b0, b1, a.pa, sh);
+  grid.sync();
+  orth_reduce(a.pa, a.nv, coef);
+  // pass 2: w <- w - Q h1 ; h2 partials
+  for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
+    double v = a.w[x];
+    for (int i = 0; i < a.nv; ++i) v -= coef[i] * a.Q[i * a.stride + x];
+    a.w[x] = v;
+  }
+  __syncthreads();
+  orth_partials(a.Q, a.stride, a.nv, a.w, b0, b1, a.pb, sh);
+  const double alpha_j = coef[a.nv - 1];
+  grid.sync();
+  orth_reduce(a.pb, a.nv, coef);
+  // pass 3: w <- w - Q h2 ; ||w||^2 partials
+  double nrm = 0.0;
+  for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
+    double v = a.w[x];
+    for (int i = 0; i < a.nv; ++i) v -= coef[i] * a.Q[i * a.stride + x];
+    a.w[x] = v;
+    nrm += v * v;
+  }
+  nrm = block_sum(nrm, red);
+  if (threadIdx.x == 0) a.pc[blockIdx.x] = nrm;
+  grid.sync();
+  __shared__ double bn_s;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int b = 0; b < static_cast<int>(gridDim.x); ++b) t += a.pc[b];
+    bn_s = sqrt(t);
+  }
+  __syncthreads();
+  const double bn = bn_s;
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) {
+      a.alpha[a.j] = alpha_j;
+      a.beta[a.j] = bn;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double theta;
+      tridiag_lowest_warp(a.alpha, a.beta, a.j + 1, &theta, a.s);
+      if (threadIdx.x == 0) {
+        a.st->theta = theta;
+        a.st->bnorm = bn;
+        a.st->alpha = alpha_j;
+        a.st->res_bound = bn * fabs(a.s[a.j]);
+      }
+    }
+  }
+  // q_{j+1} = w / beta_j (unused when the step converges or breaks down)
+  if (a.qnext && bn > 0) {
+    const double inv = 1.0 / bn;
+    for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) a.qnext[x] = a.w[x] * inv;
+  }
+}
+
 struct Kernels {
   Ctx& ctx;
   LanczosWs& ws;
@@ -399,21 +533,34 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
   K.scale(ws.q(0), v0, misc + 3, true);
 
   const int block = static_cast<int>(std::min<long>(dim, LANCZOS_BLOCK));
+  static int orth_max = 0;
+  if (orth_max == 0) {
+    int per_sm = 0;
+    ACHI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lanczos_orth_kernel,
+                                                            ORTH_THREADS, 0));
+    orth_max = std::max(1, std::min(per_sm, 2)) * ctx.num_sms;
+  }
+  // fixed for a given n: the chunking (and so every reduction order) is deterministic
+  const int orth_grid = static_cast<int>(std::max<long>(1, std::min<long>(cdiv(n, 2048), orth_max)));
+  ws.partials.reserve(static_cast<size_t>(129) * orth_grid + 64);
   double best = std::numeric_limits<double>::infinity();
   int matvecs = 0;
   while (matvecs < max_iter) {
     for (int j = 0; j < block && matvecs < max_iter; ++j) {
       apply(ws.q(j), ws.w.p);
       ++matvecs;
-      // classical Gram-Schmidt, twice (h1[j] = alpha_j = q_j . H q_j)
-      K.dots(ws.q(0), j + 1, ws.w.p, ws.h1());
-      K.axpy(ws.q(0), j + 1, ws.h1(), -1.0, ws.w.p, ws.w.p, false);
-      K.dots(ws.q(0), j + 1, ws.w.p, ws.h2());
-      K.axpy(ws.q(0), j + 1, ws.h2(), -1.0, ws.w.p, ws.w.p, true);
-      finish_step_kernel<<<1, RED_THREADS, 0, ctx.stream>>>(ws.partials.p, K.nb, ws.alpha(),
-                                                            ws.beta(), ws.h1(), ws.s(), j,
-                                                            K.dev_status());
-      ACHI_LAUNCHED(ctx);
+      // classical Gram-Schmidt twice + tridiagonal Ritz pair + q_{j+1}, one launch
+      {
+        OrthArgs oa{ws.q(0), ws.stride, j + 1, ws.w.p, n,
+                    ws.partials.p, ws.partials.p + 64L * orth_grid,
+                    ws.partials.p + 128L * orth_grid, ws.alpha(), ws.beta(), ws.s(),
+                    j + 1 <= LANCZOS_BLOCK ? ws.q(j + 1) : nullptr, K.dev_status(), j};
+        void* args[] = {&oa};
+        ACHI_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lanczos_orth_kernel),
+                                              dim3(orth_grid), dim3(ORTH_THREADS), args, 0,
+                                              ctx.stream));
+        ACHI_LAUNCHED(ctx);
+      }
       const LanczosStatus st = K.read_status();
       const int k = j + 1;
       const double theta = st.theta, bnorm = st.bnorm;
@@ -451,8 +598,6 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
         }
         break;
       }
-      // q_{j+1} = w / beta_j
-      K.scale(ws.q(j + 1), ws.w.p, ws.beta() + j, true);
     }
   }
   Error e(ACHI_E_EIGEN_NONCONVERGENCE, "eigs_lowest: no convergence within max_iter");

@@ -6,6 +6,7 @@ profiles), FP64 rounding-level for contractions, and the north_star's
 1e-10 relative energy / 1e-11 relative (to sigma_1) singular values.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -292,3 +293,24 @@ def test_launch_counter_moves(ctx):
     ctx.apply_effective_hamiltonian(np.ones((2, 5, 2)), *[np.ones((5, 2, 2, 5))] * 2,
                                     np.ones((2, 5, 2)), np.ones((2, 2, 2, 2)))
     assert ctx.launches > before
+
+
+@pytest.mark.slow
+def test_dmrg_c3_headline_parity(ctx, oracle):
+    """Config C3 (the metric's workload): Heisenberg S=1/2 N=100, PID chi_max=1024,
+    eps_trunc=1e-10, 6 sweeps.  GPU vs the real-gauge oracle: energies 1e-10
+    relative, chi profile identical every sweep; any kept-rank divergence must
+    sit within rounding of the floor threshold (reported margin < 1e-6)."""
+    spec = abi.model_spec(100, convention=abi.SPIN_HALF)
+    cfg = abi.adaptive_config(1024, 1e-10, max_sweeps=6, eps_conv=1e-300)
+    oracle.set_threads(os.cpu_count() or 1)
+    g = ctx.run_dmrg(spec, cfg)
+    o = oracle.run_dmrg(spec, cfg)
+    assert g["n_sweeps"] == o["n_sweeps"] == 6
+    for a, b in zip(g["energies"], o["energies"]):
+        assert abs(a - b) <= 1e-10 * abs(b), (a, b)
+    diverged = [(vg.sweep, vg.bond, vg.kept, vo.kept, vg.floor_margin)
+                for vg, vo in zip(g["visits"], o["visits"]) if vg.kept != vo.kept]
+    assert all(m < 1e-6 for *_, m in diverged), diverged
+    if not diverged:
+        assert np.array_equal(g["chi_profiles"], o["chi_profiles"])
