@@ -541,7 +541,8 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
     orth_max = std::max(1, std::min(per_sm, 2)) * ctx.num_sms;
   }
   // fixed for a given n: the chunking (and so every reduction order) is deterministic
-  const int orth_grid = static_cast<int>(std::max<long>(1, std::min<long>(cdiv(n, 2048), orth_max)));
+  // (about one element per thread up to two CTAs per SM: the passes are latency-bound)
+  const int orth_grid = static_cast<int>(std::max<long>(1, std::min<long>(cdiv(n, ORTH_THREADS), orth_max)));
   ws.partials.reserve(static_cast<size_t>(129) * orth_grid + 64);
   double best = std::numeric_limits<double>::infinity();
   int matvecs = 0;

@@ -73,6 +73,7 @@ struct PersArgs {
   const double* zero2;
   unsigned long long* conv;  // [MAX_SWEEPS] per-sweep max measure (whole launch)
   int* sweeps_out;
+  long long* prof;  // optional clock64 phase accounting (CTA 0), null in production
 };
 
 struct Small {
@@ -160,7 +161,7 @@ __device__ __forceinline__ void rotate_chunk(Chunk& X, const Small& sm) {
 // Each parallel step rotates 16 disjoint pairs; the two-sided update splits
 // into 16x16 independent 2x2 blocks S[{ip,jp},{iq,jq}] <- Rp^T S Rq, one per
 // thread, so a step costs two barriers.  Pair tables are precomputed.
-__device__ void inner_jacobi(Small& sm, double z2, double tol, int max_inner) {
+__device__ void inner_jacobi(Small& sm, double z2, double inv_f2, double tol, int max_inner) {
   const int t = threadIdx.x;
   const int bp = t >> 4, bq = t & 15;  // this thread's 2x2 block of S
   for (int sweep = 0; sweep < max_inner; ++sweep) {
@@ -171,11 +172,25 @@ __device__ void inner_jacobi(Small& sm, double z2, double tol, int max_inner) {
         const int i = sm.pi[step][t], j = sm.pj[step][t];
         const double app = sm.S[i][i], aqq = sm.S[j][j], apq = sm.S[i][j];
         double c = 1.0, s = 0.0;
-        if (app > z2 && aqq > z2 && fabs(apq) > tol * sqrt(app * aqq)) {
-          const double tau = (aqq - app) / (2.0 * apq);
-          const double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          c = 1.0 / sqrt(1.0 + tt * tt);
-          s = tt * c;
+        // rotate iff |apq| > tol sqrt(app aqq).  The angle t = tan(theta) of the
+        // classical Jacobi rotation is computed in FP32 from the scale-free
+        // tau = (aqq - app) / (2 apq) (an approximate angle still gives an exactly
+        // orthogonal rotation; its error only leaves a ~1e-7 relative residue
+        // that later sweeps remove, preserving superlinear convergence); c and
+        // s = t c are then made orthonormal to FP64 precision by two Newton steps
+        // on rsqrt(1 + t^2).  Cuts the serial FP64 sqrt/div chain of every step.
+        if (app > z2 && aqq > z2 && apq * apq > tol * tol * (app * aqq)) {
+          const float zf = static_cast<float>((aqq - app) * inv_f2);
+          const float qf = static_cast<float>(2.0 * apq * inv_f2);
+          const float tau = __fdividef(zf, qf);
+          const float tf = copysignf(1.0f, tau) / (fabsf(tau) + sqrtf(fmaf(tau, tau, 1.0f)));
+          const double td = tf;
+          const double x = fma(td, td, 1.0);
+          double y = rsqrtf(static_cast<float>(x));
+          y = y * (1.5 - 0.5 * x * y * y);
+          y = y * (1.5 - 0.5 * x * y * y);
+          c = y;
+          s = td * y;
           sm.changed = 1;
         }
         sm.cs[t][0] = c;
@@ -233,7 +248,7 @@ __device__ void init_pair_tables(Small& sm) {
 }
 
 // Gram -> measure -> (inner Jacobi).  Returns true when the pair must be rotated.
-__device__ bool finish_gram(Small& sm, const double (&acc)[4], double z2, const PersArgs& a,
+__device__ bool finish_gram(Small& sm, const double (&acc)[4], double z2, double inv_f2, const PersArgs& a,
                             int sweep) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3, mt = warp >> 2, nt = warp & 3;
@@ -267,7 +282,7 @@ __device__ bool finish_gram(Small& sm, const double (&acc)[4], double z2, const 
   }
   __syncthreads();
   const bool rotate = sm.red[0] > a.tol;
-  if (rotate) inner_jacobi(sm, z2, a.tol, a.max_inner);
+  if (rotate) inner_jacobi(sm, z2, inv_f2, a.tol, a.max_inner);
   return rotate;
 }
 
@@ -284,7 +299,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_resident_kernel(PersArgs a) {
   const int p = blockIdx.x % a.npairs, b = a.batch0 + blockIdx.x / a.npairs;
   double* G = a.G + b * a.gstride;
   double* V = a.V + b * a.vstride;
-  const double z2 = a.zero2[b];
+  const double z2 = a.zero2[2 * b], inv_f2 = a.zero2[2 * b + 1];
   const int ncg = (a.mg + JCH - 1) / JCH, ncv = (a.vrows + JCH - 1) / JCH;
   int sweep = 0;
   for (; sweep < MAX_SWEEPS; ++sweep) {
@@ -292,15 +307,20 @@ __global__ void __launch_bounds__(JT, 1) jacobi_resident_kernel(PersArgs a) {
       int ba, bb;
       circle_pair(a.nb, round, p, ba, bb);
       const int ca = ba * JB, cb = bb * JB;
+      const bool prof = a.prof && blockIdx.x == 0 && threadIdx.x == 0;
+      long long t0 = prof ? clock64() : 0;
       for (int k = 0; k < ncg; ++k) load_chunk_async(XG[k], G, a.ldg, a.mg, k * JCH, ca, cb);
       for (int k = 0; k < ncv; ++k) load_chunk_async(XV[k], V, a.ldv, a.vrows, k * JCH, ca, cb);
       cp_commit();
       cp_wait<0>();
       __syncthreads();
+      long long t1 = prof ? clock64() : 0;
       double acc[4] = {0, 0, 0, 0};
       for (int k = 0; k < ncg; ++k) gram_chunk(XG[k], acc);
       __syncthreads();
-      if (finish_gram(sm, acc, z2, a, sweep)) {
+      long long t2 = prof ? clock64() : 0, t3 = 0;
+      if (finish_gram(sm, acc, z2, inv_f2, a, sweep)) {
+        t3 = prof ? clock64() : 0;
         for (int k = 0; k < ncg; ++k) {
           rotate_chunk(XG[k], sm);
           store_chunk(XG[k], G, a.ldg, a.mg, k * JCH, ca, cb);
@@ -309,8 +329,20 @@ __global__ void __launch_bounds__(JT, 1) jacobi_resident_kernel(PersArgs a) {
           rotate_chunk(XV[k], sm);
           store_chunk(XV[k], V, a.ldv, a.vrows, k * JCH, ca, cb);
         }
+      } else {
+        t3 = prof ? clock64() : 0;
       }
+      long long t4 = prof ? clock64() : 0;
       grid.sync();
+      if (prof) {
+        const long long t5 = clock64();
+        a.prof[0] += t1 - t0;  // load
+        a.prof[1] += t2 - t1;  // gram
+        a.prof[2] += t3 - t2;  // measure + inner Jacobi
+        a.prof[3] += t4 - t3;  // rotate + store
+        a.prof[4] += t5 - t4;  // grid barrier
+        a.prof[5] += 1;
+      }
     }
     const double meas = __longlong_as_double(
         static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(&a.conv[sweep])));
@@ -348,7 +380,7 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
   const int p = blockIdx.x % a.npairs, b = a.batch0 + blockIdx.x / a.npairs;
   double* G = a.G + b * a.gstride;
   double* V = a.V + b * a.vstride;
-  const double z2 = a.zero2[b];
+  const double z2 = a.zero2[2 * b], inv_f2 = a.zero2[2 * b + 1];
   const int nch = (a.mg + JCH - 1) / JCH;
   int sweep = 0;
   for (; sweep < MAX_SWEEPS; ++sweep) {
@@ -367,7 +399,7 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
         gram_chunk(X[k & 1], acc);
         __syncthreads();
       }
-      if (finish_gram(sm, acc, z2, a, sweep)) {
+      if (finish_gram(sm, acc, z2, inv_f2, a, sweep)) {
         stream_rotate(X, G, a.ldg, a.mg, ca, cb, sm);
         stream_rotate(X, V, a.ldv, a.vrows, ca, cb, sm);
       }
@@ -441,7 +473,8 @@ __global__ void zero_floor_kernel(const double* __restrict__ G, long gstride, lo
     double t = 0.0;
     for (int w = 0; w < (blockDim.x >> 5); ++w) t += sh[w];
     const double f = 64.0 * sqrt(static_cast<double>(mg)) * EPS;
-    zero2[blockIdx.x] = f * f * t;
+    zero2[2 * blockIdx.x] = f * f * t;
+    zero2[2 * blockIdx.x + 1] = t > 0 ? 1.0 / t : 1.0;  // 1 / ||G||_F^2 (scale-free angles)
   }
 }
 
@@ -550,7 +583,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   double* sorted = ws.sorted.reserve(static_cast<size_t>(ng) * batch);
   int* perm = ws.perm.reserve(static_cast<size_t>(ng) * batch);
   unsigned long long* conv = ws.conv.reserve(MAX_SWEEPS * 8);
-  double* zero2 = ws.zero2.reserve(static_cast<size_t>(batch));
+  double* zero2 = ws.zero2.reserve(2 * static_cast<size_t>(batch));
   int* sweeps_dev = ws.sweeps.reserve(64);
   int* sweeps_host = ws.sweeps_host.reserve(64);
   {
@@ -598,10 +631,26 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     const int nbat = std::min(per_launch, batch - b0);
     ACHI_CUDA(cudaMemsetAsync(conv, 0, sizeof(unsigned long long) * MAX_SWEEPS, ctx.stream));
     PersArgs a{G, ldg, gstride, mg, V, ng, vstride, ng, nb, npairs, b0,
-               max_inner, tol, stop_tol, zero2, conv, sweeps_dev + (launches % 64)};
+               max_inner, tol, stop_tol, zero2, conv, sweeps_dev + (launches % 64), nullptr};
+    static const bool prof_on = std::getenv("ACHI_JACOBI_PROF") != nullptr;
+    static DevArr<long long> profbuf;
+    if (prof_on) {
+      a.prof = profbuf.reserve(8);
+      ACHI_CUDA(cudaMemsetAsync(a.prof, 0, 8 * sizeof(long long), ctx.stream));
+    }
     void* args[] = {&a};
     ACHI_CUDA(cudaLaunchCooperativeKernel(kern, dim3(npairs * nbat), dim3(JT), args, smem, ctx.stream));
     ACHI_LAUNCHED(ctx);
+    if (prof_on) {
+      long long h[8];
+      ACHI_CUDA(cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
+      ctx.sync();
+      const double r = h[5] > 0 ? static_cast<double>(h[5]) : 1.0;
+      std::fprintf(stderr,
+                   "[jacobi] n=%d rounds=%lld cycles/round: load %.0f gram %.0f inner %.0f rotate %.0f "
+                   "barrier %.0f\n",
+                   ng, h[5], h[0] / r, h[1] / r, h[2] / r, h[3] / r, h[4] / r);
+    }
   }
   // pad columns: rows side -> columns >= m_true (theta rows (l,s1), padded l last);
   // cols side with padding -> columns (s2, jr) with jr >= chr_true (d = 2 on the padded path)

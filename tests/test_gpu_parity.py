@@ -314,3 +314,34 @@ def test_dmrg_c3_headline_parity(ctx, oracle):
     assert all(m < 1e-6 for *_, m in diverged), diverged
     if not diverged:
         assert np.array_equal(g["chi_profiles"], o["chi_profiles"])
+
+
+@pytest.mark.parametrize("case", ["xxz_field", "threshold", "direct", "mult_quadratic", "fixed_overcap"])
+def test_dmrg_modes_parity(ctx, oracle, case):
+    """Controller modes and model variants through the full device sweep vs the oracle."""
+    if case == "xxz_field":
+        spec = abi.model_spec(16, jz=0.5, h=0.1)
+        cfg = abi.adaptive_config(32, 1e-8, max_sweeps=4)
+    elif case == "threshold":
+        spec = abi.model_spec(12, jz=1.5)
+        cfg = abi.dmrg_config(abi.controller_config(mode=abi.MODE_THRESHOLD, chi_max=24,
+                                                    eps_trunc=1e-9), max_sweeps=4)
+    elif case == "direct":
+        spec = abi.model_spec(12, convention=abi.SPIN_HALF)
+        cfg = abi.dmrg_config(abi.controller_config(mode=abi.MODE_DIRECT, chi_max=24,
+                                                    gamma_margin=1.5), max_sweeps=4)
+    elif case == "mult_quadratic":
+        spec = abi.model_spec(12)
+        cfg = abi.dmrg_config(abi.controller_config(mode=abi.MODE_PID, chi_max=24, s_target=1.0,
+                                                    pid_scale=abi.PID_MULTIPLICATIVE,
+                                                    predictor_order=abi.PREDICT_QUADRATIC),
+                              max_sweeps=4)
+    else:  # fixed chi above the reachable rank: zero singular values are kept (dmrg.cpp:124-134)
+        spec = abi.model_spec(10)
+        cfg = abi.fixed_config(64, max_sweeps=3)
+    g = ctx.run_dmrg(spec, cfg)
+    o = oracle.run_dmrg(spec, cfg)
+    compare_runs(g, o)
+    gt = [(t.chi, t.delta_chi, t.clamped) for t in g["trace"]]
+    ot = [(t.chi, t.delta_chi, t.clamped) for t in o["trace"]]
+    assert gt == ot
