@@ -261,6 +261,15 @@ int achi_dgemm(achi_ctx* ctx, int M, int N, int K, int a_kmajor, const double* a
  * algorithmic TFLOP/s (2 D d^2 chi^2 (2 chi) + 4 D^2 d^3 chi^2 flops). */
 int achi_heff_bench(achi_ctx* ctx, int chi, int reps, double* ms_per_matvec, double* tflops);
 
+/* Spectrum reductions on the device (one CTA, deterministic order):
+ * out[0] = entropy_from_spectrum (mps.cpp:97-113), out[1] = truncation_error
+ * at `kept` (mps.cpp:115-122), out[2] = rank_for_discarded_weight(eps)
+ * (controller.cpp:134-148), out[3] = count of sigma > 1e-14 sigma_1.
+ * Errors as the reference: empty/zero spectrum -> DegenerateSpectrum, kept
+ * out of [1, n] -> InvalidRank. */
+int achi_spectrum_stats(achi_ctx* ctx, int n_sigma, const double* sigma, int kept, double eps,
+                        double* out4);
+
 /* eigs_lowest (linalg.cpp:107-178) with a dense symmetric operator (test
  * hook for the device Lanczos): h is dim x dim row-major. */
 int achi_eigs_lowest_dense(achi_ctx* ctx, int dim, const double* h,

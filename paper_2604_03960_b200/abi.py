@@ -175,6 +175,7 @@ def load():
                                              P(C.c_int), dp]),
         "achi_dgemm": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, dp, C.c_long, C.c_int,
                                  dp, C.c_long, dp, C.c_long]),
+        "achi_spectrum_stats": (C.c_int, [vp, C.c_int, dp, C.c_int, d, dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -158,6 +158,14 @@ class Context:
                                               sweep, bond, C.byref(row), C.byref(visit)))
         return row, visit
 
+    def spectrum_stats(self, sigma, kept=1, eps=0.0):
+        """(entropy, truncation_error(kept), rank_for_discarded_weight(eps), significant)."""
+        s = _f64(sigma)
+        out = np.zeros(4)
+        self._check(self.lib.achi_spectrum_stats(self.h, len(s), _dp(s), int(kept),
+                                                 C.c_double(eps), _dp(out)))
+        return float(out[0]), float(out[1]), int(out[2]), int(out[3])
+
     def eigs_lowest_dense(self, h, v0, tol=1e-10, max_iter=200):
         h, v0 = _f64(h), _f64(v0)
         dim = h.shape[0]

@@ -185,6 +185,76 @@ __global__ void __launch_bounds__(BS_THREADS) bond_select_kernel(
   }
 }
 
+// Standalone spectrum reductions (entropy, truncation error at `kept`,
+// discarded-weight floor rank, significant count) with the same deterministic
+// orders as bond_select_kernel.  out[4]; *err = ACHI_E_* or 0.
+__global__ void __launch_bounds__(BS_THREADS) spectrum_stats_kernel(const double* __restrict__ sigma,
+                                                                    int r, int kept, double eps,
+                                                                    double* out, int* err) {
+  extern __shared__ double dyn[];
+  double* suf = dyn;
+  double* seg = dyn + r + 1;
+  __shared__ double shd[33];
+  __shared__ int shi[33];
+  const double s1 = sigma[0];
+  if (!(s1 > 0)) {
+    if (threadIdx.x == 0) *err = ACHI_E_DEGENERATE_SPECTRUM;
+    return;
+  }
+  const int per = (r + BS_THREADS - 1) / BS_THREADS;
+  const int lo = threadIdx.x * per, hi = min(r, lo + per);
+  double acc = 0.0;
+  for (int k = hi - 1; k >= lo; --k) {
+    acc += sigma[k] * sigma[k];
+    suf[k] = acc;
+  }
+  seg[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double run = 0.0;
+    for (int t = BS_THREADS - 1; t >= 0; --t) {
+      const double v = seg[t];
+      seg[t] = run;
+      run += v;
+    }
+    suf[r] = 0.0;
+  }
+  __syncthreads();
+  for (int k = lo; k < hi; ++k) suf[k] += seg[threadIdx.x];
+  __syncthreads();
+  const double thr = eps * suf[0];
+  int kstar = 0;
+  for (int k = max(lo, 1); k < hi; ++k)
+    if (suf[k] > thr) kstar = max(kstar, k);
+  kstar = bs_max_int(kstar, shi);
+  const double cutoff = 1e-14 * s1;
+  double cnt = 0.0, tot_e = 0.0;
+  for (int k = threadIdx.x; k < r; k += BS_THREADS) {
+    const double v = sigma[k];
+    cnt += v > cutoff ? 1.0 : 0.0;
+    if (v > cutoff) tot_e += v * v;
+  }
+  const double significant = bs_sum(cnt, shd);
+  tot_e = bs_sum(tot_e, shd);
+  double ent = 0.0;
+  for (int k = threadIdx.x; k < r; k += BS_THREADS) {
+    const double v = sigma[k];
+    if (v > cutoff) {
+      const double p = v * v / tot_e;
+      if (p > 0) ent -= p * log(p);
+    }
+  }
+  ent = bs_sum(ent, shd);
+  if (threadIdx.x == 0) {
+    out[0] = ent;
+    const double tail = (kept >= 1 && kept < r) ? suf[kept] : 0.0;
+    out[1] = sqrt(tail > 0 ? tail : 0.0);
+    out[2] = kstar >= 1 ? kstar + 1 : 1;
+    out[3] = significant;
+    *err = 0;
+  }
+}
+
 struct AbsorbArgs {
   const double* G;
   const double* V;
@@ -251,6 +321,20 @@ void bond_select(Ctx& ctx, const double* sigma, int r, const achi_dmrg_config& c
   if (smem > 200 * 1024) fail(ACHI_E_SIZE_GUARD, "bond_select: spectrum too long");
   bond_select_kernel<<<1, BS_THREADS, smem, ctx.stream>>>(sigma, r, cfg, states, bond, sweep,
                                                           moving_right, trace_slot, visit_slot, out);
+  ACHI_LAUNCHED(ctx);
+}
+
+void spectrum_stats(Ctx& ctx, const double* sigma, int r, int kept, double eps, double* out,
+                    int* err) {
+  const size_t smem = sizeof(double) * (static_cast<size_t>(r) + 1 + BS_THREADS);
+  static bool attr = false;
+  if (!attr) {
+    ACHI_CUDA(cudaFuncSetAttribute(spectrum_stats_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  if (smem > 200 * 1024) fail(ACHI_E_SIZE_GUARD, "spectrum_stats: spectrum too long");
+  spectrum_stats_kernel<<<1, BS_THREADS, smem, ctx.stream>>>(sigma, r, kept, eps, out, err);
   ACHI_LAUNCHED(ctx);
 }
 

@@ -20,6 +20,10 @@ void bond_select(Ctx& ctx, const double* sigma, int r, const achi_dmrg_config& c
                  achi_bond_state* states, int bond, int sweep, int moving_right,
                  achi_trace_row* trace_slot, achi_visit_record* visit_slot, BondOut* out);
 
+// entropy / truncation error / floor rank / significant count of one spectrum
+void spectrum_stats(Ctx& ctx, const double* sigma, int r, int kept, double eps, double* out,
+                    int* err);
+
 // Write site b (chl~, d, kept~) and site b+1 (kept~, d, chr~) from the SVD
 // factors (dmrg.cpp:144-158); moving_right absorbs lambda/||lambda|| into
 // site b+1, otherwise into site b.  Pads are written as zeros.

@@ -484,6 +484,27 @@ int achi_dgemm(achi_ctx* ctx, int M, int N, int K, int a_kmajor, const double* a
   });
 }
 
+int achi_spectrum_stats(achi_ctx* ctx, int n_sigma, const double* sigma, int kept, double eps,
+                        double* out4) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    if (n_sigma < 1) fail(ACHI_E_DEGENERATE_SPECTRUM, "entropy: empty spectrum");
+    if (kept < 1 || kept > n_sigma) fail(ACHI_E_INVALID_RANK, "truncation_error: kept out of range");
+    DevBuf dS, dO;
+    DevArr<int> dE;
+    dS.reserve(n_sigma);
+    dO.reserve(4);
+    dE.reserve(1);
+    h2d(c, dS.p, sigma, n_sigma);
+    spectrum_stats(c, dS.p, n_sigma, kept, eps, dO.p, dE.p);
+    int err = 0;
+    d2h(c, out4, dO.p, 4);
+    ACHI_CUDA(cudaMemcpyAsync(&err, dE.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (err) fail(err, "entropy: all-zero spectrum");
+  });
+}
+
 int achi_heff_bench(achi_ctx* ctx, int chi, int reps, double* ms_per_matvec, double* tflops) {
   return guard(ctx, [&] {
     Ctx& c = ctx->c;
