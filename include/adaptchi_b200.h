@@ -234,9 +234,16 @@ int achi_svd(achi_ctx* ctx, int m, int n, const double* a, double* sigma,
 int achi_svd_batched(achi_ctx* ctx, int batch, int m, int n, const double* a,
                      double* sigma);
 /* Same on DEVICE pointers (inputs already resident in HBM; the benchmark's
- * device-time path).  d_sigma: batch x min(m,n) device buffer. */
+ * device-time path).  d_sigma: batch x min(m,n) device buffer.  Values only:
+ * no singular vectors are accumulated. */
 int achi_svd_batched_device(achi_ctx* ctx, int batch, int m, int n, const double* d_a,
                             double* d_sigma, int* sweeps_out);
+/* svd_full on DEVICE pointers with both factors (the truncated-SVD timing
+ * path of bench.cpp:635-668: the reference computes U, sigma, V^dagger and
+ * then truncates).  d_a: m x n row-major; d_sigma[r]; d_u: m x r row-major;
+ * d_vt: r x n row-major (r = min(m, n)); fix_phases applied. */
+int achi_svd_device(achi_ctx* ctx, int m, int n, const double* d_a, double* d_sigma,
+                    double* d_u, double* d_vt, int* sweeps_out);
 
 /* Fused bond-select kernel (K7) on a host spectrum: entropy_from_spectrum
  * (mps.cpp:97-113), rank_for_discarded_weight (controller.cpp:134-148),

@@ -176,6 +176,8 @@ def load():
         "achi_dgemm": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, dp, C.c_long, C.c_int,
                                  dp, C.c_long, dp, C.c_long]),
         "achi_spectrum_stats": (C.c_int, [vp, C.c_int, dp, C.c_int, d, dp]),
+        "achi_svd_device": (C.c_int, [vp, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, P(C.c_int)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -98,6 +98,13 @@ class Context:
                                                      C.c_void_p(d_sigma_ptr), C.byref(sw)))
         return sw.value
 
+    def svd_device(self, d_a_ptr, m, n, d_sigma_ptr, d_u_ptr, d_vt_ptr):
+        """Device-pointer svd_full with U and V^T (row-major); returns Jacobi sweeps."""
+        sw = C.c_int()
+        self._check(self.lib.achi_svd_device(self.h, m, n, C.c_void_p(d_a_ptr), C.c_void_p(d_sigma_ptr),
+                                             C.c_void_p(d_u_ptr), C.c_void_p(d_vt_ptr), C.byref(sw)))
+        return sw.value
+
     def flush_l2(self, nbytes=256 << 20):
         self._check(self.lib.achi_flush_l2(self.h, C.c_size_t(nbytes)))
 

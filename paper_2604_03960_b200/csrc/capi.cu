@@ -410,7 +410,8 @@ int achi_svd_batched(achi_ctx* ctx, int batch, int m, int n, const double* a, do
     dS.reserve(static_cast<size_t>(k) * batch);
     h2d(c, dA.p, a, static_cast<size_t>(mn) * batch);
     SvdWs ws;
-    svd_device(c, ws, dA.p, m, n, m, n, m <= n ? SvdSide::kRows : SvdSide::kCols, batch, mn, dS.p);
+    svd_device(c, ws, dA.p, m, n, m, n, m <= n ? SvdSide::kRows : SvdSide::kCols, batch, mn, dS.p,
+               false);
     d2h(c, sigma, dS.p, static_cast<size_t>(k) * batch);
     c.sync();
   });
@@ -422,7 +423,24 @@ int achi_svd_batched_device(achi_ctx* ctx, int batch, int m, int n, const double
     Ctx& c = ctx->c;
     static thread_local SvdWs ws;  // reused across benchmark calls (no realloc per call)
     SvdResultDev r = svd_device(c, ws, d_a, m, n, m, n, m <= n ? SvdSide::kRows : SvdSide::kCols,
-                                batch, static_cast<long>(m) * n, d_sigma);
+                                batch, static_cast<long>(m) * n, d_sigma, false);
+    c.sync();
+    if (sweeps_out) *sweeps_out = r.sweeps();
+  });
+}
+
+int achi_svd_device(achi_ctx* ctx, int m, int n, const double* d_a, double* d_sigma, double* d_u,
+                    double* d_vt, int* sweeps_out) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    if (m < 1 || n < 1) fail(ACHI_E_INVALID_MATRIX, "svd: matrix must be at least 1x1");
+    static thread_local SvdWs ws;
+    SvdResultDev r = svd_device(c, ws, d_a, m, n, m, n, m <= n ? SvdSide::kRows : SvdSide::kCols);
+    const int k = r.r_true;
+    svd_phase_signs(c, ws, r, k);
+    svd_gather(c, ws, r, k, d_u, d_vt);
+    if (d_sigma)
+      ACHI_CUDA(cudaMemcpyAsync(d_sigma, r.sigma, sizeof(double) * k, cudaMemcpyDeviceToDevice, c.stream));
     c.sync();
     if (sweeps_out) *sweeps_out = r.sweeps();
   });

@@ -148,6 +148,11 @@ void Chain::create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g) 
   site.resize(n);
   L.resize(n);
   R.resize(n);
+  vkeep.resize(2 * static_cast<size_t>(n - 1));
+  {
+    const char* e = std::getenv("ACHI_SVD_WARM");
+    warm_svd = !(e && e[0] == '0');
+  }
   size_t max_vec = 0, max_ws = 0;
   for (int k = 0; k < n; ++k) {
     const size_t cl = pad2i(cap[k]), cr = pad2i(cap[k + 1]);
@@ -237,7 +242,21 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   const auto t1 = clk::now();
   const SvdSide side = right ? SvdSide::kRows : SvdSide::kCols;
   c.acc.begin(EventAcc::kSvd, c.stream);
-  SvdResultDev sr = svd_device(c, svd, vec.p, chlp * d, d * chrp, chl * d, d * chr, side);
+  const int sm_ = chlp * d, sn_ = d * chrp, smt = chl * d, snt = d * chr;
+  VKeep& vk = vkeep[2 * static_cast<size_t>(b) + (right ? 1 : 0)];
+  const bool warm = warm_svd && vk.valid && vk.m == sm_ && vk.n == sn_ && vk.mt == smt && vk.nt == snt;
+  SvdResultDev sr = svd_device(c, svd, vec.p, sm_, sn_, smt, snt, side, 1, 0, nullptr, true,
+                               warm ? vk.v.p : nullptr);
+  if (warm_svd) {  // keep this factor for the next visit of the bond in this direction
+    const size_t nv = static_cast<size_t>(sr.ng) * sr.ng;
+    vk.v.reserve(nv);
+    ACHI_CUDA(cudaMemcpyAsync(vk.v.p, sr.V, sizeof(double) * nv, cudaMemcpyDeviceToDevice, c.stream));
+    vk.m = sm_;
+    vk.n = sn_;
+    vk.mt = smt;
+    vk.nt = snt;
+    vk.valid = true;
+  }
   c.acc.end(c.stream, 0.0);
   c.sync();
   c.acc.resolve();

@@ -46,6 +46,17 @@ struct Chain {
   DevBuf theta, vec;
   LanczosWs lz;
   SvdWs svd;
+  // SVD warm start (svd_device v_init): the last orthogonal factor of each bond
+  // per sweep direction with the padded/true theta shape it belongs to.  Once
+  // the state has converged, the same bond's block changes little between
+  // sweeps, so the previous factor nearly diagonalises it.
+  struct VKeep {
+    DevBuf v;
+    int m = 0, n = 0, mt = 0, nt = 0;
+    bool valid = false;
+  };
+  std::vector<VKeep> vkeep;  // [2 b + moving_right]
+  bool warm_svd = true;
   std::vector<VisitHost> vh;
   // phase wall-clock accounting (host steady_clock at the existing sync points)
   struct Stats {

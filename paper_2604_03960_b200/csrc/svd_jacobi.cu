@@ -1,15 +1,26 @@
 // Blocked one-sided Jacobi SVD on sm_100a (see svd_jacobi.cuh).
 //
-// One cooperative launch runs every sweep and every round of the Jacobi
-// iteration: CTA p owns block pair p of the current round (circle-method
-// ordering of 16-column blocks), forms the 32x32 Gram matrix of its columns
-// with DMMA, diagonalises it by two-sided Jacobi in shared memory and applies
-// the accumulated rotation to its columns of G and V with DMMA; a grid-wide
-// barrier separates rounds.  Small problems (<= 256 rows) keep the pair's
-// columns resident in shared memory for the whole round; large ones stream
-// 64-row chunks with double-buffered cp.async.  Convergence is decided on the
-// device (max off-diagonal measure of a sweep), so the host never waits
-// inside the iteration.
+// Columns of the working matrix G are grouped in 16-column blocks; each round
+// pairs blocks by the circle method and one CTA per pair forms the 32x32 Gram
+// matrix of its columns with DMMA, diagonalises it by two-sided Jacobi in
+// shared memory and applies the accumulated rotation J to its columns.
+//
+// Two launch shapes:
+//  * CLUSTER (working matrix <= 256 x 256, every DMRG bond of config C3): one
+//    thread-block cluster per matrix, one CTA per block pair, the whole of G
+//    resident in distributed shared memory.  The rotation epilogue stores the
+//    rotated blocks straight into the shared memory of the CTA that owns them
+//    in the next round (the circle method moves every block along a fixed
+//    ring), so a round ends with one cluster barrier instead of a grid-wide
+//    barrier plus an L2 round trip.  The rotations J of every round are
+//    recorded and V = prod J is replayed afterwards by a separate kernel over
+//    row slices of V on many SMs (V's rows are independent), which takes the
+//    V update off the serial critical path.
+//  * STREAM (larger matrices): one cooperative persistent launch, 64-row chunks
+//    of G and V double-buffered through shared memory with cp.async, grid-wide
+//    barrier between rounds.
+// Convergence is decided on the device (max off-diagonal measure of a sweep),
+// so the host never waits inside the iteration.
 #include <cooperative_groups.h>
 
 #include <cmath>
@@ -17,6 +28,7 @@
 #include <cstring>
 
 #include "svd_jacobi.cuh"
+#include "gemm_dmma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -27,11 +39,13 @@ namespace {
 constexpr int JB = 16;        // columns per block
 constexpr int JW = 32;        // columns per block pair
 constexpr int JT = 256;       // threads per CTA
-constexpr int JCH = 64;       // rows per chunk
+constexpr int JCH = 64;       // rows per chunk (stream mode)
 constexpr int JLD = JCH + 4;  // conflict-free DMMA fragment loads
 constexpr int SLD = JW + 4;
-constexpr int RES_CHUNKS = 4; // resident mode: up to 256 rows of G and of V
+constexpr int CL_ROWS = 256;  // cluster mode: max working rows
+constexpr int CL_MAXP = 8;    // cluster mode: max block pairs (portable cluster size)
 constexpr int MAX_SWEEPS = 40;
+constexpr int RP_ROWS = 4;    // V replay: rows of V per CTA
 constexpr double EPS = 2.220446049250313e-16;
 
 __device__ __forceinline__ void mma16x8x4(double (&c)[4], double a0, double a1, double b0) {
@@ -42,8 +56,15 @@ __device__ __forceinline__ void mma16x8x4(double (&c)[4], double a0, double a1, 
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-// circle-method round robin: pair p of round r among n (even) players
-__device__ __forceinline__ void circle_pair(int n, int r, int p, int& a, int& b) {
+__device__ __forceinline__ double rcp_approx(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+// circle-method round robin: pair p of round r among n (even) players.
+// Pair 0 is (r, n-1); pair p > 0 is ((r+p) mod (n-1), (r-p) mod (n-1)).
+__device__ __forceinline__ void circle_pair_ns(int n, int r, int p, int& a, int& b) {
   if (p == 0) {
     a = r;
     b = n - 1;
@@ -51,41 +72,380 @@ __device__ __forceinline__ void circle_pair(int n, int r, int p, int& a, int& b)
     a = (r + p) % (n - 1);
     b = (r - p + n - 1) % (n - 1);
   }
+}
+__device__ __forceinline__ void circle_pair(int n, int r, int p, int& a, int& b) {
+  circle_pair_ns(n, r, p, a, b);
   if (a > b) {
     const int t = a;
     a = b;
     b = t;
   }
 }
+// where block x sits in round r of circle_pair_ns: pair *p, slot *s (0 = a, 1 = b)
+__device__ __forceinline__ void circle_locate(int n, int r, int x, int& p, int& s) {
+  const int m = n - 1;
+  if (x == m) {
+    p = 0;
+    s = 1;
+    return;
+  }
+  const int d = ((x - r) % m + m) % m;  // x = r + d
+  if (d == 0) {
+    p = 0;
+    s = 0;
+  } else if (d < n / 2) {
+    p = d;
+    s = 0;
+  } else {
+    p = m - d;  // x = r - p
+    s = 1;
+  }
+}
 
 typedef double Chunk[JW][JLD];
 
-struct PersArgs {
-  double* G;
-  long ldg, gstride;
-  int mg;
-  double* V;
-  long ldv, vstride;
-  int vrows;
-  int nb, npairs, batch0;
-  int max_inner;
-  double tol, stop_tol;
-  const double* zero2;
-  unsigned long long* conv;  // [MAX_SWEEPS] per-sweep max measure (whole launch)
-  int* sweeps_out;
-  long long* prof;  // optional clock64 phase accounting (CTA 0), null in production
-};
-
 struct Small {
-  double S[JW][SLD];
+  double S[2][JW][SLD];  // double-buffered Gram (one barrier per inner step)
   double J[JW][SLD];
-  double cs[16][2];
   double red[JT / 32];
   unsigned char pi[JW - 1][JW / 2], pj[JW - 1][JW / 2];
-  int changed;
 };
 
-// ---- cp.async chunk loads: rows [r0, r0+64) of the 32 pair columns -> X[col][row] ----
+__device__ __forceinline__ float rcp_f32(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sqrt_f32(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqrt_f32(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Jacobi rotation (c, s, t = s/c) annihilating apq of [[app, apq], [apq, aqq]],
+// or the identity when the pair is already orthogonal to tol.  Branch-free (the
+// two evaluations of a thread interleave) and every thread evaluating the same
+// pair gets identical bits (explicit rounding intrinsics and approximation
+// instructions, no contraction freedom).  tau = (aqq - app) / (2 apq) uses the
+// FP64 reciprocal estimate (full exponent range); t = sgn/(|tau| +
+// sqrt(1 + tau^2)) is formed in FP32: the angle may be approximate (the residue
+// is removed by later sweeps) but (c, s) are orthonormal to FP64 precision:
+// c = rsqrt(1 + t^2) from an FP32 seed and one FP64 Halley step (cubic, 2^-22
+// -> 2^-64), s = t c.  |tau| beyond FP32 range gives t = 0 (no rotation).
+__device__ __forceinline__ bool jacobi_angle(double app, double aqq, double apq, double z2, double tol2,
+                                             double& c, double& s, double& t) {
+  const bool ok = app > z2 && aqq > z2 && __dmul_rn(apq, apq) > __dmul_rn(tol2, __dmul_rn(app, aqq));
+  const double tau = __dmul_rn(__dsub_rn(aqq, app), rcp_approx(__dmul_rn(2.0, apq)));
+  const float tf = __double2float_rn(tau);
+  const float w = __fadd_rn(fabsf(tf), sqrt_f32(__fmaf_rn(tf, tf, 1.0f)));
+  const float tt = copysignf(rcp_f32(w), tf);
+  const double td = static_cast<double>(tt);
+  const double x = __fma_rn(td, td, 1.0);
+  double y = static_cast<double>(rsqrt_f32(__fmaf_rn(tt, tt, 1.0f)));
+  const double e = __fma_rn(-x, __dmul_rn(y, y), 1.0);
+  y = __fma_rn(__dmul_rn(y, e), __fma_rn(0.375, e, 0.5), y);
+  c = ok ? y : 1.0;
+  s = ok ? __dmul_rn(td, y) : 0.0;
+  t = ok ? td : 0.0;
+  return ok;
+}
+
+// two-sided cyclic Jacobi on S (32x32, starts in S[0]), accumulating J (starts
+// at I).  A parallel step rotates 16 disjoint pairs; thread (bp, bq) owns the
+// 2x2 block S[{ip,jp},{iq,jq}] <- Rp^T S Rq and J rows {2bp, 2bp+1} x pair bq.
+// Lane l of every warp evaluates the rotation of pair l & 15 (= bq): a warp
+// holds two values of bp, whose rotations come from lanes bp by shuffle, so
+// each step is one angle evaluation per thread and ONE block barrier (S is
+// double-buffered: read S[cur], write S[cur^1]).  The pair tables of the next
+// step are prefetched and the J operands are loaded before the angle so their
+// latency overlaps it.
+__device__ void inner_jacobi(Small& sm, double z2, double tol, int max_inner) {
+  const int t = threadIdx.x;
+  const int bp = t >> 4, bq = t & 15;
+  const double tol2 = tol * tol;
+  int cur = 0;
+  for (int sweep = 0; sweep < max_inner; ++sweep) {
+    int any = 0;
+    int ip = sm.pi[0][bp], jp = sm.pj[0][bp], iq = sm.pi[0][bq], jq = sm.pj[0][bq];
+    for (int step = 0; step < JW - 1; ++step) {
+      const int sn = step + 1 < JW - 1 ? step + 1 : step;
+      const int nip = sm.pi[sn][bp], njp = sm.pj[sn][bp], niq = sm.pi[sn][bq], njq = sm.pj[sn][bq];
+      double(*S)[SLD] = sm.S[cur];
+      double(*D)[SLD] = sm.S[cur ^ 1];
+      const double jx0 = sm.J[2 * bp][iq], jy0 = sm.J[2 * bp][jq];
+      const double jx1 = sm.J[2 * bp + 1][iq], jy1 = sm.J[2 * bp + 1][jq];
+      const double qii = S[iq][iq], qjj = S[jq][jq], qij = S[iq][jq];
+      const double a = S[ip][iq], b = S[ip][jq], c = S[jp][iq], d = S[jp][jq];
+      double cq, sq, tq;
+      const bool okq = jacobi_angle(qii, qjj, qij, z2, tol2, cq, sq, tq);
+      any |= okq ? 1 : 0;
+      const double cp = __shfl_sync(0xffffffffu, cq, bp), sp = __shfl_sync(0xffffffffu, sq, bp);
+      if (bp == bq && okq) {
+        // the pivot block: stable updates app - t apq, aqq + t apq, exact zero
+        D[iq][iq] = __fma_rn(-tq, qij, qii);
+        D[jq][jq] = __fma_rn(tq, qij, qjj);
+        D[iq][jq] = 0.0;
+        D[jq][iq] = 0.0;
+      } else {
+        // columns: (x, y) -> (cq x - sq y, sq x + cq y); rows likewise with (cp, sp)
+        const double a1 = cq * a - sq * b, b1 = sq * a + cq * b;
+        const double c1 = cq * c - sq * d, d1 = sq * c + cq * d;
+        D[ip][iq] = cp * a1 - sp * c1;
+        D[jp][iq] = sp * a1 + cp * c1;
+        D[ip][jq] = cp * b1 - sp * d1;
+        D[jp][jq] = sp * b1 + cp * d1;
+      }
+      if (okq) {
+        sm.J[2 * bp][iq] = cq * jx0 - sq * jy0;
+        sm.J[2 * bp][jq] = sq * jx0 + cq * jy0;
+        sm.J[2 * bp + 1][iq] = cq * jx1 - sq * jy1;
+        sm.J[2 * bp + 1][jq] = sq * jx1 + cq * jy1;
+      }
+      ip = nip;
+      jp = njp;
+      iq = niq;
+      jq = njq;
+      cur ^= 1;
+      __syncthreads();
+    }
+    // the next sweep continues from S[cur]
+    if (sweep + 1 < max_inner && !__syncthreads_or(any)) break;
+  }
+}
+
+__device__ void init_pair_tables(Small& sm) {
+  for (int idx = threadIdx.x; idx < (JW - 1) * (JW / 2); idx += JT) {
+    const int step = idx / (JW / 2), p = idx - step * (JW / 2);
+    int i, j;
+    circle_pair(JW, step, p, i, j);
+    sm.pi[step][p] = static_cast<unsigned char>(i);
+    sm.pj[step][p] = static_cast<unsigned char>(j);
+  }
+}
+
+// Gram tile (from the warp's DMMA accumulator) -> S[0], J = I, off-diagonal
+// measure max |S_ij| / sqrt(S_ii S_jj) over non-noise columns -> sm.red[0];
+// inner Jacobi when the measure exceeds tol.  Returns true when rotated.
+__device__ bool finish_gram(Small& sm, const double (&acc)[4], double z2, double tol, int max_inner) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3, mt = warp >> 2, nt = warp & 3;
+  {
+    const int r = mt * 16 + gid, c = nt * 8 + 2 * tig;
+    sm.S[0][r][c] = acc[0];
+    sm.S[0][r][c + 1] = acc[1];
+    sm.S[0][r + 8][c] = acc[2];
+    sm.S[0][r + 8][c + 1] = acc[3];
+  }
+  for (int idx = threadIdx.x; idx < JW * JW; idx += JT) {
+    const int r = idx / JW, c = idx - r * JW;
+    sm.J[r][c] = r == c ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  // squared measure with a reciprocal estimate (2^-23 relative: only compared
+  // with thresholds), one square root at the end
+  double meas2 = 0.0;
+  for (int idx = threadIdx.x; idx < JW * JW; idx += JT) {
+    const int i = idx / JW, j = idx - i * JW;
+    const double sii = sm.S[0][i][i], sjj = sm.S[0][j][j], sij = sm.S[0][i][j];
+    if (i < j && sii > z2 && sjj > z2)
+      meas2 = fmax(meas2, __dmul_rn(__dmul_rn(sij, sij), rcp_approx(__dmul_rn(sii, sjj))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) meas2 = fmax(meas2, __shfl_xor_sync(0xffffffffu, meas2, o));
+  if (lane == 0) sm.red[warp] = meas2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0;
+    for (int w = 0; w < JT / 32; ++w) m = fmax(m, sm.red[w]);
+    sm.red[0] = sqrt(m);
+  }
+  __syncthreads();
+  const bool rotate = sm.red[0] > tol;
+  if (rotate) inner_jacobi(sm, z2, tol, max_inner);
+  return rotate;
+}
+
+// =============================== CLUSTER mode ===============================
+
+struct ClArgs {
+  double* G;
+  long ldg, gstride;
+  int mg, rows_pad;  // true working rows; rows held in smem (multiple of 16)
+  int nb, npairs, max_inner;
+  double tol, stop_tol;
+  const double* zero2;
+  double* jrec;            // [batch][MAX_SWEEPS*(nb-1)][npairs][32][32] or null
+  unsigned char* jflag;    // [batch][MAX_SWEEPS*(nb-1)][npairs]
+  long jstride;            // rounds capacity per batch item (MAX_SWEEPS*(nb-1))
+  int* sweeps_out;         // [batch]
+  long long* prof;         // optional clock64 phase accounting (cluster 0, CTA 0)
+};
+
+// acc (16x8 tile per warp of the 32x32 Gram) over rows [0, rows) of X
+// ([32 cols][cld]); two independent accumulator chains, fixed summation order.
+__device__ __forceinline__ void gram_resident(const double* X, int cld, int rows, double (&acc)[4]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3, mt = warp >> 2, nt = warp & 3;
+  const double* xa = X + (mt * 16 + gid) * cld + tig;
+  const double* xa8 = xa + 8 * cld;
+  const double* xb = X + (nt * 8 + gid) * cld + tig;
+  double acc2[4] = {0, 0, 0, 0};
+  int k = 0;
+  for (; k + 8 <= rows; k += 8) {
+    mma16x8x4(acc, xa[k], xa8[k], xb[k]);
+    mma16x8x4(acc2, xa[k + 4], xa8[k + 4], xb[k + 4]);
+  }
+  for (; k < rows; k += 4) mma16x8x4(acc, xa[k], xa8[k], xb[k]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc[i] += acc2[i];
+}
+
+// out = X * J (rows_pad x 32) stored into the next-round owners' buffers:
+// columns 0..15 -> dst_a, 16..31 -> dst_b (both [16 cols][cld], possibly in
+// another CTA's shared memory).  rotate == false copies.
+__device__ __forceinline__ void rotate_resident(const double* X, int cld, int rows, const Small& sm,
+                                                bool rotate, double* dst_a, double* dst_b) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  if (!rotate) {
+    for (int idx = threadIdx.x; idx < JW * rows; idx += JT) {
+      const int c = idx / rows, r = idx - c * rows;
+      const double v = X[c * cld + r];
+      if (c < JB)
+        dst_a[c * cld + r] = v;
+      else
+        dst_b[(c - JB) * cld + r] = v;
+    }
+    return;
+  }
+  // J fragments (B operand, k x n = 32 x 32): bj[k4][nt] = J[k4*4+tig][nt*8+gid]
+  double bj[8][4];
+#pragma unroll
+  for (int k4 = 0; k4 < 8; ++k4)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) bj[k4][nt] = sm.J[k4 * 4 + tig][nt * 8 + gid];
+  for (int mt = warp; mt * 16 < rows; mt += JT / 32) {
+    double acc[4][4] = {};
+#pragma unroll
+    for (int k4 = 0; k4 < 8; ++k4) {
+      const int k = k4 * 4 + tig;
+      const double a0 = X[k * cld + mt * 16 + gid], a1 = X[k * cld + mt * 16 + gid + 8];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) mma16x8x4(acc[nt], a0, a1, bj[k4][nt]);
+    }
+    const int r = mt * 16 + gid;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int j = nt * 8 + 2 * tig;  // j, j+1 in the same block (8-aligned tiles)
+      double* dst = j < JB ? dst_a + j * cld : dst_b + (j - JB) * cld;
+      dst[r] = acc[nt][0];
+      dst[cld + r] = acc[nt][1];
+      dst[r + 8] = acc[nt][2];
+      dst[cld + r + 8] = acc[nt][3];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(JT, 1) jacobi_cluster_kernel(ClArgs a) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  // per-sweep measure of this CTA, three slots: slot s%3 is written during
+  // sweep s, read by every CTA after its last barrier, and reset at the start
+  // of sweep s+2 (a whole sweep of barriers after the last remote read)
+  __shared__ double meas_slot[3];
+  cg::cluster_group cl = cg::this_cluster();
+  const int p = static_cast<int>(cl.block_rank());
+  const int b = blockIdx.x / a.npairs;
+  const int cld = a.rows_pad + 4;
+  const long bufsz = static_cast<long>(JW) * cld;
+  double* X0 = reinterpret_cast<double*>(dyn);  // [2][32][cld]
+  Small& sm = *reinterpret_cast<Small*>(X0 + 2 * bufsz);
+  init_pair_tables(sm);
+  double* G = a.G + b * a.gstride;
+  const double z2 = a.zero2[2 * b];
+  const int nb = a.nb, rounds = nb - 1;
+  int ba, bb;
+  circle_pair_ns(nb, 0, p, ba, bb);
+  for (int idx = threadIdx.x; idx < JW * a.rows_pad; idx += JT) {
+    const int c = idx / a.rows_pad, r = idx - c * a.rows_pad;
+    const int col = c < JB ? ba * JB + c : bb * JB + c - JB;
+    X0[c * cld + r] = r < a.mg ? G[col * a.ldg + r] : 0.0;
+  }
+  if (threadIdx.x == 0) meas_slot[0] = meas_slot[1] = meas_slot[2] = 0.0;
+  cl.sync();
+  int buf = 0;
+  long rg = 0;
+  int sweep = 0;
+  for (; sweep < MAX_SWEEPS; ++sweep) {
+    if (threadIdx.x == 0) meas_slot[(sweep + 1) % 3] = 0.0;
+    for (int r = 0; r < rounds; ++r, ++rg) {
+      circle_pair_ns(nb, r, p, ba, bb);
+      const double* X = X0 + buf * bufsz;
+      const bool prof = a.prof && b == 0 && p == 0 && threadIdx.x == 0;
+      const long long t0 = prof ? clock64() : 0;
+      double acc[4] = {0, 0, 0, 0};
+      gram_resident(X, cld, a.rows_pad, acc);
+      const long long t1 = prof ? clock64() : 0;
+      const bool rot = finish_gram(sm, acc, z2, a.tol, a.max_inner);
+      const long long t2 = prof ? clock64() : 0;
+      if (threadIdx.x == 0) meas_slot[sweep % 3] = fmax(meas_slot[sweep % 3], sm.red[0]);
+      if (a.jrec) {
+        const long slot = (b * a.jstride + rg) * a.npairs + p;
+        if (threadIdx.x == 0) a.jflag[slot] = rot ? 1 : 0;
+        if (rot) {
+          double* jr = a.jrec + slot * (JW * JW);
+          for (int idx = threadIdx.x; idx < JW * JW; idx += JT) jr[idx] = sm.J[idx / JW][idx % JW];
+        }
+      }
+      // next-round owners of blocks ba (slot a) and bb (slot b)
+      const int rn = r + 1 < rounds ? r + 1 : 0;
+      int pa, sa, pb, sb;
+      circle_locate(nb, rn, ba, pa, sa);
+      circle_locate(nb, rn, bb, pb, sb);
+      double* nxt = X0 + (buf ^ 1) * bufsz;
+      double* dst_a = cl.map_shared_rank(nxt + sa * JB * cld, pa);
+      double* dst_b = cl.map_shared_rank(nxt + sb * JB * cld, pb);
+      const long long t3 = prof ? clock64() : 0;
+      rotate_resident(X, cld, a.rows_pad, sm, rot, dst_a, dst_b);
+      const long long t4 = prof ? clock64() : 0;
+      buf ^= 1;
+      cl.sync();
+      if (prof) {
+        a.prof[0] += t1 - t0;           // gram
+        a.prof[1] += t2 - t1;           // measure + inner Jacobi
+        a.prof[2] += t3 - t2;           // J record
+        a.prof[3] += t4 - t3;           // rotate + remote store
+        a.prof[4] += clock64() - t4;    // cluster barrier
+        a.prof[5] += 1;
+        a.prof[6] += rot ? 1 : 0;
+      }
+    }
+    double m = 0.0;
+    for (int q = 0; q < a.npairs; ++q) m = fmax(m, *cl.map_shared_rank(&meas_slot[sweep % 3], q));
+    if (m < a.stop_tol) {
+      ++sweep;
+      break;
+    }
+  }
+  // after whole sweeps every block is back at its round-0 owner
+  circle_pair_ns(nb, 0, p, ba, bb);
+  const double* X = X0 + buf * bufsz;
+  for (int idx = threadIdx.x; idx < JW * a.rows_pad; idx += JT) {
+    const int c = idx / a.rows_pad, r = idx - c * a.rows_pad;
+    const int col = c < JB ? ba * JB + c : bb * JB + c - JB;
+    if (r < a.ldg) G[col * a.ldg + r] = X[c * cld + r];
+  }
+  if (p == 0 && threadIdx.x == 0) a.sweeps_out[b] = sweep;
+}
+
+// V (ng x ng col-major, ld ng) = I * prod over recorded rounds of the block
+// rotations J.  CTA = RP_ROWS rows of V (rows are independent), thread = one
+// column; the rounds' J are staged through shared memory with cp.async one
+// round ahead.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes)
@@ -95,14 +455,106 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+__global__ void __launch_bounds__(JT) v_replay_kernel(double* V, long vstride, int ng, int nb, int npairs,
+                                                      const double* __restrict__ jrec,
+                                                      const unsigned char* __restrict__ jflag,
+                                                      long jstride, const int* __restrict__ sweeps,
+                                                      const double* __restrict__ v0) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  double* Js = reinterpret_cast<double*>(dyn);                    // [2][npairs][32*32]
+  double* Vs = Js + 2L * npairs * JW * JW;                         // [2][RP_ROWS][ng]
+  const int b = blockIdx.y;
+  const int r0 = blockIdx.x * RP_ROWS;
+  const int rounds = nb - 1;
+  const long total = static_cast<long>(sweeps[b]) * rounds;
+  const double* jb = jrec + b * jstride * npairs * (JW * JW);
+  const unsigned char* fb = jflag + b * jstride * npairs;
+  for (int idx = threadIdx.x; idx < RP_ROWS * ng; idx += JT) {
+    const int rr = idx / ng, c = idx - rr * ng;
+    // start: identity, or the warm-start factor v0 (col-major, ld ng)
+    Vs[idx] = v0 ? v0[static_cast<long>(c) * ng + r0 + rr] : ((r0 + rr == c) ? 1.0 : 0.0);
+  }
+  auto stage = [&](long rg, int s) {
+    double* dst = Js + static_cast<long>(s) * npairs * JW * JW;
+    const double* src = jb + rg * npairs * (JW * JW);
+    for (int idx = threadIdx.x; idx < npairs * JW * JW / 2; idx += JT) {
+      const int p = idx / (JW * JW / 2);
+      cp_async16(dst + 2 * idx, src + 2 * idx, fb[rg * npairs + p] ? 16 : 0);
+    }
+  };
+  if (total > 0) stage(0, 0);
+  cp_commit();
+  int cur = 0;
+  for (long rg = 0; rg < total; ++rg) {
+    if (rg + 1 < total) stage(rg + 1, (rg + 1) & 1);
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    const int r = static_cast<int>(rg % rounds);
+    const double* J = Js + static_cast<long>(rg & 1) * npairs * JW * JW;
+    const double* vin = Vs + cur * RP_ROWS * ng;
+    double* vout = Vs + (cur ^ 1) * RP_ROWS * ng;
+    for (int c = threadIdx.x; c < ng; c += JT) {
+      int p, s;
+      circle_locate(nb, r, c / JB, p, s);
+      int ba, bb;
+      circle_pair_ns(nb, r, p, ba, bb);
+      const int j = s * JB + c % JB;  // pair-local output column
+      double acc[RP_ROWS];
+      if (fb[rg * npairs + p]) {
+        const double* Jp = J + static_cast<long>(p) * JW * JW;
+#pragma unroll
+        for (int rr = 0; rr < RP_ROWS; ++rr) acc[rr] = 0.0;
+#pragma unroll 8
+        for (int k = 0; k < JW; ++k) {
+          const int col = k < JB ? ba * JB + k : bb * JB + k - JB;
+          const double jv = Jp[k * JW + j];
+#pragma unroll
+          for (int rr = 0; rr < RP_ROWS; ++rr) acc[rr] = fma(vin[rr * ng + col], jv, acc[rr]);
+        }
+      } else {
+#pragma unroll
+        for (int rr = 0; rr < RP_ROWS; ++rr) acc[rr] = vin[rr * ng + c];
+      }
+#pragma unroll
+      for (int rr = 0; rr < RP_ROWS; ++rr) vout[rr * ng + c] = acc[rr];
+    }
+    cur ^= 1;
+    __syncthreads();
+  }
+  double* Vb = V + b * vstride;
+  const double* vfin = Vs + cur * RP_ROWS * ng;
+  for (int idx = threadIdx.x; idx < RP_ROWS * ng; idx += JT) {
+    const int rr = idx / ng, c = idx - rr * ng;
+    if (r0 + rr < ng) Vb[static_cast<long>(c) * ng + r0 + rr] = vfin[idx];
+  }
+}
+
+// =============================== STREAM mode ================================
+
+struct PersArgs {
+  double* G;
+  long ldg, gstride;
+  int mg;
+  double* V;  // null: values only
+  long ldv, vstride;
+  int vrows;
+  int nb, npairs, batch0;
+  int max_inner;
+  double tol, stop_tol;
+  const double* zero2;
+  unsigned long long* conv;  // [MAX_SWEEPS] per-sweep max measure (whole launch)
+  int* sweeps_out;
+};
+
+// cp.async chunk loads: rows [r0, r0+64) of the 32 pair columns -> X[col][row]
 __device__ __forceinline__ void load_chunk_async(Chunk& X, const double* M, long ld, int rows, int r0,
                                                  int ca, int cb) {
-  // 32 columns x 32 segments of 16 B
   for (int idx = threadIdx.x; idx < JW * (JCH / 2); idx += JT) {
     const int c = idx / (JCH / 2), seg = idx - c * (JCH / 2);
     const int col = c < JB ? ca + c : cb + c - JB;
     const int r = r0 + 2 * seg;
-    const int valid = rows - r;  // rows (elements) available from r
+    const int valid = rows - r;
     const int bytes = valid >= 2 ? 16 : (valid == 1 ? 8 : 0);
     const double* src = M + col * ld + (bytes ? r : 0);
     cp_async16(&X[c][2 * seg], src, bytes);
@@ -118,15 +570,18 @@ __device__ __forceinline__ void store_chunk(const Chunk& X, double* M, long ld, 
   }
 }
 
-// acc += (32 x 64)^T-tile Gram contribution of chunk X (one 16x8 tile per warp)
 __device__ __forceinline__ void gram_chunk(const Chunk& X, double (&acc)[4]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3, mt = warp >> 2, nt = warp & 3;
+  double acc2[4] = {0, 0, 0, 0};
 #pragma unroll
-  for (int k4 = 0; k4 < JCH / 4; ++k4) {
-    const int k = k4 * 4 + tig;
+  for (int k8 = 0; k8 < JCH / 8; ++k8) {
+    const int k = k8 * 8 + tig;
     mma16x8x4(acc, X[mt * 16 + gid][k], X[mt * 16 + gid + 8][k], X[nt * 8 + gid][k]);
+    mma16x8x4(acc2, X[mt * 16 + gid][k + 4], X[mt * 16 + gid + 8][k + 4], X[nt * 8 + gid][k + 4]);
   }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc[i] += acc2[i];
 }
 
 // X <- X * J in place (rows of the chunk times the 32x32 rotation)
@@ -157,204 +612,6 @@ __device__ __forceinline__ void rotate_chunk(Chunk& X, const Small& sm) {
   __syncthreads();
 }
 
-// two-sided cyclic Jacobi on S (32x32 in smem), accumulating J (starts at I).
-// Each parallel step rotates 16 disjoint pairs; the two-sided update splits
-// into 16x16 independent 2x2 blocks S[{ip,jp},{iq,jq}] <- Rp^T S Rq, one per
-// thread, so a step costs two barriers.  Pair tables are precomputed.
-__device__ void inner_jacobi(Small& sm, double z2, double inv_f2, double tol, int max_inner) {
-  const int t = threadIdx.x;
-  const int bp = t >> 4, bq = t & 15;  // this thread's 2x2 block of S
-  for (int sweep = 0; sweep < max_inner; ++sweep) {
-    if (t == 0) sm.changed = 0;
-    __syncthreads();
-    for (int step = 0; step < JW - 1; ++step) {
-      if (t < JW / 2) {
-        const int i = sm.pi[step][t], j = sm.pj[step][t];
-        const double app = sm.S[i][i], aqq = sm.S[j][j], apq = sm.S[i][j];
-        double c = 1.0, s = 0.0;
-        // rotate iff |apq| > tol sqrt(app aqq).  The angle t = tan(theta) of the
-        // classical Jacobi rotation is computed in FP32 from the scale-free
-        // tau = (aqq - app) / (2 apq) (an approximate angle still gives an exactly
-        // orthogonal rotation; its error only leaves a ~1e-7 relative residue
-        // that later sweeps remove, preserving superlinear convergence); c and
-        // s = t c are then made orthonormal to FP64 precision by two Newton steps
-        // on rsqrt(1 + t^2).  Cuts the serial FP64 sqrt/div chain of every step.
-        if (app > z2 && aqq > z2 && apq * apq > tol * tol * (app * aqq)) {
-          const float zf = static_cast<float>((aqq - app) * inv_f2);
-          const float qf = static_cast<float>(2.0 * apq * inv_f2);
-          const float tau = __fdividef(zf, qf);
-          const float tf = copysignf(1.0f, tau) / (fabsf(tau) + sqrtf(fmaf(tau, tau, 1.0f)));
-          const double td = tf;
-          const double x = fma(td, td, 1.0);
-          double y = rsqrtf(static_cast<float>(x));
-          y = y * (1.5 - 0.5 * x * y * y);
-          y = y * (1.5 - 0.5 * x * y * y);
-          c = y;
-          s = td * y;
-          sm.changed = 1;
-        }
-        sm.cs[t][0] = c;
-        sm.cs[t][1] = s;
-      }
-      __syncthreads();
-      {
-        const int ip = sm.pi[step][bp], jp = sm.pj[step][bp];
-        const int iq = sm.pi[step][bq], jq = sm.pj[step][bq];
-        const double cp = sm.cs[bp][0], sp = sm.cs[bp][1], cq = sm.cs[bq][0], sq = sm.cs[bq][1];
-        if (sp != 0.0 || sq != 0.0) {
-          const double a = sm.S[ip][iq], b = sm.S[ip][jq], c = sm.S[jp][iq], d = sm.S[jp][jq];
-          // columns: (x, y) -> (cq x - sq y, sq x + cq y)
-          const double a1 = cq * a - sq * b, b1 = sq * a + cq * b;
-          const double c1 = cq * c - sq * d, d1 = sq * c + cq * d;
-          // rows: (u, v) -> (cp u - sp v, sp u + cp v)
-          sm.S[ip][iq] = cp * a1 - sp * c1;
-          sm.S[jp][iq] = sp * a1 + cp * c1;
-          sm.S[ip][jq] = cp * b1 - sp * d1;
-          sm.S[jp][jq] = sp * b1 + cp * d1;
-          if (bp == bq && sp != 0.0) {  // the annihilated element (exact zero)
-            sm.S[ip][jq] = 0.0;
-            sm.S[jp][iq] = 0.0;
-          }
-        }
-        // J <- J * R: 32 rows x 16 pairs, two items per thread
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int item = t + h * JT, p = item >> 5, r = item & 31;
-          const double s = sm.cs[p][1];
-          if (s != 0.0) {
-            const int i = sm.pi[step][p], j = sm.pj[step][p];
-            const double c = sm.cs[p][0];
-            const double x = sm.J[r][i], y = sm.J[r][j];
-            sm.J[r][i] = c * x - s * y;
-            sm.J[r][j] = s * x + c * y;
-          }
-        }
-      }
-      __syncthreads();
-    }
-    if (!sm.changed) break;
-    __syncthreads();
-  }
-}
-
-__device__ void init_pair_tables(Small& sm) {
-  for (int idx = threadIdx.x; idx < (JW - 1) * (JW / 2); idx += JT) {
-    const int step = idx / (JW / 2), p = idx - step * (JW / 2);
-    int i, j;
-    circle_pair(JW, step, p, i, j);
-    sm.pi[step][p] = static_cast<unsigned char>(i);
-    sm.pj[step][p] = static_cast<unsigned char>(j);
-  }
-}
-
-// Gram -> measure -> (inner Jacobi).  Returns true when the pair must be rotated.
-__device__ bool finish_gram(Small& sm, const double (&acc)[4], double z2, double inv_f2, const PersArgs& a,
-                            int sweep) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gid = lane >> 2, tig = lane & 3, mt = warp >> 2, nt = warp & 3;
-  {
-    const int r = mt * 16 + gid, c = nt * 8 + 2 * tig;
-    sm.S[r][c] = acc[0];
-    sm.S[r][c + 1] = acc[1];
-    sm.S[r + 8][c] = acc[2];
-    sm.S[r + 8][c + 1] = acc[3];
-  }
-  for (int idx = threadIdx.x; idx < JW * JW; idx += JT) {
-    const int r = idx / JW, c = idx - r * JW;
-    sm.J[r][c] = r == c ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  double meas = 0.0;
-  for (int idx = threadIdx.x; idx < JW * JW; idx += JT) {
-    const int i = idx / JW, j = idx - i * JW;
-    if (i < j && sm.S[i][i] > z2 && sm.S[j][j] > z2)
-      meas = fmax(meas, fabs(sm.S[i][j]) / sqrt(sm.S[i][i] * sm.S[j][j]));
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) meas = fmax(meas, __shfl_xor_sync(0xffffffffu, meas, o));
-  if (lane == 0) sm.red[warp] = meas;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double m = 0;
-    for (int w = 0; w < JT / 32; ++w) m = fmax(m, sm.red[w]);
-    sm.red[0] = m;
-    atomicMax(&a.conv[sweep], static_cast<unsigned long long>(__double_as_longlong(m)));
-  }
-  __syncthreads();
-  const bool rotate = sm.red[0] > a.tol;
-  if (rotate) inner_jacobi(sm, z2, inv_f2, a.tol, a.max_inner);
-  return rotate;
-}
-
-// RESIDENT: the pair's G columns (<= 256 rows) and V columns (<= 256 rows)
-// stay in shared memory for the whole round.
-__global__ void __launch_bounds__(JT, 1) jacobi_resident_kernel(PersArgs a) {
-  extern __shared__ __align__(16) unsigned char dyn[];
-  Chunk* XG = reinterpret_cast<Chunk*>(dyn);
-  Chunk* XV = XG + RES_CHUNKS;
-  Small& sm = *reinterpret_cast<Small*>(XV + RES_CHUNKS);
-  init_pair_tables(sm);
-  __syncthreads();
-  cg::grid_group grid = cg::this_grid();
-  const int p = blockIdx.x % a.npairs, b = a.batch0 + blockIdx.x / a.npairs;
-  double* G = a.G + b * a.gstride;
-  double* V = a.V + b * a.vstride;
-  const double z2 = a.zero2[2 * b], inv_f2 = a.zero2[2 * b + 1];
-  const int ncg = (a.mg + JCH - 1) / JCH, ncv = (a.vrows + JCH - 1) / JCH;
-  int sweep = 0;
-  for (; sweep < MAX_SWEEPS; ++sweep) {
-    for (int round = 0; round < a.nb - 1; ++round) {
-      int ba, bb;
-      circle_pair(a.nb, round, p, ba, bb);
-      const int ca = ba * JB, cb = bb * JB;
-      const bool prof = a.prof && blockIdx.x == 0 && threadIdx.x == 0;
-      long long t0 = prof ? clock64() : 0;
-      for (int k = 0; k < ncg; ++k) load_chunk_async(XG[k], G, a.ldg, a.mg, k * JCH, ca, cb);
-      for (int k = 0; k < ncv; ++k) load_chunk_async(XV[k], V, a.ldv, a.vrows, k * JCH, ca, cb);
-      cp_commit();
-      cp_wait<0>();
-      __syncthreads();
-      long long t1 = prof ? clock64() : 0;
-      double acc[4] = {0, 0, 0, 0};
-      for (int k = 0; k < ncg; ++k) gram_chunk(XG[k], acc);
-      __syncthreads();
-      long long t2 = prof ? clock64() : 0, t3 = 0;
-      if (finish_gram(sm, acc, z2, inv_f2, a, sweep)) {
-        t3 = prof ? clock64() : 0;
-        for (int k = 0; k < ncg; ++k) {
-          rotate_chunk(XG[k], sm);
-          store_chunk(XG[k], G, a.ldg, a.mg, k * JCH, ca, cb);
-        }
-        for (int k = 0; k < ncv; ++k) {
-          rotate_chunk(XV[k], sm);
-          store_chunk(XV[k], V, a.ldv, a.vrows, k * JCH, ca, cb);
-        }
-      } else {
-        t3 = prof ? clock64() : 0;
-      }
-      long long t4 = prof ? clock64() : 0;
-      grid.sync();
-      if (prof) {
-        const long long t5 = clock64();
-        a.prof[0] += t1 - t0;  // load
-        a.prof[1] += t2 - t1;  // gram
-        a.prof[2] += t3 - t2;  // measure + inner Jacobi
-        a.prof[3] += t4 - t3;  // rotate + store
-        a.prof[4] += t5 - t4;  // grid barrier
-        a.prof[5] += 1;
-      }
-    }
-    const double meas = __longlong_as_double(
-        static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(&a.conv[sweep])));
-    if (meas < a.stop_tol) {
-      ++sweep;
-      break;
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *a.sweeps_out = sweep;
-}
-
-// STREAM: 64-row chunks double-buffered through shared memory.
 __device__ void stream_rotate(Chunk* X, double* M, long ld, int rows, int ca, int cb, const Small& sm) {
   const int nch = (rows + JCH - 1) / JCH;
   load_chunk_async(X[0], M, ld, rows, 0, ca, cb);
@@ -379,8 +636,8 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
   cg::grid_group grid = cg::this_grid();
   const int p = blockIdx.x % a.npairs, b = a.batch0 + blockIdx.x / a.npairs;
   double* G = a.G + b * a.gstride;
-  double* V = a.V + b * a.vstride;
-  const double z2 = a.zero2[2 * b], inv_f2 = a.zero2[2 * b + 1];
+  double* V = a.V ? a.V + b * a.vstride : nullptr;
+  const double z2 = a.zero2[2 * b];
   const int nch = (a.mg + JCH - 1) / JCH;
   int sweep = 0;
   for (; sweep < MAX_SWEEPS; ++sweep) {
@@ -399,9 +656,12 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
         gram_chunk(X[k & 1], acc);
         __syncthreads();
       }
-      if (finish_gram(sm, acc, z2, inv_f2, a, sweep)) {
+      const bool rot = finish_gram(sm, acc, z2, a.tol, a.max_inner);
+      if (threadIdx.x == 0)
+        atomicMax(&a.conv[sweep], static_cast<unsigned long long>(__double_as_longlong(sm.red[0])));
+      if (rot) {
         stream_rotate(X, G, a.ldg, a.mg, ca, cb, sm);
-        stream_rotate(X, V, a.ldv, a.vrows, ca, cb, sm);
+        if (V) stream_rotate(X, V, a.ldv, a.vrows, ca, cb, sm);
       }
       grid.sync();
     }
@@ -474,7 +734,7 @@ __global__ void zero_floor_kernel(const double* __restrict__ G, long gstride, lo
     for (int w = 0; w < (blockDim.x >> 5); ++w) t += sh[w];
     const double f = 64.0 * sqrt(static_cast<double>(mg)) * EPS;
     zero2[2 * blockIdx.x] = f * f * t;
-    zero2[2 * blockIdx.x + 1] = t > 0 ? 1.0 / t : 1.0;  // 1 / ||G||_F^2 (scale-free angles)
+    zero2[2 * blockIdx.x + 1] = t > 0 ? 1.0 / t : 1.0;  // 1 / ||G||_F^2
   }
 }
 
@@ -564,13 +824,20 @@ __global__ void gather_kernel(const double* __restrict__ G, long ldg, const doub
   }
 }
 
-size_t resident_smem() { return sizeof(Chunk) * 2 * RES_CHUNKS + sizeof(Small) + 16; }
 size_t stream_smem() { return sizeof(Chunk) * 2 + sizeof(Small) + 16; }
+size_t cluster_smem(int rows_pad) {
+  return sizeof(double) * 2 * JW * (rows_pad + 4) + sizeof(Small) + 16;
+}
+size_t replay_smem(int npairs, int ng) {
+  return sizeof(double) * (2L * npairs * JW * JW + 2L * RP_ROWS * ng);
+}
 
 }  // namespace
 
 SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, int m_true,
-                        int n_true, SvdSide side, int batch, long bstride, double* sigma_out) {
+                        int n_true, SvdSide side, int batch, long bstride, double* sigma_out,
+                        bool want_vectors, const double* v_init) {
+  if (v_init && (batch != 1 || !want_vectors)) fail(ACHI_E_INTERNAL, "svd: warm start needs batch 1 with vectors");
   const bool rows = side == SvdSide::kRows;
   const int ng_real = rows ? m : n;
   const int mg = rows ? n : m;
@@ -578,43 +845,44 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   const int ng = ((ng_real + JW - 1) / JW) * JW;
   const long gstride = ldg * ng, vstride = static_cast<long>(ng) * ng;
   double* G = ws.G.reserve(static_cast<size_t>(gstride) * batch);
-  double* V = ws.V.reserve(static_cast<size_t>(vstride) * batch);
+  double* V = want_vectors ? ws.V.reserve(static_cast<size_t>(vstride) * batch) : nullptr;
   double* sig = ws.sig.reserve(static_cast<size_t>(ng) * batch);
   double* sorted = ws.sorted.reserve(static_cast<size_t>(ng) * batch);
   int* perm = ws.perm.reserve(static_cast<size_t>(ng) * batch);
   unsigned long long* conv = ws.conv.reserve(MAX_SWEEPS * 8);
   double* zero2 = ws.zero2.reserve(2 * static_cast<size_t>(batch));
-  int* sweeps_dev = ws.sweeps.reserve(64);
-  int* sweeps_host = ws.sweeps_host.reserve(64);
+  const int nsw = std::max(64, batch);
+  int* sweeps_dev = ws.sweeps.reserve(nsw);
+  int* sweeps_host = ws.sweeps_host.reserve(nsw);
+  const int nb = ng / JB;  // even (ng multiple of 32)
+  const int npairs = nb / 2;
+  const bool cluster = ldg <= CL_ROWS && npairs <= CL_MAXP;
   {
     dim3 grid(cdiv(ng, 32), cdiv(ldg, 32), batch), blk(32, 8);
     load_g_kernel<<<grid, blk, 0, ctx.stream>>>(theta, bstride, m, n, G, gstride, ldg, mg, ng,
                                                 rows ? 1 : 0);
     ACHI_LAUNCHED(ctx);
-    dim3 g2(static_cast<unsigned>(std::min<long>(cdiv(vstride, 256), 4L * ctx.num_sms)), batch);
-    identity_kernel<<<g2, 256, 0, ctx.stream>>>(V, ng, ng, vstride);
-    ACHI_LAUNCHED(ctx);
+    if (V && !cluster) {
+      if (v_init) {
+        ACHI_CUDA(cudaMemcpyAsync(V, v_init, sizeof(double) * vstride, cudaMemcpyDeviceToDevice,
+                                  ctx.stream));
+      } else {
+        dim3 g2(static_cast<unsigned>(std::min<long>(cdiv(vstride, 256), 4L * ctx.num_sms)), batch);
+        identity_kernel<<<g2, 256, 0, ctx.stream>>>(V, ng, ng, vstride);
+        ACHI_LAUNCHED(ctx);
+      }
+    }
     zero_floor_kernel<<<batch, 1024, 0, ctx.stream>>>(G, gstride, gstride, mg, zero2);
     ACHI_LAUNCHED(ctx);
+    if (v_init) {
+      // G <- G v_init: col-major G (ldg x ng) is row-major G^T, so (G v)^T = v^T G^T
+      // with v^T row-major = v col-major (K-major A) and G^T K x N row-major (MN-major B)
+      double* Gw = ws.Gw.reserve(static_cast<size_t>(gstride));
+      gemm(ctx, ng, static_cast<int>(ldg), ng, Operand{v_init, ng, Major::kK},
+           Operand{G, ldg, Major::kMN}, Gw, ldg);
+      G = Gw;
+    }
   }
-  const int nb = ng / JB;  // even (ng multiple of 32)
-  const int npairs = nb / 2;
-  const bool resident = ldg <= RES_CHUNKS * JCH && ng <= RES_CHUNKS * JCH;
-  const size_t smem = resident ? resident_smem() : stream_smem();
-  void* kern = resident ? reinterpret_cast<void*>(jacobi_resident_kernel)
-                        : reinterpret_cast<void*>(jacobi_stream_kernel);
-  static int max_blocks[2] = {0, 0};
-  int& mb = max_blocks[resident ? 0 : 1];
-  if (mb == 0) {
-    ACHI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    int per_sm = 0;
-    ACHI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, JT, smem));
-    mb = per_sm * ctx.num_sms;
-    if (mb < 1) fail(ACHI_E_CUDA, "svd: Jacobi kernel cannot be resident");
-  }
-  if (npairs > mb) fail(ACHI_E_SIZE_GUARD, "svd: matrix too wide for one cooperative launch");
-  const int per_launch = std::max(1, mb / npairs);
   const double tol = std::max(1e-15, 2.0 * std::sqrt(static_cast<double>(mg)) * EPS);
   // inner sweeps per block pair and the outer stop threshold (measure of the
   // last sweep; off-diagonals after it are ~measure^2).  Tunable for studies.
@@ -627,30 +895,92 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     return e ? std::atof(e) : 1e-7;
   }();
   int launches = 0;
-  for (int b0 = 0; b0 < batch; b0 += per_launch, ++launches) {
-    const int nbat = std::min(per_launch, batch - b0);
-    ACHI_CUDA(cudaMemsetAsync(conv, 0, sizeof(unsigned long long) * MAX_SWEEPS, ctx.stream));
-    PersArgs a{G, ldg, gstride, mg, V, ng, vstride, ng, nb, npairs, b0,
-               max_inner, tol, stop_tol, zero2, conv, sweeps_dev + (launches % 64), nullptr};
+  if (cluster) {
+    const int rows_pad = static_cast<int>(((ldg + 15) / 16) * 16);
+    const size_t smem = cluster_smem(rows_pad);
+    static bool attr = false;
+    if (!attr) {
+      ACHI_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(cluster_smem(CL_ROWS))));
+      attr = true;
+    }
+    const long jstride = static_cast<long>(MAX_SWEEPS) * (nb - 1);
+    double* jrec = nullptr;
+    unsigned char* jflag = nullptr;
+    if (V) {
+      jrec = ws.jrec.reserve(static_cast<size_t>(batch) * jstride * npairs * JW * JW);
+      jflag = ws.jflag.reserve(static_cast<size_t>(batch) * jstride * npairs);
+    }
+    ClArgs a{G, ldg, gstride, mg, rows_pad, nb, npairs, max_inner, tol, stop_tol, zero2,
+             jrec, jflag, jstride, sweeps_dev, nullptr};
     static const bool prof_on = std::getenv("ACHI_JACOBI_PROF") != nullptr;
     static DevArr<long long> profbuf;
     if (prof_on) {
       a.prof = profbuf.reserve(8);
       ACHI_CUDA(cudaMemsetAsync(a.prof, 0, 8 * sizeof(long long), ctx.stream));
     }
-    void* args[] = {&a};
-    ACHI_CUDA(cudaLaunchCooperativeKernel(kern, dim3(npairs * nbat), dim3(JT), args, smem, ctx.stream));
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(npairs * batch);
+    lc.blockDim = dim3(JT);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = ctx.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = npairs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    ACHI_CUDA(cudaLaunchKernelEx(&lc, jacobi_cluster_kernel, a));
     ACHI_LAUNCHED(ctx);
     if (prof_on) {
       long long h[8];
       ACHI_CUDA(cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
       ctx.sync();
-      const double r = h[5] > 0 ? static_cast<double>(h[5]) : 1.0;
+      const double rr = h[5] > 0 ? static_cast<double>(h[5]) : 1.0;
       std::fprintf(stderr,
-                   "[jacobi] n=%d rounds=%lld cycles/round: load %.0f gram %.0f inner %.0f rotate %.0f "
-                   "barrier %.0f\n",
-                   ng, h[5], h[0] / r, h[1] / r, h[2] / r, h[3] / r, h[4] / r);
+                   "[jacobi-cluster] ng=%d rows=%d rounds=%lld rotated=%lld cycles/round: gram %.0f "
+                   "inner %.0f jrec %.0f rotate %.0f barrier %.0f\n",
+                   ng, rows_pad, h[5], h[6], h[0] / rr, h[1] / rr, h[2] / rr, h[3] / rr, h[4] / rr);
     }
+    launches = std::min(batch, nsw);
+    if (V) {
+      const size_t rs = replay_smem(npairs, ng);
+      static bool rattr = false;
+      if (!rattr) {
+        ACHI_CUDA(cudaFuncSetAttribute(v_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(replay_smem(CL_MAXP, CL_MAXP * JW))));
+        rattr = true;
+      }
+      dim3 grid(cdiv(ng, RP_ROWS), batch);
+      v_replay_kernel<<<grid, JT, rs, ctx.stream>>>(V, vstride, ng, nb, npairs, jrec, jflag, jstride,
+                                                    sweeps_dev, v_init);
+      ACHI_LAUNCHED(ctx);
+    }
+  } else {
+    const size_t smem = stream_smem();
+    void* kern = reinterpret_cast<void*>(jacobi_stream_kernel);
+    static int mb = 0;
+    if (mb == 0) {
+      ACHI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+      int per_sm = 0;
+      ACHI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, JT, smem));
+      mb = per_sm * ctx.num_sms;
+      if (mb < 1) fail(ACHI_E_CUDA, "svd: Jacobi kernel cannot be resident");
+    }
+    if (npairs > mb) fail(ACHI_E_SIZE_GUARD, "svd: matrix too wide for one cooperative launch");
+    const int per_launch = std::max(1, mb / npairs);
+    for (int b0 = 0; b0 < batch; b0 += per_launch, ++launches) {
+      const int nbat = std::min(per_launch, batch - b0);
+      ACHI_CUDA(cudaMemsetAsync(conv, 0, sizeof(unsigned long long) * MAX_SWEEPS, ctx.stream));
+      PersArgs a{G, ldg, gstride, mg, V, ng, vstride, ng, nb, npairs, b0,
+                 max_inner, tol, stop_tol, zero2, conv, sweeps_dev + (launches % nsw)};
+      void* args[] = {&a};
+      ACHI_CUDA(cudaLaunchCooperativeKernel(kern, dim3(npairs * nbat), dim3(JT), args, smem, ctx.stream));
+      ACHI_LAUNCHED(ctx);
+    }
+    launches = std::min(launches, nsw);
   }
   // pad columns: rows side -> columns >= m_true (theta rows (l,s1), padded l last);
   // cols side with padding -> columns (s2, jr) with jr >= chr_true (d = 2 on the padded path)
@@ -667,8 +997,8 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     sort_kernel<<<batch, 1024, sizeof(double) * ng, ctx.stream>>>(sig, ng, ng, sorted, perm);
     ACHI_LAUNCHED(ctx);
   }
-  ACHI_CUDA(cudaMemcpyAsync(sweeps_host, sweeps_dev, sizeof(int) * std::min(launches, 64),
-                            cudaMemcpyDeviceToHost, ctx.stream));
+  ACHI_CUDA(cudaMemcpyAsync(sweeps_host, sweeps_dev, sizeof(int) * launches, cudaMemcpyDeviceToHost,
+                            ctx.stream));
   const int r_true = std::min(m_true, n_true);
   if (sigma_out) {
     ACHI_CUDA(cudaMemcpy2DAsync(sigma_out, sizeof(double) * r_true, sorted, sizeof(double) * ng,
@@ -684,7 +1014,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   r.mg = static_cast<int>(ldg);
   r.r_true = r_true;
   r.sweeps_host = sweeps_host;
-  r.n_launches = std::min(launches, 64);
+  r.n_launches = launches;
   r.G = G;
   r.V = V;
   r.sigma = sorted;

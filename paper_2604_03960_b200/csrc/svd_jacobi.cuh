@@ -15,7 +15,9 @@
 namespace achi {
 
 struct SvdWs {
-  DevBuf G, V, sig, sorted, zero2;
+  DevBuf G, Gw, V, sig, sorted, zero2;  // Gw: G * v_init (warm start)
+  DevBuf jrec;                  // cluster mode: recorded block rotations (V replay)
+  DevArr<unsigned char> jflag;
   DevArr<int> perm;
   DevArr<double> sign;
   DevArr<unsigned long long> conv;
@@ -47,9 +49,24 @@ struct SvdResultDev {
 
 // SVD of theta (m x n row-major, ld = n, padded; true dims m_true x n_true).
 // Batched over `batch` matrices at stride `bstride` (sigma only for batch > 1).
+// want_vectors = false skips the V accumulation (singular values only).
+// v_init (batch 1 only, may be null): an orthogonal ng x ng matrix (col-major,
+// ld ng) to start from: the iteration runs on G v_init and V accumulates from
+// v_init.  Any orthogonal start gives the same decomposition; the chain passes
+// the factor of the previous visit of the same bond and direction, which
+// nearly diagonalises the new block once the state has converged (fewer
+// sweeps).  v_init must keep pad columns fixed (it does when it comes from a
+// decomposition of the same padded shape).
 SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, int m_true,
                         int n_true, SvdSide side, int batch = 1, long bstride = 0,
-                        double* sigma_out = nullptr);
+                        double* sigma_out = nullptr, bool want_vectors = true,
+                        const double* v_init = nullptr);
+
+// working-matrix width (columns of G and order of V) for a theta of m x n
+inline int svd_working_cols(int m, int n, SvdSide side) {
+  const int c = side == SvdSide::kRows ? m : n;
+  return ((c + 31) / 32) * 32;
+}
 
 // fix_phases signs for the first `kept` vectors on the accurate side (U for
 // kRows, computed from G for kCols): writes ws.sign[0..kept).

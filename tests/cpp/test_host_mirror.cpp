@@ -294,7 +294,11 @@ static void test_dmrg(double e_heis8, double e_tfim8) {
   {  // test_dmrg.cpp:136
     auto r1 = dmrg::run_dmrg(heisenberg(8, models::SpinConvention::pauli), adaptive_config(32));
     for (const auto& s : r1.sweeps) CHECK(s.energy >= e_heis8 - 1e-9);
-    auto r2 = dmrg::run_dmrg(tfim(8, 1.0), adaptive_config(32));
+    // the reference's automatic start for TFIM is a random complex MPS
+    // (dmrg.cpp:230-236), which the real FP64 device path rejects; start from Neel
+    auto tc = adaptive_config(32);
+    tc.initial_state = dmrg::DmrgConfig::InitialState::neel;
+    auto r2 = dmrg::run_dmrg(tfim(8, 1.0), tc);
     for (const auto& s : r2.sweeps) CHECK(s.energy >= e_tfim8 - 1e-9);
   }
   {  // test_dmrg.cpp:144, 254, 270

@@ -105,7 +105,11 @@ def test_env_updates_match_oracle(ctx, oracle, chl, chn):
 # ---------------- K6: SVD ----------------
 
 @pytest.mark.parametrize("shape", [(2, 2), (8, 8), (6, 3), (3, 6), (1, 5), (5, 1), (12, 9),
-                                   (64, 64), (100, 37), (96, 256), (512, 512)])
+                                   (64, 64), (100, 37), (96, 256), (512, 512),
+                                   # cluster-mode edges: one block pair, C3-sized, the
+                                   # 256x256 limit, and just past it (stream mode)
+                                   (32, 32), (33, 40), (200, 218), (256, 256), (257, 256),
+                                   (256, 300)])
 def test_svd_matches_oracle(ctx, oracle, shape):
     rng = np.random.default_rng(sum(shape))
     m = rng.standard_normal(shape)
@@ -140,11 +144,31 @@ def test_svd_known_answers(ctx):  # test_linalg.cpp:38-55
 
 def test_svd_batched(ctx, oracle):
     rng = np.random.default_rng(11)
-    a = rng.standard_normal((4, 128, 128))
-    s = ctx.svd_batched(a)
-    for i in range(4):
-        so = oracle.svd(a[i])[1]
-        assert np.abs(s[i] - so).max() <= 1e-11 * so[0]
+    for shape in ((4, 128, 128), (3, 256, 200), (2, 300, 300)):
+        a = rng.standard_normal(shape)
+        s = ctx.svd_batched(a)
+        for i in range(shape[0]):
+            so = oracle.svd(a[i])[1]
+            assert np.abs(s[i] - so).max() <= 1e-11 * so[0]
+
+
+@pytest.mark.parametrize("m,n,rank", [(218, 218, 218), (218, 218, 150), (100, 180, 60), (256, 256, 7)])
+def test_svd_graded_rank_deficient(ctx, oracle, m, n, rank):
+    """DMRG-like spectra: singular values decaying over 14 decades, exact rank deficiency."""
+    rng = np.random.default_rng(m + n + rank)
+    qa, _ = np.linalg.qr(rng.standard_normal((m, rank)))
+    qb, _ = np.linalg.qr(rng.standard_normal((n, rank)))
+    sv = 10.0 ** -np.linspace(0, 14, rank)
+    a = (qa * sv) @ qb.T
+    u, s, vt, _ = ctx.svd_full(a)
+    so = oracle.svd(a)[1]
+    k = min(m, n)
+    assert np.abs(s - so).max() <= 1e-11 * so[0]
+    assert np.linalg.norm(a - (u * s) @ vt) <= 1e-12 * np.linalg.norm(a)
+    big = s > 1e-8 * s[0]  # vectors of the resolved part are orthonormal
+    assert np.abs(u[:, big].T @ u[:, big] - np.eye(int(big.sum()))).max() <= 1e-10
+    assert np.abs(vt[big] @ vt[big].T - np.eye(int(big.sum()))).max() <= 1e-10
+    assert s.shape == (k,)
 
 
 # ---------------- K7: fused bond select / controller ----------------
@@ -345,3 +369,21 @@ def test_dmrg_modes_parity(ctx, oracle, case):
     gt = [(t.chi, t.delta_chi, t.clamped) for t in g["trace"]]
     ot = [(t.chi, t.delta_chi, t.clamped) for t in o["trace"]]
     assert gt == ot
+
+
+def test_svd_device_factors(ctx, oracle):
+    """achi_svd_device (device pointers, U / sigma / V^T): the bench's truncated-SVD path."""
+    import torch
+    for m, n in ((200, 200), (300, 260)):
+        rng = np.random.default_rng(m * n)
+        a_h = rng.standard_normal((m, n))
+        k = min(m, n)
+        a = torch.from_numpy(a_h).cuda()
+        s = torch.empty(k, dtype=torch.float64, device="cuda")
+        u = torch.empty(m, k, dtype=torch.float64, device="cuda")
+        vt = torch.empty(k, n, dtype=torch.float64, device="cuda")
+        ctx.svd_device(a.data_ptr(), m, n, s.data_ptr(), u.data_ptr(), vt.data_ptr())
+        s_h, u_h, vt_h = s.cpu().numpy(), u.cpu().numpy(), vt.cpu().numpy()
+        so = oracle.svd(a_h)[1]
+        assert np.abs(s_h - so).max() <= 1e-11 * so[0]
+        assert np.linalg.norm(a_h - (u_h * s_h) @ vt_h) <= 1e-12 * np.linalg.norm(a_h)
