@@ -231,14 +231,19 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   // algorithmic FP64 flops of one matvec: 2 D d^2 chl chr (chl+chr) + 4 D^2 d^3 chl chr
   const double D = mpo[b].r;
   const double mv_flops = 2.0 * D * d * d * chl * chr * (chl + chr) + 4.0 * D * D * d * d * d * chl * chr;
+  // The inner Lanczos loop is a cached CUDA graph per (bond, direction); its key
+  // covers everything the captured matvec depends on (shapes and buffers).
+  uint64_t key = 1469598103934665603ull;
+  for (uint64_t v : {static_cast<uint64_t>(b), static_cast<uint64_t>(chlp), static_cast<uint64_t>(chrp),
+                     reinterpret_cast<uint64_t>(L[b].p), reinterpret_cast<uint64_t>(R[b + 1].p),
+                     reinterpret_cast<uint64_t>(c.ws_a.p), reinterpret_cast<uint64_t>(c.ws_b.p),
+                     reinterpret_cast<uint64_t>(c.ws_split.p)})
+    key = (key ^ v) * 1099511628211ull;
+  c.acc.begin(EventAcc::kMatvec, c.stream);  // the whole eigensolve (matvecs + orthogonalisation)
   EigsOut eig = eigs_lowest(
-      c, lz,
-      [&](const double* in, double* out) {
-        c.acc.begin(EventAcc::kMatvec, c.stream);
-        heff_apply(c, op, in, out);
-        c.acc.end(c.stream, mv_flops);
-      },
-      nvec, dim, theta.p, cfg.eig_tol, cfg.eig_max_iter, vec.p);
+      c, lz, [&](const double* in, double* out) { heff_apply(c, op, in, out); }, nvec, dim, theta.p,
+      cfg.eig_tol, cfg.eig_max_iter, vec.p, 2 * b + (right ? 1 : 0), key);
+  c.acc.end(c.stream, eig.matvecs * mv_flops);
   const auto t1 = clk::now();
   const SvdSide side = right ? SvdSide::kRows : SvdSide::kCols;
   c.acc.begin(EventAcc::kSvd, c.stream);

@@ -72,7 +72,10 @@ void launch(Ctx& ctx, int M, int N, int K, const Operand& A, const Operand& B, d
     return;
   }
   const long slab = static_cast<long>(M) * N;
-  double* ws = ctx.ws_split.reserve(static_cast<size_t>(slab) * splits);
+  // slab * splits <= 4096 (296 + tiles) < 4096 * 592 on this path (dispatch
+  // below): reserving that bound once keeps the buffer (and every captured
+  // graph that uses it) stable
+  double* ws = ctx.ws_split.reserve(std::max<size_t>(static_cast<size_t>(slab) * splits, 4096UL * 592));
   kern<<<grid, G::THREADS, G::SMEM, ctx.stream>>>(ma, mb, ws, N, slab, M, N, K, kt_per);
   ACHI_LAUNCHED(ctx);
   const int blocks = std::min<long>(cdiv(slab, 256), 4L * ctx.num_sms);

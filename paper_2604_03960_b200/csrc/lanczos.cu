@@ -3,6 +3,7 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <limits>
 
 #include "lanczos.cuh"
@@ -148,94 +149,77 @@ __global__ void scale_kernel(double* __restrict__ dst, const double* __restrict_
 }
 
 // ---- tridiagonal lowest eigenpair (Eigen computeFromTridiagonal, col 0) ----
-// Bisection on Sturm counts for the smallest eigenvalue, then inverse
-// iteration with partially pivoted tridiagonal elimination (dgtsv scheme).
-__device__ int sturm_count(const double* a, const double* b, int k, double x) {
-  int cnt = 0;
-  double q = a[0] - x;
-  const double tiny = 1e-300;
-  if (q < 0) ++cnt;
-  for (int i = 1; i < k; ++i) {
-    if (fabs(q) < tiny) q = -tiny;
-    q = (a[i] - x) - b[i - 1] * b[i - 1] / q;
-    if (q < 0) ++cnt;
+// The Lanczos tridiagonal T (k <= 48, a = alpha, b = beta, bb = beta^2) is
+// solved by block 0 of the fused step kernel: multisection on Sturm counts
+// for the lowest eigenvalue (bracketed with the previous step's Ritz value),
+// then a twisted factorization for the eigenvector.  Every sequential chain
+// is a division-free FMA recurrence; divisions only happen in parallel across
+// lanes.
+
+// exact power of two 2^e (|e| < 1000)
+__device__ __forceinline__ double pow2(int e) {
+  return __longlong_as_double(static_cast<long long>(1023 + e) << 52);
+}
+// binary exponent of |m| (m > 0, normal)
+__device__ __forceinline__ int exponent_of(double m) {
+  return static_cast<int>((__double_as_longlong(m) >> 52) & 0x7ff) - 1023;
+}
+
+// Sturm count (number of eigenvalues below x) from the characteristic-
+// polynomial recurrence p_{i+1} = (a_i - x) p_i - bb_{i-1} p_{i-1}, p_0 = 1:
+// the sign changes of p_0..p_k (a zero takes the sign +, counting a root of a
+// leading minor once).  One dependent FMA per step, no division; operands
+// are loaded 8 steps ahead and p is rescaled by an exact power of two, so it
+// neither overflows nor underflows.
+__device__ int sturm_count(const double* a, const double* bb, int k, double x) {
+  double pm = 1.0, p = a[0] - x;
+  int cnt = p < 0.0 ? 1 : 0;
+  for (int i0 = 1; i0 < k; i0 += 8) {
+    double da[8], db[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u;
+      da[u] = i < k ? a[i] - x : 0.0;
+      db[u] = i < k ? bb[i - 1] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (i0 + u < k) {
+        const double pn = fma(da[u], p, -db[u] * pm);
+        cnt += (pn < 0.0) != (p < 0.0) ? 1 : 0;
+        pm = p;
+        p = pn;
+      }
+    }
+    const double m = fmax(fabs(p), fabs(pm));
+    const int e = exponent_of(m);
+    if (m > 0.0 && (e > 64 || e < -64)) {
+      const double f = pow2(-e);
+      p *= f;
+      pm *= f;
+    }
   }
   return cnt;
 }
 
-// Eigenvector of the k x k tridiagonal for the eigenvalue theta by inverse
-// iteration (partially pivoted elimination, dgtsv scheme), unit norm, first
-// nonzero component positive.
-__device__ void tridiag_vector_from_theta(const double* a, const double* b, int k, double theta,
-                                          double scale, double* s) {
-  double dd[LANCZOS_BLOCK], du[LANCZOS_BLOCK], dl[LANCZOS_BLOCK], x[LANCZOS_BLOCK];
-  const double tiny = (scale > 0 ? scale : 1.0) * 1e-300 + 1e-300;
-  const double pivmin = (scale > 0 ? scale : 1.0) * 2.3e-16;
-  // generic deterministic start (a symmetric start can be an exact eigenvector)
-  for (int i = 0; i < k; ++i) x[i] = 1.0 + 0.5 * sin(1.0 + 2.3 * i);
-  for (int iter = 0; iter < 2; ++iter) {
-    for (int i = 0; i < k; ++i) dd[i] = a[i] - theta;
-    for (int i = 0; i + 1 < k; ++i) dl[i] = du[i] = b[i];
-    for (int i = 0; i + 1 < k; ++i) {
-      if (fabs(dd[i]) >= fabs(dl[i])) {
-        if (fabs(dd[i]) < pivmin) dd[i] = dd[i] >= 0 ? pivmin : -pivmin;
-        const double f = dl[i] / dd[i];
-        dd[i + 1] -= f * du[i];
-        x[i + 1] -= f * x[i];
-        dl[i] = 0.0;
-      } else {
-        const double f = dd[i] / dl[i];
-        dd[i] = dl[i];
-        const double t = dd[i + 1];
-        dd[i + 1] = du[i] - f * t;
-        if (i + 2 < k) {
-          dl[i] = du[i + 1];
-          du[i + 1] = -f * dl[i];
-        } else {
-          dl[i] = 0.0;
-        }
-        du[i] = t;
-        const double tx = x[i];
-        x[i] = x[i + 1];
-        x[i + 1] = tx - f * x[i + 1];
-      }
-    }
-    if (fabs(dd[k - 1]) < pivmin) dd[k - 1] = dd[k - 1] >= 0 ? pivmin : -pivmin;
-    x[k - 1] /= dd[k - 1];
-    x[k - 2] = (x[k - 2] - du[k - 2] * x[k - 1]) / dd[k - 2];
-    for (int i = k - 3; i >= 0; --i) x[i] = (x[i] - du[i] * x[i + 1] - dl[i] * x[i + 2]) / dd[i];
-    double nrm = 0;
-    for (int i = 0; i < k; ++i) nrm += x[i] * x[i];
-    nrm = sqrt(nrm);
-    if (!(nrm > tiny)) nrm = 1.0;
-    for (int i = 0; i < k; ++i) x[i] /= nrm;
-  }
-  // deterministic sign: first nonzero component positive
-  double sg = 1.0;
-  for (int i = 0; i < k; ++i)
-    if (x[i] != 0.0) { sg = x[i] > 0 ? 1.0 : -1.0; break; }
-  for (int i = 0; i < k; ++i) s[i] = sg * x[i];
-}
-
-// Warp version: 32-point multisection on Sturm counts (one point per lane,
-// ~11 rounds to machine precision instead of ~60 serial bisection steps),
-// then inverse iteration on lane 0.  Called by all 32 lanes of one warp.
-__device__ void tridiag_lowest_warp(const double* a, const double* b, int k, double* theta_out,
-                                    double* s) {
+// Lowest eigenvalue by 32-point multisection on Sturm counts (one point per
+// lane; all 32 lanes of one warp).  With a hint (the previous step's Ritz
+// value theta_prev and residual bound r_prev) the first round searches
+// [theta_prev - 2 r_prev, theta_prev]: by interlacing the new lowest value is
+// not above theta_prev and the residual theorem puts an eigenvalue within
+// r_prev of it; the count at the lower end verifies that it is the lowest
+// (otherwise the Gershgorin interval is searched).  Returns the upper end of
+// the final bracket; *scale_out = Gershgorin scale.
+__device__ double tridiag_lowest_value(const double* sa, const double* sb, const double* sbb, int k,
+                                       bool hinted, double theta_prev, double r_prev,
+                                       double* scale_out) {
   const int lane = threadIdx.x & 31;
-  if (k == 1) {
-    if (lane == 0) {
-      *theta_out = a[0];
-      s[0] = 1.0;
-    }
-    return;
-  }
   double lo = INFINITY, hi = -INFINITY, scale = 0.0;
   for (int i = lane; i < k; i += 32) {
-    const double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i + 1 < k ? fabs(b[i]) : 0.0);
-    lo = fmin(lo, a[i] - r);
-    hi = fmax(hi, a[i] + r);
-    scale = fmax(scale, fabs(a[i]) + r);
+    const double r = (i > 0 ? fabs(sb[i - 1]) : 0.0) + (i + 1 < k ? fabs(sb[i]) : 0.0);
+    lo = fmin(lo, sa[i] - r);
+    hi = fmax(hi, sa[i] + r);
+    scale = fmax(scale, fabs(sa[i]) + r);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -243,11 +227,28 @@ __device__ void tridiag_lowest_warp(const double* a, const double* b, int k, dou
     hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
   }
+  *scale_out = scale;
+  if (hinted) {
+    const double pad = 4.0 * 2.3e-16 * scale;
+    const double th = fmin(hi, theta_prev + pad);
+    const double tl = fmax(lo, theta_prev - 2.0 * r_prev - pad);
+    if (th > tl) {
+      const double x = lane == 31 ? th : tl + lane * ((th - tl) / 31.0);
+      const unsigned has = __ballot_sync(0xffffffffu, sturm_count(sa, sbb, k, x) >= 1);
+      if ((has & 1u) == 0u && (has >> 31) != 0u) {  // count(tl) = 0 < count(th): valid bracket
+        const int f = __ffs(has) - 1;
+        lo = __shfl_sync(0xffffffffu, x, f - 1);
+        hi = __shfl_sync(0xffffffffu, x, f);
+      } else if ((has >> 31) != 0u) {
+        hi = th;
+      }
+    }
+  }
   for (int round = 0; round < 40; ++round) {
     const double w = hi - lo;
     if (!(w > 2.3e-16 * fmax(fabs(lo), fabs(hi)))) break;
     const double x = lo + (lane + 1) * (w / 33.0);
-    const unsigned has = __ballot_sync(0xffffffffu, sturm_count(a, b, k, x) >= 1);
+    const unsigned has = __ballot_sync(0xffffffffu, sturm_count(sa, sbb, k, x) >= 1);
     const double nlo = has == 0u ? __shfl_sync(0xffffffffu, x, 31)
                                  : (__ffs(has) >= 2 ? __shfl_sync(0xffffffffu, x, __ffs(has) - 2) : lo);
     const double nhi = has == 0u ? hi : __shfl_sync(0xffffffffu, x, __ffs(has) - 1);
@@ -255,36 +256,128 @@ __device__ void tridiag_lowest_warp(const double* a, const double* b, int k, dou
     lo = nlo;
     hi = nhi;
   }
-  if (lane == 0) {
-    tridiag_vector_from_theta(a, b, k, hi, scale, s);
-    *theta_out = hi;
-  }
+  return hi;
 }
 
-// After CGS2: alpha[j] = h1[j]; beta[j] = sqrt(sum partials); tridiagonal solve.
-__global__ void __launch_bounds__(RED_THREADS) finish_step_kernel(
-    const double* __restrict__ partials, int nblocks, double* alpha, double* beta,
-    const double* h1, double* s, int j, LanczosStatus* st) {
-  __shared__ double sh[32];
-  __shared__ double bn_s;
-  double v = 0.0;
-  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) v += partials[b];
-  v = block_sum(v, sh);
-  if (threadIdx.x == 0) {
-    bn_s = sqrt(v);
-    alpha[j] = h1[j];
-    beta[j] = bn_s;
+// Eigenvector for an eigenvalue theta at the bottom of the spectrum by a
+// twisted factorization (the MRRR eigenvector kernel).  The top-down and
+// bottom-up pivots d+_i = P_{i+1}/P_i and d-_i = Q_i/Q_{i+1} come from the
+// polynomial recurrences P (top-down minors of T - theta) and Q (bottom-up
+// minors), run as division-free FMA chains on thread 0 and thread 32 at the
+// same time (stored as value and power-of-two exponent).  Both pivot
+// sequences are positive away from the end they approach because every
+// leading and trailing principal submatrix has its lowest eigenvalue above
+// theta.  Twist r = argmin |gamma_r|, gamma_r = d+_r + d-_r - (a_r - theta);
+// x_r = 1, x_i = -(b_i / d+_i) x_{i+1} (i < r), x_i = -(b_{i-1} / d-_i) x_{i-1}
+// (i > r): the ratios are formed in parallel, the two products are again two
+// concurrent chains.  Unit norm, first nonzero component positive.  Called by
+// every thread of the block (>= 2 warps).
+struct TwistScratch {
+  double pv[LANCZOS_BLOCK + 1], qv[LANCZOS_BLOCK + 1], x[LANCZOS_BLOCK];
+  int pe[LANCZOS_BLOCK + 1], qe[LANCZOS_BLOCK + 1];
+  int r;
+};
+
+__device__ void tridiag_vector_twisted(const double* a, const double* b, const double* bb, int k,
+                                       double theta, double scale, TwistScratch& w, double* s) {
+  const int t = threadIdx.x, lane = t & 31;
+  const double pivmin = (scale > 0 ? scale : 1.0) * 2.3e-16;
+  if (t == 0 || t == 32) {
+    // t == 0: P_0 = 1, P_1 = a_0 - theta, P_{i+1} = (a_i - theta) P_i - bb_{i-1} P_{i-1}
+    // t == 32: Q_k = 1, Q_{k-1} = a_{k-1} - theta, Q_i = (a_i - theta) Q_{i+1} - bb_i Q_{i+2}
+    const bool down = t == 0;
+    double* v = down ? w.pv : w.qv;
+    int* ex = down ? w.pe : w.qe;
+    const int first = down ? 0 : k, second = down ? 1 : k - 1;
+    double pm = 1.0, p = a[down ? 0 : k - 1] - theta;
+    int e_acc = 0;
+    v[first] = 1.0;
+    ex[first] = 0;
+    v[second] = p;
+    ex[second] = 0;
+    for (int step = 1; step < k; ++step) {
+      const int i = down ? step : k - 1 - step;         // row being added
+      const double c = down ? bb[i - 1] : bb[i];
+      const double pn = fma(a[i] - theta, p, -c * pm);
+      pm = p;
+      p = pn;
+      if ((step & 7) == 7) {
+        const double m = fmax(fabs(p), fabs(pm));
+        const int e = exponent_of(m);
+        if (m > 0.0 && (e > 64 || e < -64)) {
+          const double f = pow2(-e);
+          p *= f;
+          pm *= f;
+          e_acc += e;
+        }
+      }
+      const int slot = down ? step + 1 : k - 1 - step;
+      v[slot] = p;
+      ex[slot] = e_acc;
+    }
   }
   __syncthreads();
-  if (threadIdx.x < 32) {
-    double theta;
-    tridiag_lowest_warp(alpha, beta, j + 1, &theta, s);
-    if (threadIdx.x == 0) {
-      st->theta = theta;
-      st->bnorm = bn_s;
-      st->alpha = alpha[j];
-      st->res_bound = bn_s * fabs(s[j]);
+  if (t < 32) {
+    // pivots at r (parallel): d+_r = P_{r+1}/P_r, d-_r = Q_r/Q_{r+1}
+    auto dplus = [&](int i) {
+      const double d = (w.pv[i + 1] / w.pv[i]) * pow2(w.pe[i + 1] - w.pe[i]);
+      return fabs(d) < pivmin || !(d == d) ? pivmin : d;
+    };
+    auto dminus = [&](int i) {
+      const double d = (w.qv[i] / w.qv[i + 1]) * pow2(w.qe[i] - w.qe[i + 1]);
+      return fabs(d) < pivmin || !(d == d) ? pivmin : d;
+    };
+    double best = INFINITY;
+    int br = 0;
+    for (int r = lane; r < k; r += 32) {
+      const double g = fabs(dplus(r) + dminus(r) - (a[r] - theta));
+      if (g < best) {
+        best = g;
+        br = r;
+      }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+      if (ob < best || (ob == best && orr < br)) {
+        best = ob;
+        br = orr;
+      }
+    }
+    if (lane == 0) w.r = br;
+    for (int i = lane; i < k; i += 32)
+      w.x[i] = i < br ? -b[i] / dplus(i) : (i > br ? -b[i - 1] / dminus(i) : 1.0);
+  }
+  __syncthreads();
+  const int r = w.r;
+  if (t == 0) {  // x_i = ratio_i x_{i+1}, i = r-1 .. 0
+    double v = 1.0;
+    for (int i = r - 1; i >= 0; --i) {
+      v *= w.x[i];
+      w.x[i] = v;
+    }
+  } else if (t == 32) {  // x_i = ratio_i x_{i-1}, i = r+1 .. k-1
+    double v = 1.0;
+    for (int i = r + 1; i < k; ++i) {
+      v *= w.x[i];
+      w.x[i] = v;
+    }
+  }
+  __syncthreads();
+  if (t < 32) {
+    double s2 = 0.0;
+    for (int i = lane; i < k; i += 32) s2 += w.x[i] * w.x[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    int first = k;  // deterministic sign: first nonzero component positive
+    for (int i = lane; i < k; i += 32)
+      if (w.x[i] != 0.0 && i < first) first = i;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    const double sg = (first < k && w.x[first] < 0.0) ? -1.0 : 1.0;
+    const double inv = sg / sqrt(s2);
+    for (int i = lane; i < k; i += 32) s[i] = w.x[i] * inv;
   }
 }
 
@@ -323,10 +416,16 @@ int red_blocks(const Ctx&, long n) { return std::max(1, cdiv(n, CHUNK)); }
 // MGS (linalg.cpp:131-135) to rounding.  Each block owns a fixed contiguous
 // chunk and every block reduces the per-block partials in the same fixed order,
 // so all blocks see bit-identical coefficients (deterministic).
+//
+// The step index j lives on the device (ctl->j) so that one captured step
+// (matvec on qcur + this kernel) can be replayed by a graph WHILE node: block 0
+// takes the reference's per-step decision (linalg.cpp:141-148: converged
+// residual bound, breakdown, end of block, max_iter) and either advances j
+// (q_{j+1} also goes to qcur, the matvec input) or ends the loop through
+// cudaGraphSetConditional.  The host only looks at the state when the loop ends.
 struct OrthArgs {
-  const double* Q;
+  double* Q;
   long stride;
-  int nv;  // j + 1
   double* w;
   long n;
   double* pa;  // [grid][64] partials of h1
@@ -335,9 +434,12 @@ struct OrthArgs {
   double* alpha;
   double* beta;
   double* s;
-  double* qnext;
+  double* qcur;
   LanczosStatus* st;
-  int j;
+  LanczosCtl* ctl;
+  cudaGraphConditionalHandle loop;
+  int in_graph;  // 0: host-stepped (profiling mode), the loop handle is not used
+  unsigned long long* prof;  // optional clock64 phase totals (block 0), null in production
 };
 
 constexpr int ORTH_THREADS = 256;
@@ -366,17 +468,25 @@ __device__ void orth_partials(const double* Q, long stride, int nv, const double
     double t = 0.0;
 #pragma unroll
     for (int w8 = 0; w8 < ORTH_THREADS / 32; ++w8) t += sh[w8][v];
-    part[static_cast<long>(blockIdx.x) * 64 + v] = t;
+    part[static_cast<long>(v) * gridDim.x + blockIdx.x] = t;  // [v][block]: coalesced reduce
   }
   __syncthreads();
 }
 
-// every block: coef[v] = sum_b part[b][v] in fixed order
+// sum over blocks of part[v][0..grid) in a fixed order (lane-strided partial
+// sums, then a fixed shuffle tree): identical in every block
+__device__ __forceinline__ double grid_sum(const double* p, int lane) {
+  double t = 0.0;
+  for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) t += p[b];
+  return warp_sum(t);
+}
+
+// every block: coef[v] = sum_b part[v][b]; one warp per coefficient
 __device__ void orth_reduce(const double* part, int nv, double* coef) {
-  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-    double t = 0.0;
-    for (int b = 0; b < static_cast<int>(gridDim.x); ++b) t += part[static_cast<long>(b) * 64 + v];
-    coef[v] = t;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int v = warp; v < nv; v += ORTH_THREADS / 32) {
+    const double t = grid_sum(part + static_cast<long>(v) * gridDim.x, lane);
+    if (lane == 0) coef[v] = t;
   }
   __syncthreads();
 }
@@ -386,63 +496,128 @@ __global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) 
   __shared__ double coef[64];
   __shared__ double red[32];
   cg::grid_group grid = cg::this_grid();
+  const bool prof = a.prof && blockIdx.x == 0 && threadIdx.x == 0;
+  const unsigned long long c0 = prof ? clock64() : 0;
+  const int j = a.ctl->j;  // written only by block 0 after the last grid barrier
+  const int nv = j + 1;
   const long chunk = (a.n + gridDim.x - 1) / gridDim.x;
   const long b0 = static_cast<long>(blockIdx.x) * chunk, b1 = min(a.n, b0 + chunk);
   // pass 1: h1 = Q^T w
-  orth_partials(a.Q, a.stride, a.nv, a.w, b0, b1, a.pa, sh);
+  orth_partials(a.Q, a.stride, nv, a.w, b0, b1, a.pa, sh);
+  const unsigned long long c1 = prof ? clock64() : 0;
   grid.sync();
-  orth_reduce(a.pa, a.nv, coef);
+  const unsigned long long c2 = prof ? clock64() : 0;
+  orth_reduce(a.pa, nv, coef);
   // pass 2: w <- w - Q h1 ; h2 partials
   for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
     double v = a.w[x];
-    for (int i = 0; i < a.nv; ++i) v -= coef[i] * a.Q[i * a.stride + x];
+    for (int i = 0; i < nv; ++i) v -= coef[i] * a.Q[i * a.stride + x];
     a.w[x] = v;
   }
   __syncthreads();
-  orth_partials(a.Q, a.stride, a.nv, a.w, b0, b1, a.pb, sh);
-  const double alpha_j = coef[a.nv - 1];
+  orth_partials(a.Q, a.stride, nv, a.w, b0, b1, a.pb, sh);
+  const double alpha_j = coef[nv - 1];
   grid.sync();
-  orth_reduce(a.pb, a.nv, coef);
+  orth_reduce(a.pb, nv, coef);
   // pass 3: w <- w - Q h2 ; ||w||^2 partials
   double nrm = 0.0;
   for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
     double v = a.w[x];
-    for (int i = 0; i < a.nv; ++i) v -= coef[i] * a.Q[i * a.stride + x];
+    for (int i = 0; i < nv; ++i) v -= coef[i] * a.Q[i * a.stride + x];
     a.w[x] = v;
     nrm += v * v;
   }
   nrm = block_sum(nrm, red);
   if (threadIdx.x == 0) a.pc[blockIdx.x] = nrm;
   grid.sync();
+  const unsigned long long c3 = prof ? clock64() : 0;
   __shared__ double bn_s;
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int b = 0; b < static_cast<int>(gridDim.x); ++b) t += a.pc[b];
-    bn_s = sqrt(t);
+  if (threadIdx.x < 32) {
+    const double t = grid_sum(a.pc, threadIdx.x);
+    if (threadIdx.x == 0) bn_s = sqrt(t);
   }
   __syncthreads();
   const double bn = bn_s;
+  // q_{j+1} = w / beta_j into the basis and the matvec input (unused when the
+  // step converges or breaks down)
+  if (j + 1 <= LANCZOS_BLOCK && bn > 0) {
+    const double inv = 1.0 / bn;
+    double* qn = a.Q + (j + 1) * a.stride;
+    for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
+      const double v = a.w[x] * inv;
+      qn[x] = v;
+      a.qcur[x] = v;
+    }
+  }
   if (blockIdx.x == 0) {
+    __shared__ double sa[LANCZOS_BLOCK], sb[LANCZOS_BLOCK], sbb[LANCZOS_BLOCK];
     if (threadIdx.x == 0) {
-      a.alpha[a.j] = alpha_j;
-      a.beta[a.j] = bn;
+      a.alpha[j] = alpha_j;
+      a.beta[j] = bn;
+    }
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+      const double ai = i == j ? alpha_j : a.alpha[i], bi = i == j ? bn : a.beta[i];
+      sa[i] = ai;
+      sb[i] = bi;
+      sbb[i] = bi * bi;
     }
     __syncthreads();
+    const unsigned long long c4 = prof ? clock64() : 0;
+    __shared__ double th_s, sc_s;
+    __shared__ TwistScratch tw;
+    const int k = j + 1;
     if (threadIdx.x < 32) {
-      double theta;
-      tridiag_lowest_warp(a.alpha, a.beta, a.j + 1, &theta, a.s);
+      double theta = sa[0], scale = fabs(sa[0]);
+      if (k > 1) {
+        // the previous step's Ritz value / residual bound (this cycle's step j-1)
+        const double theta_prev = a.st->theta, r_prev = a.st->res_bound;
+        __syncwarp();
+        theta = tridiag_lowest_value(sa, sb, sbb, k, true, theta_prev, r_prev, &scale);
+      }
       if (threadIdx.x == 0) {
+        th_s = theta;
+        sc_s = scale;
+      }
+    }
+    __syncthreads();
+    const double theta = th_s, scale = sc_s;
+    const unsigned long long c45 = prof ? clock64() : 0;
+    if (k > 1)
+      tridiag_vector_twisted(sa, sb, sbb, k, theta, scale, tw, a.s);
+    else if (threadIdx.x == 0)
+      a.s[0] = 1.0;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      if (prof) {
+        const unsigned long long c5 = clock64();
+        a.prof[7] += c5 - c45;  // eigenvector
+        a.prof[0] += c1 - c0;  // pass 1 (dots)
+        a.prof[1] += c2 - c1;  // grid barrier 1
+        a.prof[2] += c3 - c2;  // reduce, pass 2, barrier 2, reduce, pass 3, barrier 3
+        a.prof[3] += c4 - c3;  // ||w||, q_{j+1}
+        a.prof[4] += c5 - c4;  // tridiagonal eigenpair
+        a.prof[5] += 1;
+        a.prof[6] += static_cast<unsigned long long>(j + 1);
+      }
+      if (threadIdx.x == 0) {
+        const double res_bound = bn * fabs(a.s[j]);
         a.st->theta = theta;
         a.st->bnorm = bn;
         a.st->alpha = alpha_j;
-        a.st->res_bound = bn * fabs(a.s[a.j]);
+        a.st->res_bound = res_bound;
+        // the reference's step decision (linalg.cpp:141-148)
+        LanczosCtl& c = *a.ctl;
+        const int matvecs = c.matvecs + 1;
+        const double tscale = fmax(1.0, fabs(theta));
+        const bool breakdown = bn <= 1e-14 * tscale;
+        const bool stop = res_bound <= c.tol * tscale || breakdown || j + 1 == c.block ||
+                          matvecs >= c.max_iter;
+        c.matvecs = matvecs;
+        c.steps += 1;
+        if (!stop) c.j = j + 1;
+        if (a.in_graph) cudaGraphSetConditional(a.loop, stop ? 0u : 1u);
       }
     }
-  }
-  // q_{j+1} = w / beta_j (unused when the step converges or breaks down)
-  if (a.qnext && bn > 0) {
-    const double inv = 1.0 / bn;
-    for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) a.qnext[x] = a.w[x] * inv;
   }
 }
 
@@ -486,17 +661,36 @@ struct Kernels {
 
 }  // namespace
 
+void LanczosGraph::reset() {
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  exec = nullptr;
+  graph = nullptr;
+  key = 0;
+  body_launches = 0;
+}
+
+LanczosWs::~LanczosWs() {
+  for (auto& g : graphs) g.reset();
+}
+
 void LanczosWs::reserve(long n) {
   const long s = (n + 31) & ~31L;  // 256-byte aligned vectors
   if (s > stride || basis.p == nullptr) {
+    for (auto& g : graphs) g.reset();  // captured pointers would dangle
     stride = s;
     basis.reserve(static_cast<size_t>(LANCZOS_BLOCK + 1) * s);
     w.reserve(s);
     ritz.reserve(s);
     tmp.reserve(s);
+    qcur.reserve(s);
+    // reduction partials: multi-dot (64 per CHUNK block) and the fused
+    // orthogonalisation (129 per block, at most 2 blocks per SM)
+    partials.reserve(std::max<size_t>(64L * cdiv(s, CHUNK) + 1024, 129L * 2 * 160 + 64));
+    scal.reserve(512);
+    ctl.reserve(1);
+    ctl_h.reserve(1);
   }
-  partials.reserve(64L * cdiv(s, CHUNK) + 1024);
-  scal.reserve(512);
 }
 
 void device_norm2(Ctx& ctx, const double* x, long n, double* result) {
@@ -515,7 +709,8 @@ void device_scale(Ctx& ctx, double* dst, const double* src, long n, const double
 }
 
 EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long dim,
-                    const double* v0, double tol, int max_iter, double* out) {
+                    const double* v0, double tol, int max_iter, double* out, int graph_slot,
+                    uint64_t graph_key) {
   ws.reserve(n);
   Kernels K{ctx, ws, n, red_blocks(ctx, n)};
   double* misc = ws.misc();
@@ -543,62 +738,156 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
   // fixed for a given n: the chunking (and so every reduction order) is deterministic
   // (about one element per thread up to two CTAs per SM: the passes are latency-bound)
   const int orth_grid = static_cast<int>(std::max<long>(1, std::min<long>(cdiv(n, ORTH_THREADS), orth_max)));
-  ws.partials.reserve(static_cast<size_t>(129) * orth_grid + 64);
+  const size_t need_part = static_cast<size_t>(129) * orth_grid + 64;
+  if (ws.partials.cap < need_part) {
+    for (auto& g : ws.graphs) g.reset();
+    ws.partials.reserve(need_part);
+  }
+
+  // ---- the inner loop as a graph: WHILE { apply(qcur -> w); orth + decide } ----
+  // ACHI_LANCZOS_GRAPH=0 steps the same kernels from the host instead (ncu cannot
+  // profile kernel nodes of graphs with conditional nodes).
+  static const bool use_graph = [] {
+    const char* e = std::getenv("ACHI_LANCZOS_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  // ACHI_LANCZOS_PROF=1: clock64 phase split of the fused step, printed every 200 calls
+  static const bool prof_on = std::getenv("ACHI_LANCZOS_PROF") != nullptr;
+  static DevArr<unsigned long long> prof_buf;
+  static PinnedArr<unsigned long long> prof_h;
+  static long prof_calls = 0;
+  if (prof_on && !prof_buf.p) {
+    prof_buf.reserve(8);
+    prof_h.reserve(8);
+    ACHI_CUDA(cudaMemsetAsync(prof_buf.p, 0, 8 * sizeof(unsigned long long), ctx.stream));
+  }
+  if (prof_on && ++prof_calls % 200 == 0) {
+    ACHI_CUDA(cudaMemcpyAsync(prof_h.p, prof_buf.p, 8 * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    const double s = prof_h.p[5] ? static_cast<double>(prof_h.p[5]) : 1.0;
+    std::fprintf(stderr,
+                 "[lanczos] steps=%llu avg_k=%.1f grid=%d cycles/step: dots %.0f bar1 %.0f "
+                 "rest %.0f norm+q %.0f tridiag %.0f (of which inverse iteration %.0f)\n",
+                 prof_h.p[5], prof_h.p[6] / s, orth_grid, prof_h.p[0] / s, prof_h.p[1] / s,
+                 prof_h.p[2] / s, prof_h.p[3] / s, prof_h.p[4] / s, prof_h.p[7] / s);
+  }
+  auto launch_orth = [&](cudaGraphConditionalHandle handle, int in_graph) {
+    OrthArgs oa{ws.q(0), ws.stride, ws.w.p, n,
+                ws.partials.p, ws.partials.p + 64L * orth_grid, ws.partials.p + 128L * orth_grid,
+                ws.alpha(), ws.beta(), ws.s(), ws.qcur.p, K.dev_status(), ws.ctl.p, handle, in_graph,
+                prof_on ? prof_buf.p : nullptr};
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(orth_grid);
+    lc.blockDim = dim3(ORTH_THREADS);
+    lc.stream = ctx.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    ACHI_CUDA(cudaLaunchKernelEx(&lc, lanczos_orth_kernel, oa));
+    ACHI_LAUNCHED(ctx);
+  };
+  LanczosGraph local;
+  struct LocalGuard {
+    LanczosGraph& g;
+    ~LocalGuard() { g.reset(); }
+  } local_guard{local};
+  if (graph_slot >= 0 && static_cast<size_t>(graph_slot) >= ws.graphs.size())
+    ws.graphs.resize(static_cast<size_t>(graph_slot) + 1);
+  LanczosGraph& lg = graph_slot >= 0 ? ws.graphs[static_cast<size_t>(graph_slot)] : local;
+  const uint64_t key = graph_key ^ (static_cast<uint64_t>(n) << 40) ^ static_cast<uint64_t>(orth_grid);
+  if (use_graph && (!lg.exec || lg.key != key)) {
+    lg.reset();
+    ACHI_CUDA(cudaGraphCreate(&lg.graph, 0));
+    cudaGraphConditionalHandle handle;
+    ACHI_CUDA(cudaGraphConditionalHandleCreate(&handle, lg.graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    ACHI_CUDA(cudaGraphAddNode(&node, lg.graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    const int64_t l0 = ctx.launches;
+    ACHI_CUDA(cudaStreamBeginCaptureToGraph(ctx.stream, body, nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeRelaxed));
+    try {
+      apply(ws.qcur.p, ws.w.p);
+      launch_orth(handle, 1);
+    } catch (...) {
+      cudaGraph_t dummy;
+      cudaStreamEndCapture(ctx.stream, &dummy);
+      lg.reset();
+      throw;
+    }
+    cudaGraph_t captured;
+    ACHI_CUDA(cudaStreamEndCapture(ctx.stream, &captured));
+    lg.body_launches = ctx.launches - l0;
+    ctx.launches = l0;  // counted per executed iteration below
+    ACHI_CUDA(cudaGraphInstantiate(&lg.exec, lg.graph, 0));
+    lg.key = key;
+  }
+
   double best = std::numeric_limits<double>::infinity();
   int matvecs = 0;
   while (matvecs < max_iter) {
-    for (int j = 0; j < block && matvecs < max_iter; ++j) {
-      apply(ws.q(j), ws.w.p);
-      ++matvecs;
-      // classical Gram-Schmidt twice + tridiagonal Ritz pair + q_{j+1}, one launch
-      {
-        OrthArgs oa{ws.q(0), ws.stride, j + 1, ws.w.p, n,
-                    ws.partials.p, ws.partials.p + 64L * orth_grid,
-                    ws.partials.p + 128L * orth_grid, ws.alpha(), ws.beta(), ws.s(),
-                    j + 1 <= LANCZOS_BLOCK ? ws.q(j + 1) : nullptr, K.dev_status(), j};
-        void* args[] = {&oa};
-        ACHI_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lanczos_orth_kernel),
-                                              dim3(orth_grid), dim3(ORTH_THREADS), args, 0,
-                                              ctx.stream));
-        ACHI_LAUNCHED(ctx);
+    // one restart cycle (linalg.cpp:126-150): q_0 is in the basis; qcur = q_0
+    ACHI_CUDA(cudaMemcpyAsync(ws.qcur.p, ws.q(0), sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                              ctx.stream));
+    LanczosCtl* ch = ws.ctl_h.p;
+    *ch = LanczosCtl{0, matvecs, block, max_iter, 0, 0, tol};
+    ACHI_CUDA(cudaMemcpyAsync(ws.ctl.p, ch, sizeof(LanczosCtl), cudaMemcpyHostToDevice, ctx.stream));
+    if (use_graph) {
+      ACHI_CUDA(cudaGraphLaunch(lg.exec, ctx.stream));
+    } else {
+      for (int j = 0;;) {  // host-stepped: the kernel advances j unless the loop ends
+        apply(ws.qcur.p, ws.w.p);
+        launch_orth(0, 0);
+        ACHI_CUDA(cudaMemcpyAsync(ch, ws.ctl.p, sizeof(LanczosCtl), cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+        if (ch->j == j) break;
+        j = ch->j;
       }
-      const LanczosStatus st = K.read_status();
-      const int k = j + 1;
-      const double theta = st.theta, bnorm = st.bnorm;
-      const bool breakdown = bnorm <= 1e-14 * std::max(1.0, std::fabs(theta));
-      if (st.res_bound <= tol * std::max(1.0, std::fabs(theta)) || breakdown || k == block ||
-          matvecs >= max_iter) {
-        // ritz = normalize(sum_i s_i q_i)
-        K.axpy(ws.q(0), k, ws.s(), 1.0, nullptr, ws.ritz.p, true);
-        K.norm_from_partials(misc + 4);
-        K.scale(ws.ritz.p, ws.ritz.p, misc + 4, true);
-        apply(ws.ritz.p, ws.w.p);
-        ++matvecs;
-        // ev = ritz . w ; tmp = w - ev ritz ; res = ||tmp||
-        K.dots(ws.ritz.p, 1, ws.w.p, misc + 5);
-        K.axpy(ws.ritz.p, 1, misc + 5, -1.0, ws.w.p, ws.tmp.p, true);
-        residual_kernel<<<1, RED_THREADS, 0, ctx.stream>>>(ws.partials.p, K.nb, misc + 5, misc,
-                                                           K.dev_status());
-        ACHI_LAUNCHED(ctx);
-        const LanczosStatus rs = K.read_status();
-        best = std::min(best, rs.res);
-        if (rs.res <= tol * std::max(1.0, std::fabs(rs.ev))) {
-          if (out != ws.ritz.p)
-            ACHI_CUDA(cudaMemcpyAsync(out, ws.ritz.p, sizeof(double) * n, cudaMemcpyDeviceToDevice,
-                                      ctx.stream));
-          return EigsOut{rs.ev, matvecs, rs.res};
-        }
-        if (breakdown) {
-          // q = normalize(ritz + 1e-8 * tmp / ||tmp||)
-          K.axpy(ws.tmp.p, 1, misc + 1, 1.0, ws.ritz.p, ws.q(0), true);
-          K.norm_from_partials(misc + 4);
-          K.scale(ws.q(0), ws.q(0), misc + 4, true);
-        } else {
-          ACHI_CUDA(cudaMemcpyAsync(ws.q(0), ws.ritz.p, sizeof(double) * n,
-                                    cudaMemcpyDeviceToDevice, ctx.stream));
-        }
-        break;
-      }
+    }
+    ACHI_CUDA(cudaMemcpyAsync(ch, ws.ctl.p, sizeof(LanczosCtl), cudaMemcpyDeviceToHost, ctx.stream));
+    const LanczosStatus st = K.read_status();  // syncs the stream
+    const LanczosCtl cs = *ch;
+    if (use_graph) ctx.launches += lg.body_launches * cs.steps;
+    matvecs = cs.matvecs;
+    const int k = cs.j + 1;
+    const double theta = st.theta, bnorm = st.bnorm;
+    const bool breakdown = bnorm <= 1e-14 * std::max(1.0, std::fabs(theta));
+    // ritz = normalize(sum_i s_i q_i)
+    K.axpy(ws.q(0), k, ws.s(), 1.0, nullptr, ws.ritz.p, true);
+    K.norm_from_partials(misc + 4);
+    K.scale(ws.ritz.p, ws.ritz.p, misc + 4, true);
+    apply(ws.ritz.p, ws.w.p);
+    ++matvecs;
+    // ev = ritz . w ; tmp = w - ev ritz ; res = ||tmp||
+    K.dots(ws.ritz.p, 1, ws.w.p, misc + 5);
+    K.axpy(ws.ritz.p, 1, misc + 5, -1.0, ws.w.p, ws.tmp.p, true);
+    residual_kernel<<<1, RED_THREADS, 0, ctx.stream>>>(ws.partials.p, K.nb, misc + 5, misc,
+                                                       K.dev_status());
+    ACHI_LAUNCHED(ctx);
+    const LanczosStatus rs = K.read_status();
+    best = std::min(best, rs.res);
+    if (rs.res <= tol * std::max(1.0, std::fabs(rs.ev))) {
+      if (out != ws.ritz.p)
+        ACHI_CUDA(cudaMemcpyAsync(out, ws.ritz.p, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                                  ctx.stream));
+      return EigsOut{rs.ev, matvecs, rs.res};
+    }
+    if (breakdown) {
+      // q = normalize(ritz + 1e-8 * tmp / ||tmp||)
+      K.axpy(ws.tmp.p, 1, misc + 1, 1.0, ws.ritz.p, ws.q(0), true);
+      K.norm_from_partials(misc + 4);
+      K.scale(ws.q(0), ws.q(0), misc + 4, true);
+    } else {
+      ACHI_CUDA(cudaMemcpyAsync(ws.q(0), ws.ritz.p, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                                ctx.stream));
     }
   }
   Error e(ACHI_E_EIGEN_NONCONVERGENCE, "eigs_lowest: no convergence within max_iter");

@@ -5,7 +5,9 @@
 // convergence / restart decisions.
 #pragma once
 
+#include <cstdint>
 #include <functional>
+#include <vector>
 
 #include "common.cuh"
 
@@ -13,12 +15,43 @@ namespace achi {
 
 constexpr int LANCZOS_BLOCK = 48;  // linalg.cpp:113
 
+// Device-side control of the inner Lanczos loop (read/written by the fused
+// orthogonalisation kernel, see lanczos.cu).
+struct LanczosCtl {
+  int32_t j;         // current step: qcur = q_j is the next matvec input
+  int32_t matvecs;   // matvecs of this eigs_lowest call so far
+  int32_t block;     // min(dim, LANCZOS_BLOCK)
+  int32_t max_iter;
+  int32_t steps;     // steps executed by the device loop (launch accounting)
+  int32_t pad;
+  double tol;
+};
+
+// One instantiated graph of the inner loop: WHILE { apply(qcur -> w);
+// orthogonalise + decide }.  Cached per caller slot while its key (operator
+// shape and buffers) is unchanged.
+struct LanczosGraph {
+  uint64_t key = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int64_t body_launches = 0;  // kernels per loop iteration
+  void reset();
+};
+
 struct LanczosWs {
   DevBuf basis;   // (LANCZOS_BLOCK + 1) x stride
-  DevBuf w, ritz, tmp;
+  DevBuf w, ritz, tmp, qcur;
   DevBuf partials;
   DevBuf scal;    // alpha[64] beta[64] h1[64] h2[64] s[64] misc[64]
+  DevArr<LanczosCtl> ctl;
+  PinnedArr<LanczosCtl> ctl_h;
+  std::vector<LanczosGraph> graphs;
   long stride = 0;
+  LanczosWs() = default;
+  LanczosWs(const LanczosWs&) = delete;
+  LanczosWs& operator=(const LanczosWs&) = delete;
+  ~LanczosWs();
+  // Buffers only grow here; a growth invalidates every cached graph.
   void reserve(long n);
   double* q(int i) { return basis.p + static_cast<long>(i) * stride; }
   double* alpha() { return scal.p; }
@@ -41,8 +74,14 @@ using ApplyFn = std::function<void(const double* in, double* out)>;
 // whose reference dimension is `dim` (block = min(dim, 48)).  v0 and out are
 // device vectors of length n (out may alias v0).  Throws
 // Error{ACHI_E_EIGEN_NONCONVERGENCE} with the best residual.
+// The inner loop runs as a CUDA graph (conditional WHILE node), captured from
+// `apply` on the context stream: `apply` must only enqueue kernels on
+// ctx.stream and use buffers that stay allocated.  graph_slot >= 0 caches the
+// instantiated graph under graph_key (the caller guarantees the key changes
+// whenever apply's kernels, shapes or buffers do); -1 builds a one-off graph.
 EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long dim,
-                    const double* v0, double tol, int max_iter, double* out);
+                    const double* v0, double tol, int max_iter, double* out,
+                    int graph_slot = -1, uint64_t graph_key = 0);
 
 // Deterministic device reductions used across the hot path.
 // sum_i x_i^2 -> *result (device)
