@@ -55,6 +55,17 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def measured_traffic():
+    """DRAM bytes per launch of the dominant kernels from the committed ncu
+    --set full summaries (profiles/ncu_traffic.json, written by
+    tools/ncu_traffic.py); empty when absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return {k: v["dram_bytes_per_launch"] for k, v in json.load(f)["kernels"].items()}
+    except Exception:
+        return {}
+
+
 def workload(max_sweeps):
     spec = abi.model_spec(N_SITES, convention=abi.SPIN_HALF)
     cfg = abi.adaptive_config(CHI_MAX, EPS_TRUNC, max_sweeps=max_sweeps)
@@ -201,18 +212,28 @@ def run_ours(args, dist):
     nb = N_SITES - 1
     d2h = 56 + nb * (4 + 8) + 2 * nb * (80 + 96)  # record + profiles + trace + visit rows
     hbm, hbm_src = peaks()
-    # roofline of the dominant phase (by device time)
+    # roofline of the dominant phase (by device time); both phases are FP64
+    # tensor-core work (DMMA), latency-bound at the chi <= ~110 of C3
     svd, mv = phases["svd"], phases["matvec"]
-    svd_gbs = svd["work"] / max(svd["ms"], 1e-9) / 1e6
+    svd_tfs = svd["work"] / max(svd["ms"], 1e-9) / 1e9
     mv_tfs = mv["work"] / max(mv["ms"], 1e-9) / 1e9
-    roof_svd = {"bound": "hbm", "kernel": "jacobi_round_kernel (blocked one-sided Jacobi SVD)",
-                "achieved": round(svd_gbs, 3), "peak": hbm, "unit": "GB/s",
-                "frac": round(svd_gbs / hbm, 6), "traffic": None,
-                "work_def": "16*(m*n+n^2)*jacobi_sweeps bytes per SVD", "peak_source": hbm_src}
-    roof_mv = {"bound": "tensor", "kernel": "dmma_gemm_kernel + mpo_mix_kernel (H_eff matvec)",
+    traffic = measured_traffic()
+    roof_svd = {"bound": "tensor",
+                "kernel": "jacobi_cluster_kernel + v_replay_kernel (blocked one-sided Jacobi SVD)",
+                "achieved": round(svd_tfs, 4), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": round(svd_tfs / FP64_PEAK_TFLOPS, 6),
+                "traffic": traffic.get("jacobi_cluster_kernel"),
+                "work_def": "4*ng^2*(2*mg+ng) FP64 flops per Jacobi sweep (Gram + G and V "
+                            "rotations of every block pair), summed over the sweeps of each SVD",
+                "peak_source": "measured DMMA peak (profiles/fp64_peak_r01.txt)"}
+    roof_mv = {"bound": "tensor",
+               "kernel": "Lanczos eigensolve: H_eff matvec (dmma_gemm_kernel x2 + mpo_mix_kernel) "
+                         "+ lanczos_orth_kernel",
                "achieved": round(mv_tfs, 4), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-               "frac": round(mv_tfs / FP64_PEAK_TFLOPS, 6), "traffic": None,
-               "work_def": "2*D*d^2*chl*chr*(chl+chr)+4*D^2*d^3*chl*chr flops per matvec",
+               "frac": round(mv_tfs / FP64_PEAK_TFLOPS, 6),
+               "traffic": traffic.get("lanczos_orth_kernel"),
+               "work_def": "matvecs x (2*D*d^2*chl*chr*(chl+chr)+4*D^2*d^3*chl*chr) flops over the "
+                           "eigensolve's device time (orthogonalisation and tridiagonal included)",
                "peak_source": "measured DMMA peak (profiles/fp64_peak_r01.txt)"}
     dominant = roof_svd if svd["ms"] >= mv["ms"] else roof_mv
     out = {
@@ -227,8 +248,9 @@ def run_ours(args, dist):
                    "l2": "flushed (256 MB write) before every timed sweep"},
         "e_per_site": last["energy"] / N_SITES, "chi_max_seen": int(chi.max()),
         "chi_avg": round(float(chi.mean()), 2), "setup_s": round(setup_s, 4),
+        "sweep_s": [round(m / 1e3, 4) for m in dev_ms],
         "phases_ms": {k: round(v["ms"], 3) for k, v in phases.items()},
-        "roofline": dominant, "roofline_matvec": roof_mv,
+        "roofline": dominant, "roofline_lanczos": roof_mv, "roofline_svd": roof_svd,
         "e2e": {"value": round(e2e_s, 6), "unit": "s/sweep", "h2d_bytes_per_step": 4,
                 "d2h_bytes_per_step": d2h,
                 "note": "host wall time of the public Chain.sweep call incl. result readback; "
@@ -284,12 +306,18 @@ def svd_part(ctx, args):
     e2e = time.perf_counter() - t
     hbm, _ = peaks()
     med = statistics.median(ms)
-    gbs = 16.0 * sweeps * (n * n + n * n) / (med * 1e-3) / 1e9
+    # every round of a sweep streams all of G (n x n) and V (n x n) through the
+    # SMs once (read + write); a sweep has n/16 - 1 rounds
+    gbs = 16.0 * sweeps * (n // 16 - 1) * (n * n + n * n) / (med * 1e-3) / 1e9
     return {"svd_chi2048_ms": round(med, 3), "svd_chi2048_e2e_ms": round(e2e * 1e3, 3),
             "svd_chi2048_sweeps": sweeps, "svd_chi2048_sum_sigma2_relerr": err,
             "svd_chi2048_recon_err": rec, "svd_chi2048_factors": "U, sigma, V^T (svd_full)",
-            "svd_chi2048_roofline": {"bound": "hbm", "achieved": round(gbs, 2), "peak": hbm,
-                                     "unit": "GB/s", "frac": round(gbs / hbm, 5)}}
+            "svd_chi2048_roofline": {"bound": "hbm", "kernel": "jacobi_stream_kernel",
+                                     "achieved": round(gbs, 2), "peak": hbm,
+                                     "unit": "GB/s", "frac": round(gbs / hbm, 5),
+                                     "traffic": measured_traffic().get("jacobi_stream_kernel"),
+                                     "work_def": "16*(n/16-1)*(2 n^2) bytes per Jacobi sweep "
+                                                 "(G and V read+written once per round)"}}
 
 
 def cpu_baseline_sample(spec, cfg, ch, last):
@@ -353,6 +381,7 @@ def run_reference(args, dist):
             "config": {"workload": "C3: Heisenberg S=1/2 OBC N=100, PID/EMA chi_max=1024, "
                                    "eps_trunc=1e-10", "n": N_SITES, "chi_max": CHI_MAX},
             "e_per_site": rec.energy / N_SITES, "chi_max_seen": int(chi.max()),
+            "sweep_s": [round(w, 4) for w in walls],
             "cpu_baseline": {"value": round(v, 4), "unit": "s/sweep", "cores": threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": round(v, 4), "unit": "s/sweep", "h2d_bytes_per_step": 0,

@@ -266,10 +266,12 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   c.sync();
   c.acc.resolve();
   const int svd_sweeps = sr.sweeps();
-  // algorithmic bytes: 16 (m n + n^2) per Jacobi sweep (read+write G and V)
+  // algorithmic FP64 flops of the blocked Jacobi: per sweep
+  // C(ng/16, 2) block pairs x 2 * 32^2 * (2 mg + ng) (Gram + rotation of G,
+  // rotation of V) ~= 4 ng^2 (2 mg + ng)
   if (c.acc.enabled)
-    c.acc.work[EventAcc::kSvd] +=
-        16.0 * svd_sweeps * (static_cast<double>(sr.mg) * sr.ng + static_cast<double>(sr.ng) * sr.ng);
+    c.acc.work[EventAcc::kSvd] += 4.0 * svd_sweeps * static_cast<double>(sr.ng) * sr.ng *
+                                  (2.0 * sr.mg + sr.ng);
   const auto t2 = clk::now();
   bond_select(c, sr.sigma, sr.r_true, cfg, states.p, b, sweep_index, right ? 1 : 0,
               trace.p + slot, visits.p + slot, bout.p);
