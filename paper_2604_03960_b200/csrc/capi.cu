@@ -9,6 +9,7 @@ using namespace achi;
 namespace {
 
 int guard(achi_ctx* ctx, const std::function<void()>& f) {
+  AllocStream as(ctx ? ctx->c.stream : nullptr);
   try {
     f();
     if (ctx) ctx->c.last_error.clear();
@@ -82,6 +83,16 @@ int achi_ctx_create(int device, achi_ctx** out) {
     ctx->c.device = device;
     ctx->c.num_sms = prop.multiProcessorCount;
     ACHI_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+    // keep freed pool memory cached (stream-ordered allocations, common.cuh)
+    cudaMemPool_t pool;
+    ACHI_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    ACHI_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    {
+      // the split-K workspace is used inside captured graphs: size it up front
+      AllocStream as(ctx->c.stream);
+      ctx->c.ws_split.reserve(4096UL * 592);
+    }
     *out = ctx.release();
   });
 }
@@ -89,9 +100,12 @@ int achi_ctx_create(int device, achi_ctx** out) {
 int achi_ctx_destroy(achi_ctx* ctx) {
   if (!ctx) return ACHI_OK;
   cudaSetDevice(ctx->c.device);
-  cudaStreamSynchronize(ctx->c.stream);
   cudaStream_t s = ctx->c.stream;
-  delete ctx;
+  {
+    AllocStream as(s);
+    delete ctx;
+  }
+  cudaStreamSynchronize(s);
   cudaStreamDestroy(s);
   return ACHI_OK;
 }
@@ -170,7 +184,7 @@ int achi_chain_create(achi_ctx* ctx, const achi_model_spec* spec, const achi_dmr
 
 int achi_chain_destroy(achi_chain* chain) {
   if (chain) {
-    cudaStreamSynchronize(chain->ch.ctx->stream);
+    AllocStream as(chain->ch.ctx->stream);
     delete chain;
   }
   return ACHI_OK;

@@ -38,6 +38,34 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
     ++(ctx).launches;                                                 \
   } while (0)
 
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync /
+// cudaFreeAsync on the stream of the context being driven, see AllocStream),
+// whose release threshold is raised at context creation: buffers that grow
+// while chi grows reuse cached pool memory instead of a synchronising
+// cudaFree + cudaMalloc (which stalled sweeps for up to ~0.5 s).
+inline cudaStream_t& alloc_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  return s;
+}
+// RAII: route allocations of this thread to `s` for the scope of a C-ABI call
+struct AllocStream {
+  cudaStream_t prev;
+  explicit AllocStream(cudaStream_t s) : prev(alloc_stream()) { alloc_stream() = s; }
+  ~AllocStream() { alloc_stream() = prev; }
+};
+inline void* dev_alloc(size_t bytes) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (alloc_stream()) cudaStreamIsCapturing(alloc_stream(), &cs);
+  if (cs != cudaStreamCaptureStatusNone)  // buffers must be sized before graph capture
+    fail(ACHI_E_INTERNAL, "device allocation inside a stream capture");
+  void* p = nullptr;
+  ACHI_CUDA(cudaMallocAsync(&p, bytes, alloc_stream()));
+  return p;
+}
+inline void dev_free(void* p) {
+  if (p) cudaFreeAsync(p, alloc_stream());
+}
+
 // Owning device allocation (capacity-based, grows but never shrinks).
 struct DevBuf {
   double* p = nullptr;
@@ -52,7 +80,7 @@ struct DevBuf {
   }
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    dev_free(p);
     p = nullptr;
     cap = 0;
   }
@@ -60,8 +88,7 @@ struct DevBuf {
   double* reserve(size_t n) {
     if (n > cap) {
       release();
-      size_t bytes = (n == 0 ? 1 : n) * sizeof(double);
-      ACHI_CUDA(cudaMalloc(&p, bytes));
+      p = static_cast<double*>(dev_alloc((n == 0 ? 1 : n) * sizeof(double)));
       cap = n;
     }
     return p;
@@ -75,12 +102,11 @@ struct DevArr {
   DevArr() = default;
   DevArr(const DevArr&) = delete;
   DevArr& operator=(const DevArr&) = delete;
-  ~DevArr() { if (p) cudaFree(p); }
+  ~DevArr() { dev_free(p); }
   T* reserve(size_t n) {
     if (n > cap) {
-      if (p) cudaFree(p);
-      p = nullptr;
-      ACHI_CUDA(cudaMalloc(&p, (n == 0 ? 1 : n) * sizeof(T)));
+      dev_free(p);
+      p = static_cast<T*>(dev_alloc((n == 0 ? 1 : n) * sizeof(T)));
       cap = n;
     }
     return p;

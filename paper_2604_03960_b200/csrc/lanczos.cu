@@ -2,6 +2,7 @@
 // block owns a fixed contiguous chunk and partials are summed in fixed order.
 #include <cooperative_groups.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <limits>
@@ -798,7 +799,14 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
     ws.graphs.resize(static_cast<size_t>(graph_slot) + 1);
   LanczosGraph& lg = graph_slot >= 0 ? ws.graphs[static_cast<size_t>(graph_slot)] : local;
   const uint64_t key = graph_key ^ (static_cast<uint64_t>(n) << 40) ^ static_cast<uint64_t>(orth_grid);
+  static long builds = 0;
+  static double build_s = 0.0;
+  if (prof_on && prof_calls % 200 == 0)
+    std::fprintf(stderr, "[lanczos] graph builds %ld, %.3f ms each\n", builds,
+                 builds ? 1e3 * build_s / builds : 0.0);
   if (use_graph && (!lg.exec || lg.key != key)) {
+    const auto tb = std::chrono::steady_clock::now();
+    ++builds;
     lg.reset();
     ACHI_CUDA(cudaGraphCreate(&lg.graph, 0));
     cudaGraphConditionalHandle handle;
@@ -829,6 +837,7 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
     ctx.launches = l0;  // counted per executed iteration below
     ACHI_CUDA(cudaGraphInstantiate(&lg.exec, lg.graph, 0));
     lg.key = key;
+    build_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - tb).count();
   }
 
   double best = std::numeric_limits<double>::infinity();
