@@ -24,13 +24,19 @@ def rows(rep):
 
 def to_bytes(v, unit):
     v = float(v.replace(",", ""))
-    return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6,
-                "GB": 1e9}.get(unit, 1)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    if unit not in scale:
+        raise ValueError(f"unknown byte unit {unit!r}")
+    return v * scale[unit]
 
 
 def to_ns(v, unit):
     v = float(v.replace(",", ""))
-    return v * {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "ns": 1, "us": 1e3, "ms": 1e6}.get(unit, 1)
+    scale = {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3,
+             "ms": 1e6, "s": 1e9}
+    if unit not in scale:
+        raise ValueError(f"unknown time unit {unit!r}")
+    return v * scale[unit]
 
 
 def main():
