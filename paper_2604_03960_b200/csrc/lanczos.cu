@@ -756,7 +756,7 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
   static const bool prof_on = std::getenv("ACHI_LANCZOS_PROF") != nullptr;
   static DevArr<unsigned long long> prof_buf;
   static PinnedArr<unsigned long long> prof_h;
-  static long prof_calls = 0;
+  static thread_local long prof_calls = 0;
   if (prof_on && !prof_buf.p) {
     prof_buf.reserve(8);
     prof_h.reserve(8);
@@ -799,8 +799,8 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
     ws.graphs.resize(static_cast<size_t>(graph_slot) + 1);
   LanczosGraph& lg = graph_slot >= 0 ? ws.graphs[static_cast<size_t>(graph_slot)] : local;
   const uint64_t key = graph_key ^ (static_cast<uint64_t>(n) << 40) ^ static_cast<uint64_t>(orth_grid);
-  static long builds = 0;
-  static double build_s = 0.0;
+  static thread_local long builds = 0;
+  static thread_local double build_s = 0.0;
   if (prof_on && prof_calls % 200 == 0)
     std::fprintf(stderr, "[lanczos] graph builds %ld, %.3f ms each\n", builds,
                  builds ? 1e3 * build_s / builds : 0.0);
