@@ -75,3 +75,44 @@ def test_sharded_gather_world2_gloo():
     for u in range(7):
         assert np.array_equal(out2[u], fake_work(u))
     assert sorted(plan[0] + plan[1]) == list(range(10))
+
+
+def _runner_worker(rank, world, port, q):
+    """ensemble_run.main end to end on gloo, with the per-unit GPU work replaced."""
+    import contextlib
+    import io
+    import json
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    from paper_2604_03960_b200 import ensemble_run
+
+    def fake_workers(units, inflight, work, device_index):
+        # deterministic per-unit records and a per-rank "device time"
+        return {u: [float(u), -0.4 - 0.001 * u, 5.0, 100.0, 1.0] for u in units}, 1.0 + rank
+
+    ensemble_run.run_workers = fake_workers
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        ensemble_run.main(["--job", "c4", "--chains", "12", "--inflight", "2"])
+    if rank == 0:
+        q.put(json.loads(buf.getvalue().strip().splitlines()[-1]))
+
+
+def test_ensemble_runner_world2_gloo():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_runner_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    line = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert line["n_gpus"] == 2 and line["job"] == "c4"
+    assert line["device_s"] == 2.0                     # max over ranks
+    assert abs(line["value"] - 12 / 2.0) < 1e-12       # units / job time
+    res = np.array(line["results"])
+    assert res.shape == (12, 5)
+    assert np.array_equal(res[:, 0], np.arange(12))    # every chain exactly once, by index
