@@ -176,6 +176,14 @@ void mix(Ctx& ctx, const double* x, double* y, const DevMix& W, const MixGeom& g
 // Contractions
 // ---------------------------------------------------------------------------
 void heff_apply(Ctx& ctx, const HeffOps& op, const double* theta, double* out) {
+  static const bool small_on = [] {
+    const char* e = std::getenv("ACHI_HEFF_SMALL");
+    return !(e && e[0] == '0');
+  }();
+  if (small_on && heff_small_applicable(op)) {
+    heff_apply_small(ctx, op, theta, out);
+    return;
+  }
   const long chl = op.chl, chr = op.chr, d = op.d, D1 = op.D1, D3 = op.D3;
   double* X = ctx.ws_a.reserve(static_cast<size_t>(chl * D1 * d * d * chr));
   double* Y = ctx.ws_b.reserve(static_cast<size_t>(chl * d * d * D3 * chr));

@@ -58,8 +58,12 @@ struct HeffOps {
   DevMix mix;       // mix_heff(W_b, W_{b+1})
 };
 
-// out = H_eff theta (dmrg.cpp:58-71); theta/out (chl~, d, d, chr~).
+// out = H_eff theta (dmrg.cpp:58-71); theta/out (chl~, d, d, chr~).  Bonds with
+// chl~, chr~ <= 128 take the fused one-launch path (heff_small.cu), larger ones
+// the TMA GEMM -> mixing -> GEMM path.
 void heff_apply(Ctx& ctx, const HeffOps& op, const double* theta, double* out);
+bool heff_small_applicable(const HeffOps& op);
+void heff_apply_small(Ctx& ctx, const HeffOps& op, const double* theta, double* out);
 
 // Lnew (chn~, Dr, chn~) from L (chl~, Dl, chl~) and A (chl~, d, chn~) (dmrg.cpp:26-37)
 void env_left(Ctx& ctx, const double* L, const double* A, int chl, int chn, int d, int Dl, int Dr,

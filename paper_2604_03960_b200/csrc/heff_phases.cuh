@@ -1,0 +1,228 @@
+// Device phases of the fused small-chi H_eff matvec (heff_small.cu).  See
+// heff_small.cu for the contraction; each phase loops its work items over the
+// CTAs [blk, blk + nblk) of a cooperative grid, and the caller puts a grid
+// barrier between phases.
+#pragma once
+
+#include "contract.cuh"
+
+namespace achi {
+namespace hs {
+
+constexpr int HS_THREADS = 256;
+constexpr int HS_TM = 32;        // tile rows
+constexpr int HS_TN = 64;        // tile cols
+constexpr int HS_KMAX = 128;     // max contraction length (chl for A, chr for B)
+constexpr int HS_LD = HS_KMAX + 4;
+constexpr int HS_MAXW = 64;      // max MPO mixing inputs/outputs (D d^2)
+constexpr int HS_MAXNNZ = 512;
+
+struct HsArgs {
+  const double* L;
+  const double* R;
+  const double* theta;
+  double* out;
+  double* X;     // Y, the mixed first contraction: [chl*d*d][D3][chr]
+  double* part;  // [D3][chl*d*d][chr]
+  DevMix mix;
+  int chl, chr, d, D1, D3;
+};
+
+__device__ __forceinline__ void mma16x8x4(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// C (32 x 64) = As (32 x K, row-major, ld HS_LD) * Bs^T (Bs: 64 x K, ld HS_LD);
+// warp w: rows 16 (w / 4), cols 16 (w % 4) = two n8 tiles.  Returns the
+// warp's accumulators for the store.
+__device__ __forceinline__ void tile_mma(const double* As, const double* Bs, int K, double (&acc)[2][4]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int mr = (warp >> 2) * 16, nc = (warp & 3) * 16;
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[q][i] = 0.0;
+  // every lane runs the same number of mma.sync; K tails are zero-padded by the loaders
+  const int K4 = (K + 3) & ~3;
+  for (int k = tig; k < K4; k += 4) {
+    const double a0 = As[(mr + gid) * HS_LD + k], a1 = As[(mr + gid + 8) * HS_LD + k];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) mma16x8x4(acc[q], a0, a1, Bs[(nc + q * 8 + gid) * HS_LD + k]);
+  }
+}
+
+__device__ __forceinline__ void tile_store(const double (&acc)[2][4], double* C, long ldc, int m0,
+                                           int n0, int M, int N) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int mr = m0 + (warp >> 2) * 16 + gid, nc0 = n0 + (warp & 3) * 16;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int c = nc0 + q * 8 + 2 * tig;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = mr + 8 * h;
+      if (r < M) {
+        if (c < N) C[static_cast<long>(r) * ldc + c] = acc[q][2 * h];
+        if (c + 1 < N) C[static_cast<long>(r) * ldc + c + 1] = acc[q][2 * h + 1];
+      }
+    }
+  }
+}
+
+
+// Mixing coefficients of the bond (CSR) staged once per CTA.
+struct MixSmem {
+  double wv[HS_MAXNNZ];
+  int wc[HS_MAXNNZ], wr[HS_MAXW + 1];
+};
+__device__ __forceinline__ void load_mix(const DevMix& m, MixSmem& w) {
+  for (int i = threadIdx.x; i < m.nnz; i += blockDim.x) {
+    w.wv[i] = m.val[i];
+    w.wc[i] = m.col[i];
+  }
+  for (int i = threadIdx.x; i <= m.nout; i += blockDim.x) w.wr[i] = m.rowptr[i];
+}
+
+// Tile shape of phase A: rows = a block of `blb` left indices bl with all D1
+// MPO rows a (blb * D1 <= 32), columns = a block of 16 right indices jr for
+// all d^2 physical pairs s (d^2 * 16 = 64), so the MPO mixing of the tile's
+// outputs only needs the tile itself.
+__device__ __forceinline__ int phase_a_blb(const HsArgs& a) { return HS_TM / a.D1; }
+constexpr int HS_JRB = 16;  // jr per phase-A tile (d = 2)
+
+// A: Y[((bl,s'),e), jr] = sum_{(a,s)} W12[(s',e),(a,s)] sum_jl L[(bl,a),jl] theta[jl,(s,jr)]
+// The GEMM tile is staged in shared memory and mixed there (no X buffer).
+__device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const double* theta,
+                                        double* As, double* Bs, int blk, int nblk) {
+  const int t = threadIdx.x;
+  const int chl = a.chl, chr = a.chr, dd = a.d * a.d, D1 = a.D1, D3 = a.D3;
+  const int N1 = dd * chr, blb = phase_a_blb(a), rows = blb * D1;
+  const int tm = (chl + blb - 1) / blb, tn = (chr + HS_JRB - 1) / HS_JRB;
+  const int K4 = (chl + 3) & ~3;  // zero-padded K tail
+  for (int item = blk; item < tm * tn; item += nblk) {
+    const int bl0 = (item / tn) * blb, jr0 = (item % tn) * HS_JRB;
+    __syncthreads();
+    {
+      // As[m][k] = L[bl0*D1 + m][k] (m < blb*D1): thread -> (k = t % 128, rows t / 128 + 2u);
+      // every load of a thread is issued before its stores
+      const int k = t & (HS_KMAX - 1), r0 = t >> 7;
+      double v[HS_TM / 2];
+#pragma unroll
+      for (int u = 0; u < HS_TM / 2; ++u) {
+        const int m = r0 + 2 * u;
+        v[u] = (m < rows && bl0 * D1 + m < chl * D1 && k < chl)
+                   ? a.L[static_cast<long>(bl0 * D1 + m) * chl + k]
+                   : 0.0;
+      }
+      if (k < K4)
+#pragma unroll
+        for (int u = 0; u < HS_TM / 2; ++u) As[(r0 + 2 * u) * HS_LD + k] = v[u];
+    }
+    {
+      // Bs[n][k] = theta[k][s*chr + jr0 + q], n = s*16 + q: thread -> (n = t % 64, k = t / 64 + 4u)
+      const int n = t & (HS_TN - 1), kq = t >> 6;
+      const int s = n / HS_JRB, jr = jr0 + (n % HS_JRB);
+      const bool ok = s < dd && jr < chr;
+      double v[HS_KMAX / 4];
+#pragma unroll
+      for (int u = 0; u < HS_KMAX / 4; ++u) {
+        const int k = kq + 4 * u;
+        v[u] = (ok && k < chl) ? theta[static_cast<long>(k) * N1 + s * chr + jr] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < HS_KMAX / 4; ++u)
+        if (kq + 4 * u < K4) Bs[n * HS_LD + kq + 4 * u] = v[u];
+    }
+    __syncthreads();
+    double acc[2][4];
+    tile_mma(As, Bs, chl, acc);
+    __syncthreads();
+    // stage the 32 x 64 tile (rows (bl, a), cols (s, q)) into As, then mix
+    tile_store(acc, As, HS_LD, 0, 0, HS_TM, HS_TN);
+    __syncthreads();
+    const int nout = blb * dd * D3 * HS_JRB;  // outputs (bl, s', e, q)
+    for (int o = t; o < nout; o += HS_THREADS) {
+      const int q = o % HS_JRB, rest = o / HS_JRB;
+      const int e = rest % D3, r2 = rest / D3;
+      const int sp = r2 % dd, bll = r2 / dd;
+      const int bl = bl0 + bll, jr = jr0 + q;
+      if (bl >= chl || jr >= chr) continue;
+      const int j = sp * D3 + e;
+      double v = 0.0;
+      for (int p = w.wr[j]; p < w.wr[j + 1]; ++p) {
+        const int in = w.wc[p], aa = in / dd, s = in - aa * dd;  // input (a, s)
+        v += w.wv[p] * As[(bll * D1 + aa) * HS_LD + s * HS_JRB + q];
+      }
+      a.X[((static_cast<long>(bl) * dd + sp) * D3 + e) * chr + jr] = v;  // Y[(bl s') (e jr)]
+    }
+  }
+}
+
+// B: P_e[(bl,s'), br] = sum_jr Y[(bl,s'),(e,jr)] R[br,(e,jr)]  (one item per e: split-K)
+__device__ __forceinline__ void phase_b(const HsArgs& a, double* As, double* Bs, int blk, int nblk) {
+  const int t = threadIdx.x;
+  const int chl = a.chl, chr = a.chr, dd = a.d * a.d, D3 = a.D3;
+  const int M2 = chl * dd, N2 = chr;
+  const int tm = (M2 + HS_TM - 1) / HS_TM, tn = (N2 + HS_TN - 1) / HS_TN;
+  const int items = tm * tn * D3;
+  const int K4 = (chr + 3) & ~3;  // zero-padded K tail
+  for (int item = blk; item < items; item += nblk) {
+    const int e = item / (tm * tn), rest = item - e * tm * tn;
+    const int m0 = (rest / tn) * HS_TM, n0 = (rest % tn) * HS_TN;
+    __syncthreads();
+    {
+      // As[m][jr] = Y[(m0+m), e, jr]: thread -> (jr = t % 128, rows t / 128 + 2u)
+      const int jr = t & (HS_KMAX - 1), r0 = t >> 7;
+      double v[HS_TM / 2];
+#pragma unroll
+      for (int u = 0; u < HS_TM / 2; ++u) {
+        const int row = m0 + r0 + 2 * u;
+        v[u] = (row < M2 && jr < chr) ? a.X[(static_cast<long>(row) * D3 + e) * chr + jr] : 0.0;
+      }
+      if (jr < K4)
+#pragma unroll
+        for (int u = 0; u < HS_TM / 2; ++u) As[(r0 + 2 * u) * HS_LD + jr] = v[u];
+    }
+    {
+      // Bs[n][jr] = R[n0+n][e][jr]: thread -> (jr = t % 128, n = t / 128 + 2u)
+      const int jr = t & (HS_KMAX - 1), q0 = t >> 7;
+      double v[HS_TN / 2];
+#pragma unroll
+      for (int u = 0; u < HS_TN / 2; ++u) {
+        const int n = q0 + 2 * u;
+        v[u] = (n0 + n < N2 && jr < chr) ? a.R[(static_cast<long>(n0 + n) * D3 + e) * chr + jr] : 0.0;
+      }
+      if (jr < K4)
+#pragma unroll
+        for (int u = 0; u < HS_TN / 2; ++u) Bs[(q0 + 2 * u) * HS_LD + jr] = v[u];
+    }
+    __syncthreads();
+    double acc[2][4];
+    tile_mma(As, Bs, chr, acc);
+    tile_store(acc, a.part + static_cast<long>(e) * M2 * N2, N2, m0, n0, M2, N2);
+  }
+}
+
+// C: out = sum_e P_e (fixed order)
+__device__ __forceinline__ void phase_c(const HsArgs& a, double* out, int blk, int nblk) {
+  const int t = threadIdx.x;
+  const int M2 = a.chl * a.d * a.d, N2 = a.chr;
+  const long tot = static_cast<long>(M2) * N2;
+  for (long i = blk * static_cast<long>(HS_THREADS) + t; i < tot;
+       i += static_cast<long>(nblk) * HS_THREADS) {
+    double v = 0.0;
+    for (int e = 0; e < a.D3; ++e) v += a.part[e * tot + i];
+    out[i] = v;
+  }
+}
+
+inline size_t smem_bytes() { return sizeof(double) * (HS_TM + HS_TN) * HS_LD; }
+
+}  // namespace hs
+}  // namespace achi

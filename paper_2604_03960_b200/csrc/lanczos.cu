@@ -492,14 +492,15 @@ __device__ void orth_reduce(const double* part, int nv, double* coef) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) {
+// Orthogonalisation + tridiagonal + decision of step j (called by every CTA of
+// a cooperative grid; block 0 writes the status and ctl, advancing ctl->j
+// unless the loop ends).
+__device__ void orth_and_decide(const OrthArgs& a, int j, cg::grid_group& grid) {
   __shared__ double sh[ORTH_THREADS / 32][65];
   __shared__ double coef[64];
   __shared__ double red[32];
-  cg::grid_group grid = cg::this_grid();
   const bool prof = a.prof && blockIdx.x == 0 && threadIdx.x == 0;
   const unsigned long long c0 = prof ? clock64() : 0;
-  const int j = a.ctl->j;  // written only by block 0 after the last grid barrier
   const int nv = j + 1;
   const long chunk = (a.n + gridDim.x - 1) / gridDim.x;
   const long b0 = static_cast<long>(blockIdx.x) * chunk, b1 = min(a.n, b0 + chunk);
@@ -547,7 +548,7 @@ __global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) 
     for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
       const double v = a.w[x] * inv;
       qn[x] = v;
-      a.qcur[x] = v;
+      if (a.qcur) a.qcur[x] = v;
     }
   }
   if (blockIdx.x == 0) {
@@ -620,6 +621,11 @@ __global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) 
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  orth_and_decide(a, a.ctl->j, grid);  // ctl->j is written only after the last grid barrier
 }
 
 struct Kernels {

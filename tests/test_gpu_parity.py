@@ -31,7 +31,9 @@ def rand_env(rng, chi, D):
 
 # ---------------- K1: effective Hamiltonian ----------------
 
-@pytest.mark.parametrize("chl,chr_", [(1, 1), (1, 2), (3, 5), (8, 8), (17, 13), (64, 64), (130, 96)])
+@pytest.mark.parametrize("chl,chr_", [(1, 1), (1, 2), (3, 5), (8, 8), (17, 13), (64, 64), (130, 96),
+                                      # fused small-chi path edges (<= 128) and just past it
+                                      (2, 128), (128, 2), (109, 110), (127, 128), (128, 129)])
 def test_heff_matches_oracle(ctx, oracle, chl, chr_):
     rng = np.random.default_rng(chl * 1000 + chr_)
     w = oracle.build_mpo(abi.model_spec(6, jz=1.3, h=0.4))
