@@ -185,27 +185,21 @@ __device__ void inner_jacobi(Small& sm, double z2, double tol, int max_inner) {
       const bool okq = jacobi_angle(qii, qjj, qij, z2, tol2, cq, sq, tq);
       any |= okq ? 1 : 0;
       const double cp = __shfl_sync(0xffffffffu, cq, bp), sp = __shfl_sync(0xffffffffu, sq, bp);
-      if (bp == bq && okq) {
-        // the pivot block: stable updates app - t apq, aqq + t apq, exact zero
-        D[iq][iq] = __fma_rn(-tq, qij, qii);
-        D[jq][jq] = __fma_rn(tq, qij, qjj);
-        D[iq][jq] = 0.0;
-        D[jq][iq] = 0.0;
-      } else {
-        // columns: (x, y) -> (cq x - sq y, sq x + cq y); rows likewise with (cp, sp)
-        const double a1 = cq * a - sq * b, b1 = sq * a + cq * b;
-        const double c1 = cq * c - sq * d, d1 = sq * c + cq * d;
-        D[ip][iq] = cp * a1 - sp * c1;
-        D[jp][iq] = sp * a1 + cp * c1;
-        D[ip][jq] = cp * b1 - sp * d1;
-        D[jp][jq] = sp * b1 + cp * d1;
-      }
-      if (okq) {
-        sm.J[2 * bp][iq] = cq * jx0 - sq * jy0;
-        sm.J[2 * bp][jq] = sq * jx0 + cq * jy0;
-        sm.J[2 * bp + 1][iq] = cq * jx1 - sq * jy1;
-        sm.J[2 * bp + 1][jq] = sq * jx1 + cq * jy1;
-      }
+      // columns: (x, y) -> (cq x - sq y, sq x + cq y); rows likewise with (cp, sp).
+      // Branch-free: the pivot block (bp == bq: the same four positions) takes the
+      // stable updates app - t apq, aqq + t apq and an exact zero; a pair that is
+      // not rotated has (c, s) = (1, 0), which leaves every value bit-identical.
+      const double a1 = cq * a - sq * b, b1 = sq * a + cq * b;
+      const double c1 = cq * c - sq * d, d1 = sq * c + cq * d;
+      const bool piv = bp == bq && okq;
+      D[ip][iq] = piv ? __fma_rn(-tq, qij, qii) : cp * a1 - sp * c1;
+      D[jp][iq] = piv ? 0.0 : sp * a1 + cp * c1;
+      D[ip][jq] = piv ? 0.0 : cp * b1 - sp * d1;
+      D[jp][jq] = piv ? __fma_rn(tq, qij, qjj) : sp * b1 + cp * d1;
+      sm.J[2 * bp][iq] = cq * jx0 - sq * jy0;
+      sm.J[2 * bp][jq] = sq * jx0 + cq * jy0;
+      sm.J[2 * bp + 1][iq] = cq * jx1 - sq * jy1;
+      sm.J[2 * bp + 1][jq] = sq * jx1 + cq * jy1;
       ip = nip;
       jp = njp;
       iq = niq;
@@ -612,17 +606,24 @@ __device__ __forceinline__ void rotate_chunk(Chunk& X, const Small& sm) {
   __syncthreads();
 }
 
+// STREAM_STAGES chunks in flight per CTA (one CTA per SM: the passes are
+// bandwidth-bound and need the memory-level parallelism)
+constexpr int STREAM_STAGES = 4;
+
 __device__ void stream_rotate(Chunk* X, double* M, long ld, int rows, int ca, int cb, const Small& sm) {
   const int nch = (rows + JCH - 1) / JCH;
-  load_chunk_async(X[0], M, ld, rows, 0, ca, cb);
-  cp_commit();
-  for (int k = 0; k < nch; ++k) {
-    if (k + 1 < nch) load_chunk_async(X[(k + 1) & 1], M, ld, rows, (k + 1) * JCH, ca, cb);
+  for (int k = 0; k < STREAM_STAGES - 1; ++k) {
+    if (k < nch) load_chunk_async(X[k], M, ld, rows, k * JCH, ca, cb);
     cp_commit();
-    cp_wait<1>();
+  }
+  for (int k = 0; k < nch; ++k) {
+    const int kn = k + STREAM_STAGES - 1;
+    if (kn < nch) load_chunk_async(X[kn % STREAM_STAGES], M, ld, rows, kn * JCH, ca, cb);
+    cp_commit();
+    cp_wait<STREAM_STAGES - 1>();
     __syncthreads();
-    rotate_chunk(X[k & 1], sm);
-    store_chunk(X[k & 1], M, ld, rows, k * JCH, ca, cb);
+    rotate_chunk(X[k % STREAM_STAGES], sm);
+    store_chunk(X[k % STREAM_STAGES], M, ld, rows, k * JCH, ca, cb);
     __syncthreads();
   }
 }
@@ -630,7 +631,7 @@ __device__ void stream_rotate(Chunk* X, double* M, long ld, int rows, int ca, in
 __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
   Chunk* X = reinterpret_cast<Chunk*>(dyn);
-  Small& sm = *reinterpret_cast<Small*>(X + 2);
+  Small& sm = *reinterpret_cast<Small*>(X + STREAM_STAGES);
   init_pair_tables(sm);
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
@@ -646,14 +647,17 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
       circle_pair(a.nb, round, p, ba, bb);
       const int ca = ba * JB, cb = bb * JB;
       double acc[4] = {0, 0, 0, 0};
-      load_chunk_async(X[0], G, a.ldg, a.mg, 0, ca, cb);
-      cp_commit();
-      for (int k = 0; k < nch; ++k) {
-        if (k + 1 < nch) load_chunk_async(X[(k + 1) & 1], G, a.ldg, a.mg, (k + 1) * JCH, ca, cb);
+      for (int k = 0; k < STREAM_STAGES - 1; ++k) {
+        if (k < nch) load_chunk_async(X[k], G, a.ldg, a.mg, k * JCH, ca, cb);
         cp_commit();
-        cp_wait<1>();
+      }
+      for (int k = 0; k < nch; ++k) {
+        const int kn = k + STREAM_STAGES - 1;
+        if (kn < nch) load_chunk_async(X[kn % STREAM_STAGES], G, a.ldg, a.mg, kn * JCH, ca, cb);
+        cp_commit();
+        cp_wait<STREAM_STAGES - 1>();
         __syncthreads();
-        gram_chunk(X[k & 1], acc);
+        gram_chunk(X[k % STREAM_STAGES], acc);
         __syncthreads();
       }
       const bool rot = finish_gram(sm, acc, z2, a.tol, a.max_inner);
@@ -824,7 +828,7 @@ __global__ void gather_kernel(const double* __restrict__ G, long ldg, const doub
   }
 }
 
-size_t stream_smem() { return sizeof(Chunk) * 2 + sizeof(Small) + 16; }
+size_t stream_smem() { return sizeof(Chunk) * STREAM_STAGES + sizeof(Small) + 16; }
 size_t cluster_smem(int rows_pad) {
   return sizeof(double) * 2 * JW * (rows_pad + 4) + sizeof(Small) + 16;
 }
