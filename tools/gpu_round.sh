@@ -13,14 +13,15 @@ if [ "$2" != "skip_ref" ]; then
 fi
 # launch list of the bench command (host-stepped Lanczos so ncu sees every kernel;
 # ncu cannot profile kernel nodes of graphs with conditional nodes)
+# (skip sweeps 0-2, ~45k launches, then list 3000 launches of the first timed sweep)
 ACHI_LANCZOS_GRAPH=0 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none \
-  -s 140000 -c 8000 --csv --log-file $O/launches.csv \
-  python bench.py --steps 2 --warmup 5 --skip-svd --no-cpu-baseline > $O/ncu_list.log 2>&1
+  -s 50000 -c 3000 --csv --log-file $O/launches.csv \
+  python bench.py --steps 1 --warmup 3 --skip-svd --no-cpu-baseline > $O/ncu_list.log 2>&1
 echo "list rc=$?" >> $O/status.txt
 python tools/ncu_summary.py $O/launches.csv > $O/launches_summary.txt 2>&1
 # full captures of the dominant kernels in the steady state of C3 (sweeps 5-6)
 for K in jacobi_cluster_kernel:1000 v_replay_kernel:1000 lanczos_orth_kernel:14000 \
-         mpo_mix_kernel:14000 dmma_gemm_kernel:30000; do
+         heff_small_kernel:14000; do
   name=${K%%:*}; skip=${K##*:}
   ACHI_LANCZOS_GRAPH=0 timeout 900 ncu --set full --import-source on --clock-control none \
     -k regex:$name -s $skip -c 2 -o $O/full_$name python tools/ncu_c3.py 7 > $O/ncu_$name.log 2>&1
