@@ -83,6 +83,9 @@ int achi_ctx_create(int device, achi_ctx** out) {
     ctx->c.device = device;
     ctx->c.num_sms = prop.multiProcessorCount;
     ACHI_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+    ACHI_CUDA(cudaStreamCreateWithFlags(&ctx->c.aux, cudaStreamNonBlocking));
+    ACHI_CUDA(cudaEventCreateWithFlags(&ctx->c.ev_fork, cudaEventDisableTiming));
+    ACHI_CUDA(cudaEventCreateWithFlags(&ctx->c.ev_join, cudaEventDisableTiming));
     // keep freed pool memory cached (stream-ordered allocations, common.cuh)
     cudaMemPool_t pool;
     ACHI_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -100,12 +103,17 @@ int achi_ctx_create(int device, achi_ctx** out) {
 int achi_ctx_destroy(achi_ctx* ctx) {
   if (!ctx) return ACHI_OK;
   cudaSetDevice(ctx->c.device);
-  cudaStream_t s = ctx->c.stream;
+  cudaStream_t s = ctx->c.stream, aux = ctx->c.aux;
+  cudaEvent_t e1 = ctx->c.ev_fork, e2 = ctx->c.ev_join;
   {
     AllocStream as(s);
     delete ctx;
   }
   cudaStreamSynchronize(s);
+  cudaStreamSynchronize(aux);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  cudaStreamDestroy(aux);
   cudaStreamDestroy(s);
   return ACHI_OK;
 }

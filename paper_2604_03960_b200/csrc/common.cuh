@@ -202,6 +202,10 @@ struct Ctx {
   PinnedArr<double> host_small;
   PinnedArr<LanczosStatus> status;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // second stream for fork/join inside captured graphs (Lanczos: the
+  // tridiagonal step runs beside the next matvec)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DevBuf flush;
   void sync() { ACHI_CUDA(cudaStreamSynchronize(stream)); }
 };

@@ -495,10 +495,15 @@ __device__ void orth_reduce(const double* part, int nv, double* coef) {
 // Orthogonalisation + tridiagonal + decision of step j (called by every CTA of
 // a cooperative grid; block 0 writes the status and ctl, advancing ctl->j
 // unless the loop ends).
-__device__ void orth_and_decide(const OrthArgs& a, int j, cg::grid_group& grid) {
+// Step j, part 1 (every CTA of a cooperative grid): w <- w - Q (Q^T w) twice,
+// beta_j = ||w||, q_{j+1} = w / beta_j into the basis and into qcur (the next
+// matvec input); block 0 stores alpha_j, beta_j.
+__global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) {
   __shared__ double sh[ORTH_THREADS / 32][65];
   __shared__ double coef[64];
   __shared__ double red[32];
+  cg::grid_group grid = cg::this_grid();
+  const int j = a.ctl->j;  // advanced only by the tridiagonal kernel, after this one
   const bool prof = a.prof && blockIdx.x == 0 && threadIdx.x == 0;
   const unsigned long long c0 = prof ? clock64() : 0;
   const int nv = j + 1;
@@ -540,92 +545,93 @@ __device__ void orth_and_decide(const OrthArgs& a, int j, cg::grid_group& grid) 
   }
   __syncthreads();
   const double bn = bn_s;
-  // q_{j+1} = w / beta_j into the basis and the matvec input (unused when the
-  // step converges or breaks down)
+  // q_{j+1} = w / beta_j (unused when the step converges or breaks down)
   if (j + 1 <= LANCZOS_BLOCK && bn > 0) {
     const double inv = 1.0 / bn;
     double* qn = a.Q + (j + 1) * a.stride;
     for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
       const double v = a.w[x] * inv;
       qn[x] = v;
-      if (a.qcur) a.qcur[x] = v;
+      a.qcur[x] = v;
     }
   }
-  if (blockIdx.x == 0) {
-    __shared__ double sa[LANCZOS_BLOCK], sb[LANCZOS_BLOCK], sbb[LANCZOS_BLOCK];
-    if (threadIdx.x == 0) {
-      a.alpha[j] = alpha_j;
-      a.beta[j] = bn;
-    }
-    for (int i = threadIdx.x; i <= j; i += blockDim.x) {
-      const double ai = i == j ? alpha_j : a.alpha[i], bi = i == j ? bn : a.beta[i];
-      sa[i] = ai;
-      sb[i] = bi;
-      sbb[i] = bi * bi;
-    }
-    __syncthreads();
-    const unsigned long long c4 = prof ? clock64() : 0;
-    __shared__ double th_s, sc_s;
-    __shared__ TwistScratch tw;
-    const int k = j + 1;
-    if (threadIdx.x < 32) {
-      double theta = sa[0], scale = fabs(sa[0]);
-      if (k > 1) {
-        // the previous step's Ritz value / residual bound (this cycle's step j-1)
-        const double theta_prev = a.st->theta, r_prev = a.st->res_bound;
-        __syncwarp();
-        theta = tridiag_lowest_value(sa, sb, sbb, k, true, theta_prev, r_prev, &scale);
-      }
-      if (threadIdx.x == 0) {
-        th_s = theta;
-        sc_s = scale;
-      }
-    }
-    __syncthreads();
-    const double theta = th_s, scale = sc_s;
-    const unsigned long long c45 = prof ? clock64() : 0;
-    if (k > 1)
-      tridiag_vector_twisted(sa, sb, sbb, k, theta, scale, tw, a.s);
-    else if (threadIdx.x == 0)
-      a.s[0] = 1.0;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      if (prof) {
-        const unsigned long long c5 = clock64();
-        a.prof[7] += c5 - c45;  // eigenvector
-        a.prof[0] += c1 - c0;  // pass 1 (dots)
-        a.prof[1] += c2 - c1;  // grid barrier 1
-        a.prof[2] += c3 - c2;  // reduce, pass 2, barrier 2, reduce, pass 3, barrier 3
-        a.prof[3] += c4 - c3;  // ||w||, q_{j+1}
-        a.prof[4] += c5 - c4;  // tridiagonal eigenpair
-        a.prof[5] += 1;
-        a.prof[6] += static_cast<unsigned long long>(j + 1);
-      }
-      if (threadIdx.x == 0) {
-        const double res_bound = bn * fabs(a.s[j]);
-        a.st->theta = theta;
-        a.st->bnorm = bn;
-        a.st->alpha = alpha_j;
-        a.st->res_bound = res_bound;
-        // the reference's step decision (linalg.cpp:141-148)
-        LanczosCtl& c = *a.ctl;
-        const int matvecs = c.matvecs + 1;
-        const double tscale = fmax(1.0, fabs(theta));
-        const bool breakdown = bn <= 1e-14 * tscale;
-        const bool stop = res_bound <= c.tol * tscale || breakdown || j + 1 == c.block ||
-                          matvecs >= c.max_iter;
-        c.matvecs = matvecs;
-        c.steps += 1;
-        if (!stop) c.j = j + 1;
-        if (a.in_graph) cudaGraphSetConditional(a.loop, stop ? 0u : 1u);
-      }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.alpha[j] = alpha_j;
+    a.beta[j] = bn;
+    if (prof) {
+      a.prof[0] += c1 - c0;  // pass 1 (dots)
+      a.prof[1] += c2 - c1;  // grid barrier 1
+      a.prof[2] += c3 - c2;  // reduce, pass 2, barrier 2, reduce, pass 3, barrier 3
+      a.prof[3] += clock64() - c3;  // ||w||, q_{j+1}
     }
   }
 }
 
-__global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  orth_and_decide(a, a.ctl->j, grid);  // ctl->j is written only after the last grid barrier
+// Step j, part 2 (one CTA): lowest eigenpair of T_{j+1}, residual bound and
+// the reference's step decision (linalg.cpp:141-148), which advances ctl->j or
+// ends the loop.  In the graph it runs concurrently with the speculative
+// matvec of q_{j+1} (wasted only on the last step of a cycle).
+__global__ void __launch_bounds__(ORTH_THREADS) lanczos_tridiag_kernel(OrthArgs a) {
+  __shared__ double sa[LANCZOS_BLOCK], sb[LANCZOS_BLOCK], sbb[LANCZOS_BLOCK];
+  __shared__ double th_s, sc_s;
+  __shared__ TwistScratch tw;
+  const int j = a.ctl->j;
+  const bool prof = a.prof && threadIdx.x == 0;
+  const unsigned long long c4 = prof ? clock64() : 0;
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+    const double bi = a.beta[i];
+    sa[i] = a.alpha[i];
+    sb[i] = bi;
+    sbb[i] = bi * bi;
+  }
+  __syncthreads();
+  const int k = j + 1;
+  const double alpha_j = sa[j], bn = sb[j];
+  if (threadIdx.x < 32) {
+    double theta = sa[0], scale = fabs(sa[0]);
+    if (k > 1) {
+      // the previous step's Ritz value / residual bound (this cycle's step j-1)
+      const double theta_prev = a.st->theta, r_prev = a.st->res_bound;
+      __syncwarp();
+      theta = tridiag_lowest_value(sa, sb, sbb, k, true, theta_prev, r_prev, &scale);
+    }
+    if (threadIdx.x == 0) {
+      th_s = theta;
+      sc_s = scale;
+    }
+  }
+  __syncthreads();
+  const double theta = th_s, scale = sc_s;
+  const unsigned long long c45 = prof ? clock64() : 0;
+  if (k > 1)
+    tridiag_vector_twisted(sa, sb, sbb, k, theta, scale, tw, a.s);
+  else if (threadIdx.x == 0)
+    a.s[0] = 1.0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (prof) {
+      const unsigned long long c5 = clock64();
+      a.prof[7] += c5 - c45;  // eigenvector
+      a.prof[4] += c5 - c4;   // tridiagonal eigenpair
+      a.prof[5] += 1;
+      a.prof[6] += static_cast<unsigned long long>(k);
+    }
+    const double res_bound = bn * fabs(a.s[j]);
+    a.st->theta = theta;
+    a.st->bnorm = bn;
+    a.st->alpha = alpha_j;
+    a.st->res_bound = res_bound;
+    LanczosCtl& c = *a.ctl;
+    const int matvecs = c.matvecs + 1;
+    const double tscale = fmax(1.0, fabs(theta));
+    const bool breakdown = bn <= 1e-14 * tscale;
+    const bool stop = res_bound <= c.tol * tscale || breakdown || j + 1 == c.block ||
+                      matvecs >= c.max_iter;
+    c.matvecs = matvecs;
+    c.steps += 1;
+    if (!stop) c.j = j + 1;
+    if (a.in_graph) cudaGraphSetConditional(a.loop, stop ? 0u : 1u);
+  }
 }
 
 struct Kernels {
@@ -795,6 +801,11 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
     lc.numAttrs = 1;
     ACHI_CUDA(cudaLaunchKernelEx(&lc, lanczos_orth_kernel, oa));
     ACHI_LAUNCHED(ctx);
+    return oa;
+  };
+  auto launch_tridiag = [&](const OrthArgs& oa, cudaStream_t s) {
+    lanczos_tridiag_kernel<<<1, ORTH_THREADS, 0, s>>>(oa);
+    ACHI_LAUNCHED(ctx);
   };
   LanczosGraph local;
   struct LocalGuard {
@@ -829,8 +840,15 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
     ACHI_CUDA(cudaStreamBeginCaptureToGraph(ctx.stream, body, nullptr, nullptr, 0,
                                             cudaStreamCaptureModeRelaxed));
     try {
+      // orthogonalise step j; then the tridiagonal/decision kernel on the aux
+      // stream runs concurrently with the (speculative) matvec of q_{j+1}
+      const OrthArgs oa = launch_orth(handle, 1);
+      ACHI_CUDA(cudaEventRecord(ctx.ev_fork, ctx.stream));
+      ACHI_CUDA(cudaStreamWaitEvent(ctx.aux, ctx.ev_fork, 0));
+      launch_tridiag(oa, ctx.aux);
+      ACHI_CUDA(cudaEventRecord(ctx.ev_join, ctx.aux));
       apply(ws.qcur.p, ws.w.p);
-      launch_orth(handle, 1);
+      ACHI_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_join, 0));
     } catch (...) {
       cudaGraph_t dummy;
       cudaStreamEndCapture(ctx.stream, &dummy);
@@ -855,16 +873,17 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
     LanczosCtl* ch = ws.ctl_h.p;
     *ch = LanczosCtl{0, matvecs, block, max_iter, 0, 0, tol};
     ACHI_CUDA(cudaMemcpyAsync(ws.ctl.p, ch, sizeof(LanczosCtl), cudaMemcpyHostToDevice, ctx.stream));
+    apply(ws.qcur.p, ws.w.p);  // w = H q_0; every later matvec runs inside the loop
     if (use_graph) {
       ACHI_CUDA(cudaGraphLaunch(lg.exec, ctx.stream));
     } else {
-      for (int j = 0;;) {  // host-stepped: the kernel advances j unless the loop ends
-        apply(ws.qcur.p, ws.w.p);
-        launch_orth(0, 0);
+      for (int j = 0;;) {  // host-stepped: the tridiagonal kernel advances j unless the loop ends
+        launch_tridiag(launch_orth(0, 0), ctx.stream);
         ACHI_CUDA(cudaMemcpyAsync(ch, ws.ctl.p, sizeof(LanczosCtl), cudaMemcpyDeviceToHost, ctx.stream));
         ctx.sync();
         if (ch->j == j) break;
         j = ch->j;
+        apply(ws.qcur.p, ws.w.p);
       }
     }
     ACHI_CUDA(cudaMemcpyAsync(ch, ws.ctl.p, sizeof(LanczosCtl), cudaMemcpyDeviceToHost, ctx.stream));
