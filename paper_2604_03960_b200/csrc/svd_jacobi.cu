@@ -45,7 +45,7 @@ constexpr int SLD = JW + 4;
 constexpr int CL_ROWS = 256;  // cluster mode: max working rows
 constexpr int CL_MAXP = 8;    // cluster mode: max block pairs (portable cluster size)
 constexpr int MAX_SWEEPS = 40;
-constexpr int RP_ROWS = 4;    // V replay: rows of V per CTA
+constexpr int RP_ROWS = 2;    // V replay: rows of V per CTA
 constexpr double EPS = 2.220446049250313e-16;
 
 __device__ __forceinline__ void mma16x8x4(double (&c)[4], double a0, double a1, double b0) {

@@ -389,3 +389,17 @@ def test_svd_device_factors(ctx, oracle):
         so = oracle.svd(a_h)[1]
         assert np.abs(s_h - so).max() <= 1e-11 * so[0]
         assert np.linalg.norm(a_h - (u_h * s_h) @ vt_h) <= 1e-12 * np.linalg.norm(a_h)
+
+
+@pytest.mark.slow
+def test_dmrg_large_chi_paths(ctx, oracle):
+    """Fixed chi = 256 at N = 20: the centre bonds take the TMA GEMM H_eff path
+    (chi > 128) and the streamed Jacobi SVD (working matrix 512 wide, > 256), the
+    edges the small-chi paths; sweep energies and chi profiles against the oracle
+    (real-gauge restatement of run_dmrg)."""
+    spec = abi.model_spec(20)
+    cfg = abi.fixed_config(256, max_sweeps=5)  # chi grows by up to d^2 per sweep from Neel
+    g = ctx.run_dmrg(spec, cfg)
+    o = oracle.run_dmrg(spec, cfg)
+    compare_runs(g, o)
+    assert max(g["chi_profiles"][-1]) > 128
