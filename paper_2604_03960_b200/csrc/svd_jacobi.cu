@@ -724,7 +724,7 @@ __global__ void load_g_kernel(const double* __restrict__ theta, long tstride, in
 // is undefined and their norm is below the reference's own normwise accuracy):
 // they are not rotated and do not enter the convergence measure.
 __global__ void zero_floor_kernel(const double* __restrict__ G, long gstride, long len, int mg,
-                                  double* __restrict__ zero2) {
+                                  double frel, double* __restrict__ zero2) {
   __shared__ double sh[32];
   const double* g = G + blockIdx.x * gstride;
   double s = 0.0;
@@ -736,7 +736,7 @@ __global__ void zero_floor_kernel(const double* __restrict__ G, long gstride, lo
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < (blockDim.x >> 5); ++w) t += sh[w];
-    const double f = 64.0 * sqrt(static_cast<double>(mg)) * EPS;
+    const double f = frel > 0 ? frel : 64.0 * sqrt(static_cast<double>(mg)) * EPS;
     zero2[2 * blockIdx.x] = f * f * t;
     zero2[2 * blockIdx.x + 1] = t > 0 ? 1.0 / t : 1.0;  // 1 / ||G||_F^2
   }
@@ -876,7 +876,11 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
         ACHI_LAUNCHED(ctx);
       }
     }
-    zero_floor_kernel<<<batch, 1024, 0, ctx.stream>>>(G, gstride, gstride, mg, zero2);
+    static const double frel = [] {  // study knob: relative noise floor (default 64 sqrt(m) eps)
+      const char* e = std::getenv("ACHI_JACOBI_FLOOR");
+      return e ? std::atof(e) : 0.0;
+    }();
+    zero_floor_kernel<<<batch, 1024, 0, ctx.stream>>>(G, gstride, gstride, mg, frel, zero2);
     ACHI_LAUNCHED(ctx);
     if (v_init) {
       // G <- G v_init: col-major G (ldg x ng) is row-major G^T, so (G v)^T = v^T G^T
