@@ -59,7 +59,14 @@ enum { ACHI_SPIN_HALF = 0, ACHI_PAULI = 1 };
 enum { ACHI_MODE_FIXED = 0, ACHI_MODE_THRESHOLD = 1, ACHI_MODE_DIRECT = 2, ACHI_MODE_PID = 3 };
 enum { ACHI_PREDICT_OFF = 0, ACHI_PREDICT_LINEAR = 1, ACHI_PREDICT_QUADRATIC = 2 };
 enum { ACHI_PID_ADDITIVE = 0, ACHI_PID_MULTIPLICATIVE = 1 };
-enum { ACHI_INIT_AUTOMATIC = 0, ACHI_INIT_NEEL = 1, ACHI_INIT_RANDOM = 2 };
+/* Initial state (dmrg.cpp:222-235).  ACHI_INIT_RANDOM is the reference's complex
+ * random_mps (mps.cpp:75-95) and is rejected by the real FP64 path.
+ * ACHI_INIT_RANDOM_REAL draws the same mt19937_64(seed) normal sequence, one
+ * real value per entry, on capped_bond_dims(n, 2, chi_min) (mps.cpp:60-73),
+ * then canonicalize(psi, 0) and normalise as random_mps does.  On the real path
+ * ACHI_INIT_AUTOMATIC resolves to RANDOM_REAL for the transverse-field Ising
+ * family (its Hamiltonian is real, so its ground state is real). */
+enum { ACHI_INIT_AUTOMATIC = 0, ACHI_INIT_NEEL = 1, ACHI_INIT_RANDOM = 2, ACHI_INIT_RANDOM_REAL = 3 };
 
 typedef struct achi_model_spec {
   int32_t family;      /* ACHI_HEISENBERG_XXZ | ACHI_TRANSVERSE_ISING */

@@ -616,6 +616,30 @@ inline MPS<cd> random_mps(int n, int d, int chi, uint64_t seed) {
   return psi;
 }
 
+// Real-valued variant of random_mps for the real FP64 path: the same
+// mt19937_64(seed) normal sequence, one draw per entry (not part of the
+// reference; the product path's ACHI_INIT_RANDOM_REAL mirrors it).
+template <class T>
+MPS<T> random_mps_real(int n, int d, int chi, uint64_t seed) {
+  if (chi < 1) fail(E_INVALID_RANK, "random_mps: chi must be >= 1");
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  auto dims = capped_bond_dims(n, d, chi);
+  MPS<T> psi;
+  for (int i = 0; i < n; ++i) {
+    long l = i == 0 ? 1 : dims[i - 1];
+    long r = i == n - 1 ? 1 : dims[i];
+    Tensor<T> t({l, d, r});
+    for (long k = 0; k < t.size(); ++k) t.data[k] = T(gauss(rng));
+    psi.sites.push_back(std::move(t));
+  }
+  canonicalize(psi, 0);
+  double nrm = psi.sites[0].norm();
+  if (!(nrm > 0)) fail(E_NUMERICAL_FAILURE, "random_mps: zero-norm state");
+  for (auto& x : psi.sites[0].data) x *= 1.0 / nrm;
+  return psi;
+}
+
 // ---- controller (controller.cpp:12-190) -------------------------------------
 struct ControllerConfig {
   int mode = 3;  // fixed, threshold, direct, pid
@@ -1107,8 +1131,11 @@ SweepRecord two_site_sweep(MPS<T>& psi, const std::vector<Tensor<T>>& mpo, Envir
 template <class T>
 void init_run(const ModelSpec& spec, const DmrgConfig& cfg, MPS<T>& psi) {
   int init = cfg.initial_state;
-  if (init == 0) init = spec.family == 0 ? 1 : 2;
-  if (init == 1) {
+  // automatic (dmrg.cpp:222-225): TFIM -> random; on the real path random_real
+  if (init == 0) init = spec.family == 0 ? 1 : (std::is_same_v<T, cd> ? 2 : 3);
+  if (init == 3) {
+    psi = random_mps_real<T>(spec.n, 2, cfg.controller.chi_min, cfg.seed);
+  } else if (init == 1) {
     std::vector<int> basis(spec.n);
     for (int i = 0; i < spec.n; ++i) basis[i] = i % 2;
     psi = product_state<T>(spec.n, 2, basis);

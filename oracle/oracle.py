@@ -331,7 +331,21 @@ def build_mpo(spec, real_gauge=True):
     return sites
 
 
+def tfim_free_fermion_energy(n, coupling_j, field_h, convention):
+    """tfim_free_fermion_energy (models.cpp:225-239): E0 = -1/2 sum of the
+    singular values of M = 2(h I - j L), L the lower shift (open chain)."""
+    j, h = coupling_j, field_h
+    if convention == abi.SPIN_HALF:
+        j, h = j * 0.25, h * 0.5
+    m = np.diag(np.full(n, 2.0 * h)) + np.diag(np.full(n - 1, -2.0 * j), -1)
+    return -0.5 * float(np.linalg.svd(m, compute_uv=False).sum())
+
+
 def exact_ground_energy(spec, cap=14):
+    """exact_ground_energy (models.cpp:241-259): free fermions for the
+    transverse-field Ising family, matrix-free Lanczos for XXZ (n <= cap)."""
+    if spec.family == abi.TRANSVERSE_ISING:
+        return tfim_free_fermion_energy(spec.n, spec.jz, spec.h, spec.convention)
     out = C.c_double()
     buf, bl = _err()
     _check(lib().oracle_exact_ground_energy(C.byref(spec), cap, C.byref(out), buf,

@@ -18,7 +18,7 @@ SPIN_HALF, PAULI = 0, 1
 MODE_FIXED, MODE_THRESHOLD, MODE_DIRECT, MODE_PID = 0, 1, 2, 3
 PREDICT_OFF, PREDICT_LINEAR, PREDICT_QUADRATIC = 0, 1, 2
 PID_ADDITIVE, PID_MULTIPLICATIVE = 0, 1
-INIT_AUTOMATIC, INIT_NEEL, INIT_RANDOM = 0, 1, 2
+INIT_AUTOMATIC, INIT_NEEL, INIT_RANDOM, INIT_RANDOM_REAL = 0, 1, 2, 3
 
 ERROR_NAMES = {
     1: "Error", 2: "InvalidMatrix", 3: "NumericalFailure", 4: "InvalidRank",

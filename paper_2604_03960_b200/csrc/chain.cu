@@ -3,6 +3,7 @@
 #include <chrono>
 #include <cmath>
 #include <limits>
+#include <random>
 
 #include "chain.cuh"
 
@@ -109,6 +110,121 @@ std::vector<std::vector<double>> neel_canonical(int n, int d) {
   return s;
 }
 
+// capped_bond_dims (mps.cpp:60-73): min(chi, d^k, d^(n-k)) per bond
+std::vector<int> capped_bond_dims(int n, int d, int chi) {
+  std::vector<int> dims(n - 1, chi);
+  long grow = 1;
+  for (int i = 0; i < n - 1; ++i) {
+    grow = std::min<long>(grow * d, chi);
+    dims[i] = static_cast<int>(std::min<long>(dims[i], grow));
+  }
+  grow = 1;
+  for (int i = n - 2; i >= 0; --i) {
+    grow = std::min<long>(grow * d, chi);
+    dims[i] = static_cast<int>(std::min<long>(dims[i], grow));
+  }
+  return dims;
+}
+
+// Thin Householder QR of a column-major m x k matrix (m >= k), reflector
+// signs as LAPACK dlarfg (beta = -sign(alpha) * ||x||): a -> Q (m x k),
+// r -> R (k x k, upper).  Setup-sized (chi_min columns), host side.
+void householder_qr(std::vector<double>& a, int m, int k, std::vector<double>& r) {
+  std::vector<double> v(static_cast<size_t>(m) * k, 0.0), tau(k, 0.0);
+  auto A = [&](int i, int j) -> double& { return a[static_cast<size_t>(j) * m + i]; };
+  for (int j = 0; j < k; ++j) {
+    double xn = 0;
+    for (int i = j + 1; i < m; ++i) xn += A(i, j) * A(i, j);
+    xn = std::sqrt(xn);
+    const double alpha = A(j, j);
+    double* vj = &v[static_cast<size_t>(j) * m];
+    vj[j] = 1.0;
+    if (xn == 0.0) {
+      tau[j] = 0.0;
+    } else {
+      const double beta = alpha >= 0 ? -std::hypot(alpha, xn) : std::hypot(alpha, xn);
+      tau[j] = (beta - alpha) / beta;
+      for (int i = j + 1; i < m; ++i) vj[i] = A(i, j) / (alpha - beta);
+      A(j, j) = beta;
+      for (int i = j + 1; i < m; ++i) A(i, j) = 0.0;
+      for (int c = j + 1; c < k; ++c) {  // apply H_j to the trailing columns
+        double s = 0;
+        for (int i = j; i < m; ++i) s += vj[i] * A(i, c);
+        s *= tau[j];
+        for (int i = j; i < m; ++i) A(i, c) -= s * vj[i];
+      }
+    }
+  }
+  r.assign(static_cast<size_t>(k) * k, 0.0);
+  for (int j = 0; j < k; ++j)
+    for (int i = 0; i <= j; ++i) r[static_cast<size_t>(j) * k + i] = A(i, j);
+  // Q = H_0 ... H_{k-1} [I_k; 0]
+  std::fill(a.begin(), a.end(), 0.0);
+  for (int j = 0; j < k; ++j) A(j, j) = 1.0;
+  for (int j = k - 1; j >= 0; --j) {
+    const double* vj = &v[static_cast<size_t>(j) * m];
+    for (int c = 0; c < k; ++c) {
+      double s = 0;
+      for (int i = j; i < m; ++i) s += vj[i] * A(i, c);
+      s *= tau[j];
+      for (int i = j; i < m; ++i) A(i, c) -= s * vj[i];
+    }
+  }
+}
+
+// canonicalize(psi, 0) (mps.cpp:172-210) for right moves only: push_left on
+// sites n-1..1.  Site k is (dims[k], d, dims[k+1]) row-major; push_left may
+// shrink dims[k] to min(d * dims[k+1], dims[k]).
+void canonicalize_left(std::vector<std::vector<double>>& s, std::vector<int>& dims, int d) {
+  const int n = static_cast<int>(s.size());
+  for (int i = n - 1; i >= 1; --i) {
+    const int l = dims[i], r = dims[i + 1], m = d * r, k = std::min(m, l);
+    // M^T with M = site as l x (d r): column-major (m x l) buffer == site row-major
+    std::vector<double> a(s[i].begin(), s[i].end()), rr;
+    if (k < l) fail(ACHI_E_INVALID_RANK, "canonicalize: bond wider than d * right bond");
+    householder_qr(a, m, k, rr);
+    // site i <- Q^T (k x m) row-major == Q column-major (m x k)
+    s[i] = a;
+    // site i-1 (ll*d x l) <- site i-1 * R^T
+    const int ll = dims[i - 1];
+    std::vector<double> nb(static_cast<size_t>(ll) * d * k, 0.0);
+    for (int row = 0; row < ll * d; ++row)
+      for (int c = 0; c < k; ++c) {
+        double acc = 0;  // (R^T)(t, c) = R(c, t), nonzero for t >= c
+        for (int t = c; t < l; ++t) acc += s[i - 1][static_cast<size_t>(row) * l + t] * rr[static_cast<size_t>(t) * k + c];
+        nb[static_cast<size_t>(row) * k + c] = acc;
+      }
+    s[i - 1] = nb;
+    dims[i] = k;
+  }
+}
+
+// random_mps (mps.cpp:75-95) with one real normal draw per entry, then the
+// second canonicalize of run_dmrg (dmrg.cpp:236).
+std::vector<std::vector<double>> random_real_canonical(int n, int d, int chi, uint64_t seed,
+                                                       std::vector<int>& dims_out) {
+  if (chi < 1) fail(ACHI_E_INVALID_RANK, "random_mps: chi must be >= 1");
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  const auto cd = capped_bond_dims(n, d, chi);
+  std::vector<int> dims(n + 1, 1);
+  for (int k = 1; k < n; ++k) dims[k] = cd[k - 1];
+  std::vector<std::vector<double>> s(n);
+  for (int i = 0; i < n; ++i) {
+    s[i].resize(static_cast<size_t>(dims[i]) * d * dims[i + 1]);
+    for (double& x : s[i]) x = gauss(rng);
+  }
+  canonicalize_left(s, dims, d);
+  double nrm = 0;
+  for (double x : s[0]) nrm += x * x;
+  nrm = std::sqrt(nrm);
+  if (!(nrm > 0)) fail(ACHI_E_NUMERICAL_FAILURE, "random_mps: zero-norm state");
+  for (double& x : s[0]) x /= nrm;
+  canonicalize_left(s, dims, d);
+  dims_out = dims;
+  return s;
+}
+
 __global__ void set_boundary_kernel(double* p) { p[0] = 1.0; }
 
 }  // namespace
@@ -122,8 +238,9 @@ void Chain::create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g) 
   n = s.n;
   mpo = build_mpo_real(s);
   int init = g.initial_state;
-  if (init == ACHI_INIT_AUTOMATIC) init = s.family == ACHI_HEISENBERG_XXZ ? ACHI_INIT_NEEL : ACHI_INIT_RANDOM;
-  if (init != ACHI_INIT_NEEL)
+  if (init == ACHI_INIT_AUTOMATIC)
+    init = s.family == ACHI_HEISENBERG_XXZ ? ACHI_INIT_NEEL : ACHI_INIT_RANDOM_REAL;
+  if (init != ACHI_INIT_NEEL && init != ACHI_INIT_RANDOM_REAL)
     fail(ACHI_E_UNSUPPORTED_MODEL,
          "random complex initial state (random_mps, mps.cpp:75-95) is not on the real FP64 path");
   // mixing matrices
@@ -184,8 +301,15 @@ void Chain::create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g) 
   ACHI_LAUNCHED(c);
   set_boundary_kernel<<<1, 1, 0, c.stream>>>(R[n - 1].p);
   ACHI_LAUNCHED(c);
-  // Neel + canonicalize, environments, controller cold start (dmrg.cpp:222-250)
-  upload_sites(neel_canonical(n, d));
+  // initial state + canonicalize, environments, controller cold start (dmrg.cpp:222-250)
+  if (init == ACHI_INIT_NEEL) {
+    upload_sites(neel_canonical(n, d));
+  } else {
+    std::vector<int> dims;
+    auto hs = random_real_canonical(n, d, g.controller.chi_min, g.seed, dims);
+    for (int k = 1; k < n; ++k) chi[k] = dims[k];
+    upload_sites(hs);
+  }
   std::vector<achi_bond_state> st(n - 1);
   for (auto& b : st) {
     b = achi_bond_state{};
@@ -250,6 +374,13 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   const int sm_ = chlp * d, sn_ = d * chrp, smt = chl * d, snt = d * chr;
   VKeep& vk = vkeep[2 * static_cast<size_t>(b) + (right ? 1 : 0)];
   const bool warm = warm_svd && vk.valid && vk.m == sm_ && vk.n == sn_ && vk.mt == smt && vk.nt == snt;
+  static const char* dump_path = std::getenv("ACHI_SVD_DUMP");  // debug: input of a failing SVD
+  std::vector<double> dump;
+  if (dump_path) {
+    dump.resize(static_cast<size_t>(sm_) * sn_);
+    ACHI_CUDA(cudaMemcpyAsync(dump.data(), vec.p, sizeof(double) * dump.size(),
+                              cudaMemcpyDeviceToHost, c.stream));
+  }
   SvdResultDev sr = svd_device(c, svd, vec.p, sm_, sn_, smt, snt, side, 1, 0, nullptr, true,
                                warm ? vk.v.p : nullptr);
   if (warm_svd) {  // keep this factor for the next visit of the bond in this direction
@@ -265,7 +396,19 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   c.acc.end(c.stream, 0.0);
   c.sync();
   c.acc.resolve();
-  const int svd_sweeps = sr.sweeps();
+  int svd_sweeps = 0;
+  try {
+    svd_sweeps = sr.sweeps();
+  } catch (const Error&) {
+    if (dump_path)
+      if (FILE* f = std::fopen(dump_path, "wb")) {
+        const int32_t hdr[6] = {sm_, sn_, smt, snt, right ? 1 : 0, warm ? 1 : 0};
+        std::fwrite(hdr, sizeof(hdr), 1, f);
+        std::fwrite(dump.data(), sizeof(double), dump.size(), f);
+        std::fclose(f);
+      }
+    throw;
+  }
   // algorithmic FP64 flops of the blocked Jacobi: per sweep
   // C(ng/16, 2) block pairs x 2 * 32^2 * (2 mg + ng) (Gram + rotation of G,
   // rotation of V) ~= 4 ng^2 (2 mg + ng)

@@ -108,6 +108,7 @@ struct Small {
   double S[2][JW][SLD];  // double-buffered Gram (one barrier per inner step)
   double J[JW][SLD];
   double red[JT / 32];
+  double red2[JT / 32];
   unsigned char pi[JW - 1][JW / 2], pj[JW - 1][JW / 2];
 };
 
@@ -223,9 +224,16 @@ __device__ void init_pair_tables(Small& sm) {
 }
 
 // Gram tile (from the warp's DMMA accumulator) -> S[0], J = I, off-diagonal
-// measure max |S_ij| / sqrt(S_ii S_jj) over non-noise columns -> sm.red[0];
+// measure c = max |S_ij| / sqrt(S_ii S_jj) over non-noise columns -> sm.red[0];
 // inner Jacobi when the measure exceeds tol.  Returns true when rotated.
-__device__ bool finish_gram(Small& sm, const double (&acc)[4], double z2, double tol, int max_inner) {
+// The stop measure -> sm.red2[0] weights each pair by the relative norm of its
+// smaller column, w = c * (min(|x_i|, |x_j|) / ||G||_F)^(1/2): a residual
+// cosine c moves the singular values by at most ~c^2 min|x| (second order),
+// so w < stop_tol bounds that error by stop_tol^2 ||G||_F for every column,
+// while a column a few orders above the noise floor (whose direction is only
+// defined to ~noise/|x|) no longer holds the stop test open forever.
+__device__ bool finish_gram(Small& sm, const double (&acc)[4], double z2, double ig2, double tol,
+                            int max_inner) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3, mt = warp >> 2, nt = warp & 3;
   {
@@ -242,21 +250,34 @@ __device__ bool finish_gram(Small& sm, const double (&acc)[4], double z2, double
   __syncthreads();
   // squared measure with a reciprocal estimate (2^-23 relative: only compared
   // with thresholds), one square root at the end
-  double meas2 = 0.0;
+  double meas2 = 0.0, w4 = 0.0;
   for (int idx = threadIdx.x; idx < JW * JW; idx += JT) {
     const int i = idx / JW, j = idx - i * JW;
     const double sii = sm.S[0][i][i], sjj = sm.S[0][j][j], sij = sm.S[0][i][j];
-    if (i < j && sii > z2 && sjj > z2)
-      meas2 = fmax(meas2, __dmul_rn(__dmul_rn(sij, sij), rcp_approx(__dmul_rn(sii, sjj))));
+    if (i < j && sii > z2 && sjj > z2) {
+      const double c2 = __dmul_rn(__dmul_rn(sij, sij), rcp_approx(__dmul_rn(sii, sjj)));
+      meas2 = fmax(meas2, c2);
+      w4 = fmax(w4, __dmul_rn(__dmul_rn(c2, c2), __dmul_rn(fmin(sii, sjj), ig2)));
+    }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) meas2 = fmax(meas2, __shfl_xor_sync(0xffffffffu, meas2, o));
-  if (lane == 0) sm.red[warp] = meas2;
+  for (int o = 16; o > 0; o >>= 1) {
+    meas2 = fmax(meas2, __shfl_xor_sync(0xffffffffu, meas2, o));
+    w4 = fmax(w4, __shfl_xor_sync(0xffffffffu, w4, o));
+  }
+  if (lane == 0) {
+    sm.red[warp] = meas2;
+    sm.red2[warp] = w4;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double m = 0;
-    for (int w = 0; w < JT / 32; ++w) m = fmax(m, sm.red[w]);
+    double m = 0, w = 0;
+    for (int k = 0; k < JT / 32; ++k) {
+      m = fmax(m, sm.red[k]);
+      w = fmax(w, sm.red2[k]);
+    }
     sm.red[0] = sqrt(m);
+    sm.red2[0] = sqrt(sqrt(w));
   }
   __syncthreads();
   const bool rotate = sm.red[0] > tol;
@@ -360,7 +381,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_cluster_kernel(ClArgs a) {
   Small& sm = *reinterpret_cast<Small*>(X0 + 2 * bufsz);
   init_pair_tables(sm);
   double* G = a.G + b * a.gstride;
-  const double z2 = a.zero2[2 * b];
+  const double z2 = a.zero2[2 * b], ig2 = a.zero2[2 * b + 1];
   const int nb = a.nb, rounds = nb - 1;
   int ba, bb;
   circle_pair_ns(nb, 0, p, ba, bb);
@@ -384,9 +405,9 @@ __global__ void __launch_bounds__(JT, 1) jacobi_cluster_kernel(ClArgs a) {
       double acc[4] = {0, 0, 0, 0};
       gram_resident(X, cld, a.rows_pad, acc);
       const long long t1 = prof ? clock64() : 0;
-      const bool rot = finish_gram(sm, acc, z2, a.tol, a.max_inner);
+      const bool rot = finish_gram(sm, acc, z2, ig2, a.tol, a.max_inner);
       const long long t2 = prof ? clock64() : 0;
-      if (threadIdx.x == 0) meas_slot[sweep % 3] = fmax(meas_slot[sweep % 3], sm.red[0]);
+      if (threadIdx.x == 0) meas_slot[sweep % 3] = fmax(meas_slot[sweep % 3], sm.red2[0]);
       if (a.jrec) {
         const long slot = (b * a.jstride + rg) * a.npairs + p;
         if (threadIdx.x == 0) a.jflag[slot] = rot ? 1 : 0;
@@ -638,7 +659,7 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
   const int p = blockIdx.x % a.npairs, b = a.batch0 + blockIdx.x / a.npairs;
   double* G = a.G + b * a.gstride;
   double* V = a.V ? a.V + b * a.vstride : nullptr;
-  const double z2 = a.zero2[2 * b];
+  const double z2 = a.zero2[2 * b], ig2 = a.zero2[2 * b + 1];
   const int nch = (a.mg + JCH - 1) / JCH;
   int sweep = 0;
   for (; sweep < MAX_SWEEPS; ++sweep) {
@@ -660,9 +681,9 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
         gram_chunk(X[k % STREAM_STAGES], acc);
         __syncthreads();
       }
-      const bool rot = finish_gram(sm, acc, z2, a.tol, a.max_inner);
+      const bool rot = finish_gram(sm, acc, z2, ig2, a.tol, a.max_inner);
       if (threadIdx.x == 0)
-        atomicMax(&a.conv[sweep], static_cast<unsigned long long>(__double_as_longlong(sm.red[0])));
+        atomicMax(&a.conv[sweep], static_cast<unsigned long long>(__double_as_longlong(sm.red2[0])));
       if (rot) {
         stream_rotate(X, G, a.ldg, a.mg, ca, cb, sm);
         if (V) stream_rotate(X, V, a.ldv, a.vrows, ca, cb, sm);

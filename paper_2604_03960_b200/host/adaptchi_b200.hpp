@@ -395,7 +395,7 @@ struct DmrgConfig {
   double eig_tol = 1e-10;
   int eig_max_iter = 200;
   ctrl::ControllerConfig controller{};
-  enum class InitialState { automatic, neel, random };
+  enum class InitialState { automatic, neel, random, random_real };
   InitialState initial_state = InitialState::automatic;
   uint64_t seed = 1234;
   double noise_floor = 1e-14;

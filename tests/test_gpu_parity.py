@@ -248,12 +248,16 @@ def test_eigs_nonconvergence(ctx):  # test_linalg.cpp:208-226
 
 # ---------------- full local update: DMRG parity ----------------
 
-def compare_runs(g, o, e_rel=1e-10):
+def compare_runs(g, o, e_rel=1e-10, s_tol=1e-8, s_tol_first=None):
     assert g["n_sweeps"] == o["n_sweeps"]
     for a, b in zip(g["energies"], o["energies"]):
         assert abs(a - b) <= e_rel * abs(b), (a, b)
     assert np.array_equal(g["chi_profiles"], o["chi_profiles"])
-    assert np.abs(g["entropy_profiles"] - o["entropy_profiles"]).max() <= 1e-8
+    ds = np.abs(g["entropy_profiles"] - o["entropy_profiles"])
+    if s_tol_first is not None:
+        assert ds[0].max() <= s_tol_first
+        ds = ds[1:]
+    assert ds.max(initial=0.0) <= s_tol
     assert [v.kept for v in g["visits"]] == [v.kept for v in o["visits"]]
 
 
@@ -403,3 +407,72 @@ def test_dmrg_large_chi_paths(ctx, oracle):
     o = oracle.run_dmrg(spec, cfg)
     compare_runs(g, o)
     assert max(g["chi_profiles"][-1]) > 128
+
+
+# ---------------- transverse-field Ising family ----------------
+
+def tfim(n, h):  # acceptance_main.cpp:39-47
+    return abi.model_spec(n, family=abi.TRANSVERSE_ISING, jz=1.0, h=h)
+
+
+@pytest.mark.parametrize("n,h", [(8, 1.0), (8, 0.2), (12, 1.0), (12, 0.2)])
+def test_dmrg_tfim_criterion1_parity(ctx, oracle, n, h):  # acceptance_main.cpp:73-104
+    """Automatic init resolves to the real random start on both sides; the
+    GPU trajectory equals the oracle's and the energy matches free fermions."""
+    spec = tfim(n, h)
+    cfg = abi.fixed_config(1 << (n // 2), eps_conv=1e-11, max_sweeps=16)
+    cfg.eig_tol, cfg.eig_max_iter = 1e-12, 400
+    g = ctx.run_dmrg(spec, cfg)
+    o = oracle.run_dmrg(spec, cfg)
+    # ordered phase (h=0.2): the two lowest states form a doublet split by
+    # ~h^n (4e-9 at n=12), so the eigenvector inside it -- and with it the
+    # bond entropies -- is fixed only to ~eig_tol*|E|/split; any mixture is
+    # an exact ground state.  Energies, sweep counts and chi profiles stay exact.
+    compare_runs(g, o, s_tol=1e-8 if h >= 1 else 1.0)
+    assert abs(g["energy"] - oracle.exact_ground_energy(spec)) <= 1e-8
+
+
+def test_dmrg_tfim_criterion4_parity(ctx, oracle):  # acceptance_main.cpp:159-174
+    spec = tfim(20, 1.0)
+    cfg = abi.adaptive_config(64, 1e-10)
+    g = ctx.run_dmrg(spec, cfg)
+    o = oracle.run_dmrg(spec, cfg)
+    compare_runs(g, o)
+    gt = [(t.chi, t.delta_chi, t.clamped) for t in g["trace"]]
+    ot = [(t.chi, t.delta_chi, t.clamped) for t in o["trace"]]
+    assert gt == ot
+    epn = g["energy"] / 20
+    assert abs(epn + 1.25539) <= 1e-4
+    assert abs(epn - oracle.exact_ground_energy(spec) / 20) <= 1e-4
+
+
+def test_acceptance_criterion3_energies(ctx):  # acceptance_main.cpp:130-157 (energy caps)
+    rows = [(abi.model_spec(20), 1e-4), (tfim(20, 1.0), 1e-8), (tfim(20, 0.2), 1e-8),
+            (abi.model_spec(20, jz=1.5), 1e-4)]
+    for spec, cap in rows:
+        f = ctx.run_dmrg(spec, abi.fixed_config(64))
+        a = ctx.run_dmrg(spec, abi.adaptive_config(64, 1e-10))
+        assert f["converged"] and a["converged"]
+        assert abs(a["energy"] - f["energy"]) / 20 <= cap
+
+
+@pytest.mark.parametrize("family", ["heisenberg", "ising_critical"])
+def test_acceptance_criteria6_7(ctx, family):  # acceptance_main.cpp:206-273
+    spec, eps = (abi.model_spec(20), 1e-5) if family == "heisenberg" else (tfim(20, 1.0), 1e-10)
+    base = abi.adaptive_config(64, eps)
+    ref = ctx.run_dmrg(spec, base)
+    for scale in (0.5, 0.75, 1.25, 1.5):  # criterion 6: gain robustness
+        cfg = abi.adaptive_config(64, eps)
+        cfg.controller.kp *= scale
+        cfg.controller.ki *= scale
+        cfg.controller.kd *= scale
+        r = ctx.run_dmrg(spec, cfg)
+        assert abs(r["energy"] - ref["energy"]) / 20 <= 1e-4 and r["n_sweeps"] == ref["n_sweeps"]
+    b0 = abi.adaptive_config(64, eps)
+    b0.controller.beta_predict = 0.0
+    r0 = ctx.run_dmrg(spec, b0)
+    for beta in (0.4, 0.8):  # criterion 7: predictor neutrality
+        cfg = abi.adaptive_config(64, eps)
+        cfg.controller.beta_predict = beta
+        r = ctx.run_dmrg(spec, cfg)
+        assert abs(r["energy"] - r0["energy"]) <= 1e-8 and r["n_sweeps"] == r0["n_sweeps"]

@@ -343,3 +343,74 @@ def test_acceptance_criterion_2(oracle):  # acceptance_main.cpp:106-126
     assert abs(p["energy"] / 20 - f["energy"] / 20) <= 1e-4
     assert p["records"][-1].average_chi <= 10.0 and p["max_chi_used"] <= 14
     assert f["converged"] and p["converged"]
+
+
+def tfim(n, h):  # acceptance_main.cpp:39-47
+    return abi.model_spec(n, family=abi.TRANSVERSE_ISING, jz=1.0, h=h)
+
+
+def test_tfim_free_fermion_small_n(oracle):  # models.cpp:225-239 vs ED of the dense MPO
+    for n, h in [(4, 1.0), (6, 0.2), (8, 0.7)]:
+        spec = tfim(n, h)
+        hd = dense_from_mpo(oracle.build_mpo(spec))
+        assert abs(np.linalg.eigvalsh(hd)[0] - oracle.exact_ground_energy(spec)) <= 1e-10
+
+
+def test_acceptance_criterion_1_tfim_rows(oracle):  # acceptance_main.cpp:73-104 (Ising rows)
+    for n in (4, 6, 8, 10, 12):
+        for h in (1.0, 0.2):
+            spec = tfim(n, h)
+            cfg = abi.fixed_config(1 << (n // 2), eps_conv=1e-11, max_sweeps=16)
+            cfg.eig_tol, cfg.eig_max_iter = 1e-12, 400
+            r = oracle.run_dmrg(spec, cfg)  # automatic init -> random real on the real path
+            assert abs(r["energy"] - oracle.exact_ground_energy(spec)) <= 1e-8
+
+
+def test_acceptance_criterion_4(oracle):  # acceptance_main.cpp:159-174
+    spec = tfim(20, 1.0)
+    r = oracle.run_dmrg(spec, abi.adaptive_config(64, 1e-10))
+    epn = r["energy"] / 20
+    assert abs(epn + 1.25539) <= 1e-4
+    assert abs(epn - oracle.exact_ground_energy(spec) / 20) <= 1e-4
+
+
+def test_random_real_init_real_equals_complex_mode(oracle):
+    """ACHI_INIT_RANDOM_REAL: the real-gauge run and the complex128 run of the
+    same real random start agree (energies 1e-12 rel, identical chi profiles)."""
+    spec = tfim(20, 1.0)
+    cfg = abi.adaptive_config(64, 1e-10)
+    cfg.initial_state = abi.INIT_RANDOM_REAL
+    r = oracle.run_dmrg(spec, cfg)
+    c = oracle.run_dmrg(spec, cfg, complex_mode=True)
+    assert r["n_sweeps"] == c["n_sweeps"]
+    assert np.array_equal(r["chi_profiles"], c["chi_profiles"])
+    for a, b in zip(r["energies"], c["energies"]):
+        assert abs(a - b) <= 1e-12 * abs(b)
+    cfg.initial_state = abi.INIT_RANDOM  # complex random_mps needs complex arithmetic
+    with pytest.raises(Exception, match="UnsupportedModel"):
+        oracle.run_dmrg(spec, cfg)
+
+
+def test_acceptance_criteria_3_6_7(oracle):  # acceptance_main.cpp:130-157,206-273 (energies, sweeps)
+    for spec, cap in [(abi.model_spec(20), 1e-4), (tfim(20, 1.0), 1e-8), (tfim(20, 0.2), 1e-8),
+                      (abi.model_spec(20, jz=1.5), 1e-4)]:
+        f = oracle.run_dmrg(spec, abi.fixed_config(64))
+        a = oracle.run_dmrg(spec, abi.adaptive_config(64, 1e-10))
+        assert f["converged"] and a["converged"] and abs(a["energy"] - f["energy"]) / 20 <= cap
+    for spec, eps in [(abi.model_spec(20), 1e-5), (tfim(20, 1.0), 1e-10)]:
+        ref = oracle.run_dmrg(spec, abi.adaptive_config(64, eps))
+        for scale in (0.5, 0.75, 1.25, 1.5):
+            cfg = abi.adaptive_config(64, eps)
+            cfg.controller.kp *= scale
+            cfg.controller.ki *= scale
+            cfg.controller.kd *= scale
+            r = oracle.run_dmrg(spec, cfg)
+            assert abs(r["energy"] - ref["energy"]) / 20 <= 1e-4 and r["n_sweeps"] == ref["n_sweeps"]
+        b0 = abi.adaptive_config(64, eps)
+        b0.controller.beta_predict = 0.0
+        r0 = oracle.run_dmrg(spec, b0)
+        for beta in (0.4, 0.8):
+            cfg = abi.adaptive_config(64, eps)
+            cfg.controller.beta_predict = beta
+            r = oracle.run_dmrg(spec, cfg)
+            assert abs(r["energy"] - r0["energy"]) <= 1e-8 and r["n_sweeps"] == r0["n_sweeps"]
