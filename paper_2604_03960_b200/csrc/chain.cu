@@ -416,11 +416,14 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
     c.acc.work[EventAcc::kSvd] += 4.0 * svd_sweeps * static_cast<double>(sr.ng) * sr.ng *
                                   (2.0 * sr.mg + sr.ng);
   const auto t2 = clk::now();
-  static const bool visit_log = std::getenv("ACHI_VISIT_LOG") != nullptr;
+  static const int visit_log = [] {  // 1: slow visits only, 2: every visit
+    const char* e = std::getenv("ACHI_VISIT_LOG");
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
   if (visit_log) {
     const double svd_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
     const double lz_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
-    if (svd_ms > 5.0 || lz_ms > 20.0)
+    if (visit_log >= 2 || svd_ms > 5.0 || lz_ms > 20.0)
       std::fprintf(stderr, "[visit] sweep %d bond %d %s chl %d chr %d lanczos %.2f ms svd %.2f ms "
                    "(%d Jacobi sweeps, warm %d)\n", sweep_index, b, right ? "R" : "L", chl, chr,
                    lz_ms, svd_ms, svd_sweeps, warm ? 1 : 0);

@@ -23,6 +23,7 @@
 // so the host never waits inside the iteration.
 #include <cooperative_groups.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -863,6 +864,20 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
                         int n_true, SvdSide side, int batch, long bstride, double* sigma_out,
                         bool want_vectors, const double* v_init) {
   if (v_init && (batch != 1 || !want_vectors)) fail(ACHI_E_INTERNAL, "svd: warm start needs batch 1 with vectors");
+  // ACHI_SVD_TRACE (study): synchronise after each stage and print the stage
+  // times of calls slower than 4 ms
+  static const bool trace = std::getenv("ACHI_SVD_TRACE") != nullptr;
+  using tclk = std::chrono::steady_clock;
+  std::vector<std::pair<const char*, double>> marks;
+  auto t_prev = tclk::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    ctx.sync();
+    const auto t = tclk::now();
+    marks.emplace_back(what, std::chrono::duration<double, std::milli>(t - t_prev).count());
+    t_prev = t;
+  };
+  mark("entry");
   const bool rows = side == SvdSide::kRows;
   const int ng_real = rows ? m : n;
   const int mg = rows ? n : m;
@@ -876,6 +891,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   int* perm = ws.perm.reserve(static_cast<size_t>(ng) * batch);
   unsigned long long* conv = ws.conv.reserve(MAX_SWEEPS * 8);
   double* zero2 = ws.zero2.reserve(2 * static_cast<size_t>(batch));
+  mark("reserve");
   const int nsw = std::max(64, batch);
   int* sweeps_dev = ws.sweeps.reserve(nsw);
   int* sweeps_host = ws.sweeps_host.reserve(nsw);
@@ -903,6 +919,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     }();
     zero_floor_kernel<<<batch, 1024, 0, ctx.stream>>>(G, gstride, gstride, mg, frel, zero2);
     ACHI_LAUNCHED(ctx);
+    mark("load+floor");
     if (v_init) {
       // G <- G v_init: col-major G (ldg x ng) is row-major G^T, so (G v)^T = v^T G^T
       // with v^T row-major = v col-major (K-major A) and G^T K x N row-major (MN-major B)
@@ -937,9 +954,14 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     double* jrec = nullptr;
     unsigned char* jflag = nullptr;
     if (V) {
-      jrec = ws.jrec.reserve(static_cast<size_t>(batch) * jstride * npairs * JW * JW);
-      jflag = ws.jflag.reserve(static_cast<size_t>(batch) * jstride * npairs);
+      // sized once for the largest cluster problem (40 MB): growing it with
+      // chi went through the pool's slow path (up to ~20-90 ms per growth)
+      const size_t cap = static_cast<size_t>(MAX_SWEEPS) * (2 * CL_MAXP - 1) * CL_MAXP;
+      const size_t need = static_cast<size_t>(batch) * jstride * npairs;
+      jrec = ws.jrec.reserve(std::max(need, cap) * JW * JW);
+      jflag = ws.jflag.reserve(std::max(need, cap));
     }
+    mark("jrec reserve");
     ClArgs a{G, ldg, gstride, mg, rows_pad, nb, npairs, max_inner, tol, stop_tol, zero2,
              jrec, jflag, jstride, sweeps_dev, nullptr};
     static const bool prof_on = std::getenv("ACHI_JACOBI_PROF") != nullptr;
@@ -962,6 +984,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     lc.numAttrs = 1;
     ACHI_CUDA(cudaLaunchKernelEx(&lc, jacobi_cluster_kernel, a));
     ACHI_LAUNCHED(ctx);
+    mark("cluster");
     if (prof_on) {
       long long h[8];
       ACHI_CUDA(cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
@@ -985,6 +1008,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
       v_replay_kernel<<<grid, JT, rs, ctx.stream>>>(V, vstride, ng, nb, npairs, jrec, jflag, jstride,
                                                     sweeps_dev, v_init);
       ACHI_LAUNCHED(ctx);
+      mark("replay");
     }
   } else {
     const size_t smem = stream_smem();
@@ -1028,6 +1052,16 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   }
   ACHI_CUDA(cudaMemcpyAsync(sweeps_host, sweeps_dev, sizeof(int) * launches, cudaMemcpyDeviceToHost,
                             ctx.stream));
+  mark("norms+sort");
+  if (trace) {
+    double tot = 0;
+    for (auto& [w, ms] : marks) tot += ms;
+    if (tot > 4.0) {
+      std::fprintf(stderr, "[svd-trace] %dx%d ng=%d total %.2f ms:", m, n, ng, tot);
+      for (auto& [w, ms] : marks) std::fprintf(stderr, " %s %.2f", w, ms);
+      std::fprintf(stderr, "\n");
+    }
+  }
   const int r_true = std::min(m_true, n_true);
   if (sigma_out) {
     ACHI_CUDA(cudaMemcpy2DAsync(sigma_out, sizeof(double) * r_true, sorted, sizeof(double) * ng,
