@@ -457,7 +457,13 @@ int achi_svd_device(achi_ctx* ctx, int m, int n, const double* d_a, double* d_si
     Ctx& c = ctx->c;
     if (m < 1 || n < 1) fail(ACHI_E_INVALID_MATRIX, "svd: matrix must be at least 1x1");
     static thread_local SvdWs ws;
-    SvdResultDev r = svd_device(c, ws, d_a, m, n, m, n, m <= n ? SvdSide::kRows : SvdSide::kCols);
+    static const int side_env = [] {  // study knob: force the orthogonalised side (rows|cols)
+      const char* e = std::getenv("ACHI_SVD_SIDE");
+      return e ? (e[0] == 'r' ? 0 : 1) : -1;
+    }();
+    const SvdSide side = side_env < 0 ? (m <= n ? SvdSide::kRows : SvdSide::kCols)
+                                      : (side_env == 0 ? SvdSide::kRows : SvdSide::kCols);
+    SvdResultDev r = svd_device(c, ws, d_a, m, n, m, n, side);
     const int k = r.r_true;
     svd_phase_signs(c, ws, r, k);
     svd_gather(c, ws, r, k, d_u, d_vt);

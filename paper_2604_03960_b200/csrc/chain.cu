@@ -375,6 +375,11 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   VKeep& vk = vkeep[2 * static_cast<size_t>(b) + (right ? 1 : 0)];
   const bool warm = warm_svd && vk.valid && vk.m == sm_ && vk.n == sn_ && vk.mt == smt && vk.nt == snt;
   static const char* dump_path = std::getenv("ACHI_SVD_DUMP");  // debug: input of a failing SVD
+  static const int dump_at = [] {  // study: ACHI_SVD_DUMP_AT=sweep*100000+bond*2+right dumps that visit
+    const char* e = std::getenv("ACHI_SVD_DUMP_AT");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool dump_now = dump_path && dump_at == sweep_index * 100000 + 2 * b + (right ? 1 : 0);
   std::vector<double> dump;
   if (dump_path) {
     dump.resize(static_cast<size_t>(sm_) * sn_);
@@ -396,19 +401,22 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   c.acc.end(c.stream, 0.0);
   c.sync();
   c.acc.resolve();
+  auto write_dump = [&] {
+    if (FILE* f = std::fopen(dump_path, "wb")) {
+      const int32_t hdr[6] = {sm_, sn_, smt, snt, right ? 1 : 0, warm ? 1 : 0};
+      std::fwrite(hdr, sizeof(hdr), 1, f);
+      std::fwrite(dump.data(), sizeof(double), dump.size(), f);
+      std::fclose(f);
+    }
+  };
   int svd_sweeps = 0;
   try {
     svd_sweeps = sr.sweeps();
   } catch (const Error&) {
-    if (dump_path)
-      if (FILE* f = std::fopen(dump_path, "wb")) {
-        const int32_t hdr[6] = {sm_, sn_, smt, snt, right ? 1 : 0, warm ? 1 : 0};
-        std::fwrite(hdr, sizeof(hdr), 1, f);
-        std::fwrite(dump.data(), sizeof(double), dump.size(), f);
-        std::fclose(f);
-      }
+    if (dump_path) write_dump();
     throw;
   }
+  if (dump_now) write_dump();
   // algorithmic FP64 flops of the blocked Jacobi: per sweep
   // C(ng/16, 2) block pairs x 2 * 32^2 * (2 mg + ng) (Gram + rotation of G,
   // rotation of V) ~= 4 ng^2 (2 mg + ng)

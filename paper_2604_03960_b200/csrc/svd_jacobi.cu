@@ -866,7 +866,9 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   if (v_init && (batch != 1 || !want_vectors)) fail(ACHI_E_INTERNAL, "svd: warm start needs batch 1 with vectors");
   // ACHI_SVD_TRACE (study): synchronise after each stage and print the stage
   // times of calls slower than 4 ms
-  static const bool trace = std::getenv("ACHI_SVD_TRACE") != nullptr;
+  static const char* trace_env = std::getenv("ACHI_SVD_TRACE");  // value: print threshold in ms
+  static const bool trace = trace_env != nullptr;
+  static const double trace_ms = trace_env ? std::atof(trace_env) : 0.0;
   using tclk = std::chrono::steady_clock;
   std::vector<std::pair<const char*, double>> marks;
   auto t_prev = tclk::now();
@@ -898,6 +900,19 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   const int nb = ng / JB;  // even (ng multiple of 32)
   const int npairs = nb / 2;
   const bool cluster = ldg <= CL_ROWS && npairs <= CL_MAXP;
+  // pad columns: rows side -> columns >= m_true (theta rows (l,s1), padded l last);
+  // cols side with padding -> columns (s2, jr) with jr >= chr_true (d = 2 on the padded path)
+  int pad_mod = ng, pad_lim = rows ? m_true : n_true;
+  if (!rows && n != n_true) {
+    pad_mod = n / 2;
+    pad_lim = n_true / 2;
+  }
+  const int nr_real = (ng_real / pad_mod) * pad_lim + std::min(ng_real % pad_mod, pad_lim);
+  static const int precond_min = [] {  // ACHI_SVD_PRECOND_MIN: smallest width preconditioned (0: off)
+    const char* e = std::getenv("ACHI_SVD_PRECOND_MIN");
+    const int v = e ? std::atoi(e) : 64;
+    return v <= 0 ? (1 << 30) : v;
+  }();
   {
     dim3 grid(cdiv(ng, 32), cdiv(ldg, 32), batch), blk(32, 8);
     load_g_kernel<<<grid, blk, 0, ctx.stream>>>(theta, bstride, m, n, G, gstride, ldg, mg, ng,
@@ -927,6 +942,15 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
       gemm(ctx, ng, static_cast<int>(ldg), ng, Operand{v_init, ng, Major::kK},
            Operand{G, ldg, Major::kMN}, Gw, ldg);
       G = Gw;
+    } else if (cluster && V && batch == 1 && ng_real >= precond_min && qr_precond_applicable(mg, nr_real)) {
+      // cold start: QR preconditioning (svd_precond.cu), G <- G Q, V starts from Q
+      double* vq = ws.Vq.reserve(static_cast<size_t>(vstride));
+      dim3 g2(static_cast<unsigned>(std::min<long>(cdiv(vstride, 256), 4L * ctx.num_sms)), 1);
+      identity_kernel<<<g2, 256, 0, ctx.stream>>>(vq, ng, ng, vstride);
+      ACHI_LAUNCHED(ctx);
+      qr_precond(ctx, G, ldg, mg, ng, nr_real, pad_mod, pad_lim, vq);
+      v_init = vq;
+      mark("precond");
     }
   }
   const double tol = std::max(1e-15, 2.0 * std::sqrt(static_cast<double>(mg)) * EPS);
@@ -1035,13 +1059,6 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     }
     launches = std::min(launches, nsw);
   }
-  // pad columns: rows side -> columns >= m_true (theta rows (l,s1), padded l last);
-  // cols side with padding -> columns (s2, jr) with jr >= chr_true (d = 2 on the padded path)
-  int pad_mod = ng, pad_lim = rows ? m_true : n_true;
-  if (!rows && n != n_true) {
-    pad_mod = n / 2;
-    pad_lim = n_true / 2;
-  }
   {
     dim3 grid(cdiv(ng, 8), batch);
     col_norm_kernel<<<grid, 256, 0, ctx.stream>>>(G, gstride, ldg, ng, ng_real, pad_mod, pad_lim,
@@ -1056,7 +1073,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   if (trace) {
     double tot = 0;
     for (auto& [w, ms] : marks) tot += ms;
-    if (tot > 4.0) {
+    if (tot >= trace_ms) {
       std::fprintf(stderr, "[svd-trace] %dx%d ng=%d total %.2f ms:", m, n, ng, tot);
       for (auto& [w, ms] : marks) std::fprintf(stderr, " %s %.2f", w, ms);
       std::fprintf(stderr, "\n");

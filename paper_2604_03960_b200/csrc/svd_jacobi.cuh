@@ -16,6 +16,7 @@ namespace achi {
 
 struct SvdWs {
   DevBuf G, Gw, V, sig, sorted, zero2;  // Gw: G * v_init (warm start)
+  DevBuf Vq;                    // QR preconditioner factor (cold cluster-path SVDs)
   DevBuf jrec;                  // cluster mode: recorded block rotations (V replay)
   DevArr<unsigned char> jflag;
   DevArr<int> perm;
@@ -61,6 +62,12 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
                         int n_true, SvdSide side, int batch = 1, long bstride = 0,
                         double* sigma_out = nullptr, bool want_vectors = true,
                         const double* v_init = nullptr);
+
+// QR preconditioner (svd_precond.cu): G <- G Q in place and V0 <- Q (ng x ng,
+// col-major, identity on entry) with G^T Pi = Q R over the real coordinates.
+bool qr_precond_applicable(int mr, int nr);
+void qr_precond(Ctx& ctx, double* G, long ldg, int mr, int ng, int nr, int pad_mod, int pad_lim,
+                double* V0);
 
 // working-matrix width (columns of G and order of V) for a theta of m x n
 inline int svd_working_cols(int m, int n, SvdSide side) {
