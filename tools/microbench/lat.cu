@@ -76,6 +76,33 @@ __global__ void k_lds(double* out, long long* cyc, double a) {
   out[threadIdx.x] = x;
   if (threadIdx.x == 0) *cyc = t1 - t0;
 }
+__global__ void k_dsqrt(double* out, long long* cyc, double a) {
+  double x = a + 1.0;
+  long long t0 = clock64();
+#pragma unroll 8
+  for (int i = 0; i < N; ++i) x = sqrt(x) + 1.0;
+  long long t1 = clock64();
+  out[threadIdx.x] = x;
+  if (threadIdx.x == 0) *cyc = t1 - t0;
+}
+__global__ void k_ddiv(double* out, long long* cyc, double a) {
+  double x = a + 1.0;
+  long long t0 = clock64();
+#pragma unroll 8
+  for (int i = 0; i < N; ++i) x = 1.0 / x + 1.0;
+  long long t1 = clock64();
+  out[threadIdx.x] = x;
+  if (threadIdx.x == 0) *cyc = t1 - t0;
+}
+__global__ void k_shfl(double* out, long long* cyc, double a) {
+  double x = a + threadIdx.x;
+  long long t0 = clock64();
+#pragma unroll 8
+  for (int i = 0; i < N; ++i) x += __shfl_xor_sync(0xffffffffu, x, 1 + (i & 15));
+  long long t1 = clock64();
+  out[threadIdx.x] = x;
+  if (threadIdx.x == 0) *cyc = t1 - t0;
+}
 __global__ void k_bar(double* out, long long* cyc, double a) {
   long long t0 = clock64();
   for (int i = 0; i < N; ++i) __syncthreads();
@@ -94,7 +121,8 @@ int main() {
   struct { const char* name; K k; int threads; double per; } ks[] = {
       {"DFMA", k_dfma, 32, N},        {"DADD", k_dadd, 32, N},     {"FFMA", k_ffma, 32, N},
       {"MUFU.RCP64H", k_rcp64, 32, N}, {"MUFU.RCP", k_rcp32, 32, N}, {"F2F d->f->d (pair)", k_f2f, 32, N / 2},
-      {"LDS.32 chain", k_lds, 32, N},  {"BAR.SYNC 256 thr", k_bar, 256, N}, {"BAR.SYNC 32 thr", k_bar, 32, N}};
+      {"LDS.32 chain", k_lds, 32, N}, {"DSQRT+DADD", k_dsqrt, 32, N}, {"DDIV+DADD", k_ddiv, 32, N},
+      {"SHFL.f64+DADD", k_shfl, 32, N},  {"BAR.SYNC 256 thr", k_bar, 256, N}, {"BAR.SYNC 32 thr", k_bar, 32, N}};
   for (auto& k : ks) {
     long long best = 1LL << 60;
     for (int rep = 0; rep < 5; ++rep) {
