@@ -20,7 +20,7 @@ ACHI_LANCZOS_GRAPH=0 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-c
 echo "list rc=$?" >> $O/status.txt
 python tools/ncu_summary.py $O/launches.csv > $O/launches_summary.txt 2>&1
 # full captures of the dominant kernels in the steady state of C3 (sweeps 5-6)
-for K in jacobi_cluster_kernel:1000 v_replay_kernel:1000 lanczos_orth_kernel:14000 \
+for K in jacobi_cluster_kernel:1000 v_replay_kernel:1000 qr_precond_kernel:100 lanczos_orth_kernel:14000 \
          heff_small_kernel:14000; do
   name=${K%%:*}; skip=${K##*:}
   ACHI_LANCZOS_GRAPH=0 timeout 900 ncu --set full --import-source on --clock-control none \
