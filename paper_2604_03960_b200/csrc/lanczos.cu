@@ -816,14 +816,19 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
     ws.graphs.resize(static_cast<size_t>(graph_slot) + 1);
   LanczosGraph& lg = graph_slot >= 0 ? ws.graphs[static_cast<size_t>(graph_slot)] : local;
   const uint64_t key = graph_key ^ (static_cast<uint64_t>(n) << 40) ^ static_cast<uint64_t>(orth_grid);
-  static thread_local long builds = 0;
+  static thread_local long builds = 0, updates = 0;
   static thread_local double build_s = 0.0;
   if (prof_on && prof_calls % 200 == 0)
-    std::fprintf(stderr, "[lanczos] graph builds %ld, %.3f ms each\n", builds,
-                 builds ? 1e3 * build_s / builds : 0.0);
+    std::fprintf(stderr, "[lanczos] graph builds %ld (%ld by exec update), %.3f ms each\n", builds,
+                 updates, builds ? 1e3 * build_s / builds : 0.0);
   if (use_graph && (!lg.exec || lg.key != key)) {
     const auto tb = std::chrono::steady_clock::now();
     ++builds;
+    // keep the executable graph: a graph of the same topology (another shape
+    // of this bond) is applied to it by cudaGraphExecUpdate, much cheaper than
+    // a new instantiation; anything else re-instantiates
+    cudaGraphExec_t old_exec = lg.exec;
+    lg.exec = nullptr;
     lg.reset();
     ACHI_CUDA(cudaGraphCreate(&lg.graph, 0));
     cudaGraphConditionalHandle handle;
@@ -853,13 +858,32 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
       cudaGraph_t dummy;
       cudaStreamEndCapture(ctx.stream, &dummy);
       lg.reset();
+      if (old_exec) cudaGraphExecDestroy(old_exec);
       throw;
     }
     cudaGraph_t captured;
     ACHI_CUDA(cudaStreamEndCapture(ctx.stream, &captured));
     lg.body_launches = ctx.launches - l0;
     ctx.launches = l0;  // counted per executed iteration below
-    ACHI_CUDA(cudaGraphInstantiate(&lg.exec, lg.graph, 0));
+    static const bool exec_update = [] {
+      const char* e = std::getenv("ACHI_GRAPH_UPDATE");
+      return !(e && e[0] == '0');
+    }();
+    bool updated = false;
+    if (old_exec && exec_update) {
+      cudaGraphExecUpdateResultInfo info;
+      if (cudaGraphExecUpdate(old_exec, lg.graph, &info) == cudaSuccess) {
+        lg.exec = old_exec;
+        updated = true;
+        ++updates;
+      } else {
+        cudaGetLastError();  // clear the failed update
+      }
+    }
+    if (!updated) {
+      if (old_exec) cudaGraphExecDestroy(old_exec);
+      ACHI_CUDA(cudaGraphInstantiate(&lg.exec, lg.graph, 0));
+    }
     lg.key = key;
     build_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - tb).count();
   }
