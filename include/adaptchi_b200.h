@@ -204,6 +204,17 @@ int achi_chain_set_states(achi_chain* chain, const achi_bond_state* in);
  * The state must be right-canonical with centre 0. */
 int achi_chain_load_state(achi_chain* chain, const int32_t* bond_dims,
                           const double* const* sites);
+/* Same, for any state: canonicalize != 0 first brings it to right-canonical
+ * form with centre 0 (canonicalize(psi, 0), mps.cpp:172-210: Householder QR of
+ * each site, host side, bond dimensions may shrink to min(chi, d * right)).
+ * Replaces load_mps + canonicalize + Environment::rebuild for a resumed run. */
+int achi_chain_load_mps(achi_chain* chain, const int32_t* bond_dims, const double* const* sites,
+                        int canonicalize);
+/* expectation_energy (dmrg.cpp:284-298) of the chain's current state on the
+ * device: left environments rebuilt from the boundary through every site
+ * (independent of the cached environments); <psi|H|psi> (psi is normalised
+ * after every visit). */
+int achi_chain_energy(achi_chain* chain, double* energy);
 
 /* Phase accounting since chain creation (host wall clock at sync points):
  * out[0..7] = {lanczos+merge s, svd s, bond-select s, absorb+env s, matvecs,

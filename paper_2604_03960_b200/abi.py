@@ -161,6 +161,8 @@ def load():
         "achi_chain_get_states": (C.c_int, [vp, P(BondState)]),
         "achi_chain_set_states": (C.c_int, [vp, P(BondState)]),
         "achi_chain_load_state": (C.c_int, [vp, P(i32), P(dp)]),
+        "achi_chain_load_mps": (C.c_int, [vp, P(i32), P(dp), C.c_int]),
+        "achi_chain_energy": (C.c_int, [vp, dp]),
         "achi_heff_apply": (C.c_int, [vp] + [C.c_int] * 6 + [dp] * 6),
         "achi_env_update_left": (C.c_int, [vp] + [C.c_int] * 5 + [dp] * 4),
         "achi_env_update_right": (C.c_int, [vp] + [C.c_int] * 5 + [dp] * 4),

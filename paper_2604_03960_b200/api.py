@@ -300,11 +300,23 @@ class Chain:
         self.ctx._check(self.ctx.lib.achi_chain_get_states(self.h, arr))
         return list(arr)
 
-    def load_state(self, sites):
+    def load_state(self, sites, canonicalize=False):
+        """Load site tensors (l, d, r) and rebuild environments at centre 0;
+        canonicalize=True first applies canonicalize(psi, 0) (mps.cpp:172-210)."""
         dims = np.array([s.shape[2] for s in sites[:-1]], np.int32)
         flat = [np.ascontiguousarray(s, dtype=np.float64) for s in sites]
         ptrs = (C.POINTER(C.c_double) * len(flat))(*[_dp(a) for a in flat])
-        self.ctx._check(self.ctx.lib.achi_chain_load_state(self.h, _ip(dims), ptrs))
+        self.ctx._check(self.ctx.lib.achi_chain_load_mps(self.h, _ip(dims), ptrs, int(canonicalize)))
+
+    def sites(self):
+        """The MPS as a list of host (l, d, r) arrays (MatrixProductState::sites)."""
+        return [self.site(k) for k in range(self.n)]
+
+    def energy(self):
+        """expectation_energy (dmrg.cpp:284-298) of the current state, on the device."""
+        e = C.c_double()
+        self.ctx._check(self.ctx.lib.achi_chain_energy(self.h, C.byref(e)))
+        return e.value
 
 
 def heff_bench(ctx: Context, chi: int, reps: int = 20):

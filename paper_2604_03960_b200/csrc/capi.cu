@@ -1,4 +1,5 @@
 // extern "C" boundary (include/adaptchi_b200.h): typed errors -> int codes.
+#include <cmath>
 #include <cstring>
 #include <memory>
 
@@ -317,23 +318,42 @@ int achi_chain_set_states(achi_chain* chain, const achi_bond_state* in) {
   });
 }
 
-int achi_chain_load_state(achi_chain* chain, const int32_t* bond_dims, const double* const* sites) {
+int achi_chain_load_mps(achi_chain* chain, const int32_t* bond_dims, const double* const* sites,
+                        int canonicalize) {
   Chain& ch = chain->ch;
   achi_ctx* ctx = ch.owner;
   return guard(ctx, [&] {
+    std::vector<int> dims(ch.n + 1, 1);
     for (int k = 1; k < ch.n; ++k) {
-      if (bond_dims[k - 1] < 1 || bond_dims[k - 1] > ch.cap[k])
-        fail(ACHI_E_INVALID_RANK, "load_state: bond dimension exceeds capacity");
-      ch.chi[k] = bond_dims[k - 1];
+      if (bond_dims[k - 1] < 1) fail(ACHI_E_INVALID_RANK, "load_mps: bond dimension must be >= 1");
+      dims[k] = bond_dims[k - 1];
     }
     std::vector<std::vector<double>> hs(ch.n);
     for (int k = 0; k < ch.n; ++k) {
-      const size_t sz = static_cast<size_t>(ch.chi[k]) * ch.d * ch.chi[k + 1];
+      const size_t sz = static_cast<size_t>(dims[k]) * ch.d * dims[k + 1];
       hs[k].assign(sites[k], sites[k] + sz);
+      for (double x : hs[k])
+        if (!std::isfinite(x)) fail(ACHI_E_INVALID_MATRIX, "load_mps: non-finite site entry");
     }
+    if (canonicalize) canonicalize_left(hs, dims, ch.d);  // canonicalize(psi, 0), mps.cpp:204-210
+    for (int k = 1; k < ch.n; ++k)
+      if (dims[k] > ch.cap[k]) fail(ACHI_E_INVALID_RANK, "load_mps: bond dimension exceeds capacity");
+    for (int k = 1; k < ch.n; ++k) ch.chi[k] = dims[k];
     ch.upload_sites(hs);
     ch.rebuild_envs();
     ch.ctx->sync();
+  });
+}
+
+int achi_chain_load_state(achi_chain* chain, const int32_t* bond_dims, const double* const* sites) {
+  return achi_chain_load_mps(chain, bond_dims, sites, 0);
+}
+
+int achi_chain_energy(achi_chain* chain, double* energy) {
+  Chain& ch = chain->ch;
+  return guard(ch.owner, [&] {
+    if (!energy) fail(ACHI_E_INVALID_CONFIG, "chain_energy: null output");
+    *energy = ch.expectation_energy();
   });
 }
 

@@ -126,10 +126,12 @@ std::vector<int> capped_bond_dims(int n, int d, int chi) {
   return dims;
 }
 
-// Thin Householder QR of a column-major m x k matrix (m >= k), reflector
-// signs as LAPACK dlarfg (beta = -sign(alpha) * ||x||): a -> Q (m x k),
-// r -> R (k x k, upper).  Setup-sized (chi_min columns), host side.
-void householder_qr(std::vector<double>& a, int m, int k, std::vector<double>& r) {
+// Thin Householder QR of a column-major m x ncol matrix, k = min(m, ncol)
+// reflectors with LAPACK dlarfg signs (beta = -sign(alpha) * ||x||):
+// a -> Q (m x k, column-major), r -> R (k x ncol, column-major, upper
+// trapezoidal).  Setup-sized (host side).
+int householder_qr(std::vector<double>& a, int m, int ncol, std::vector<double>& r) {
+  const int k = std::min(m, ncol);
   std::vector<double> v(static_cast<size_t>(m) * k, 0.0), tau(k, 0.0);
   auto A = [&](int i, int j) -> double& { return a[static_cast<size_t>(j) * m + i]; };
   for (int j = 0; j < k; ++j) {
@@ -147,7 +149,7 @@ void householder_qr(std::vector<double>& a, int m, int k, std::vector<double>& r
       for (int i = j + 1; i < m; ++i) vj[i] = A(i, j) / (alpha - beta);
       A(j, j) = beta;
       for (int i = j + 1; i < m; ++i) A(i, j) = 0.0;
-      for (int c = j + 1; c < k; ++c) {  // apply H_j to the trailing columns
+      for (int c = j + 1; c < ncol; ++c) {  // apply H_j to the trailing columns
         double s = 0;
         for (int i = j; i < m; ++i) s += vj[i] * A(i, c);
         s *= tau[j];
@@ -155,49 +157,55 @@ void householder_qr(std::vector<double>& a, int m, int k, std::vector<double>& r
       }
     }
   }
-  r.assign(static_cast<size_t>(k) * k, 0.0);
-  for (int j = 0; j < k; ++j)
-    for (int i = 0; i <= j; ++i) r[static_cast<size_t>(j) * k + i] = A(i, j);
+  r.assign(static_cast<size_t>(k) * ncol, 0.0);
+  for (int j = 0; j < ncol; ++j)
+    for (int i = 0; i <= std::min(j, k - 1); ++i) r[static_cast<size_t>(j) * k + i] = A(i, j);
   // Q = H_0 ... H_{k-1} [I_k; 0]
-  std::fill(a.begin(), a.end(), 0.0);
-  for (int j = 0; j < k; ++j) A(j, j) = 1.0;
+  std::vector<double> q(static_cast<size_t>(m) * k, 0.0);
+  auto Q = [&](int i, int j) -> double& { return q[static_cast<size_t>(j) * m + i]; };
+  for (int j = 0; j < k; ++j) Q(j, j) = 1.0;
   for (int j = k - 1; j >= 0; --j) {
     const double* vj = &v[static_cast<size_t>(j) * m];
     for (int c = 0; c < k; ++c) {
       double s = 0;
-      for (int i = j; i < m; ++i) s += vj[i] * A(i, c);
+      for (int i = j; i < m; ++i) s += vj[i] * Q(i, c);
       s *= tau[j];
-      for (int i = j; i < m; ++i) A(i, c) -= s * vj[i];
+      for (int i = j; i < m; ++i) Q(i, c) -= s * vj[i];
     }
   }
+  a.swap(q);
+  return k;
 }
 
-// canonicalize(psi, 0) (mps.cpp:172-210) for right moves only: push_left on
-// sites n-1..1.  Site k is (dims[k], d, dims[k+1]) row-major; push_left may
+}  // namespace
+
+// canonicalize(psi, 0) (mps.cpp:172-210): push_left on sites n-1..1 (right
+// moves only).  Site k is (dims[k], d, dims[k+1]) row-major; push_left may
 // shrink dims[k] to min(d * dims[k+1], dims[k]).
 void canonicalize_left(std::vector<std::vector<double>>& s, std::vector<int>& dims, int d) {
   const int n = static_cast<int>(s.size());
   for (int i = n - 1; i >= 1; --i) {
-    const int l = dims[i], r = dims[i + 1], m = d * r, k = std::min(m, l);
+    const int l = dims[i], r = dims[i + 1], m = d * r;
     // M^T with M = site as l x (d r): column-major (m x l) buffer == site row-major
     std::vector<double> a(s[i].begin(), s[i].end()), rr;
-    if (k < l) fail(ACHI_E_INVALID_RANK, "canonicalize: bond wider than d * right bond");
-    householder_qr(a, m, k, rr);
-    // site i <- Q^T (k x m) row-major == Q column-major (m x k)
-    s[i] = a;
-    // site i-1 (ll*d x l) <- site i-1 * R^T
+    const int k = householder_qr(a, m, l, rr);  // a: Q (m x k), rr: R (k x l)
+    s[i] = a;  // site i <- Q^T (k x m) row-major == Q column-major
+    // site i-1 (ll*d x l) <- site i-1 * R^T (l x k)
     const int ll = dims[i - 1];
     std::vector<double> nb(static_cast<size_t>(ll) * d * k, 0.0);
     for (int row = 0; row < ll * d; ++row)
       for (int c = 0; c < k; ++c) {
         double acc = 0;  // (R^T)(t, c) = R(c, t), nonzero for t >= c
-        for (int t = c; t < l; ++t) acc += s[i - 1][static_cast<size_t>(row) * l + t] * rr[static_cast<size_t>(t) * k + c];
+        for (int t = c; t < l; ++t)
+          acc += s[i - 1][static_cast<size_t>(row) * l + t] * rr[static_cast<size_t>(t) * k + c];
         nb[static_cast<size_t>(row) * k + c] = acc;
       }
     s[i - 1] = nb;
     dims[i] = k;
   }
 }
+
+namespace {
 
 // random_mps (mps.cpp:75-95) with one real normal draw per entry, then the
 // second canonicalize of run_dmrg (dmrg.cpp:236).
@@ -333,6 +341,37 @@ void Chain::upload_sites(const std::vector<std::vector<double>>& hs) {
     upload_padded3(*ctx, hs[k].data(), l, d, r, site[k].p);
   }
   ctx->sync();
+}
+
+// expectation_energy (dmrg.cpp:284-298): left environments from the boundary
+// through every site into two scratch buffers; L_n (1 x 1 x 1, stored padded)
+// is <psi|H|psi>.  Independent of the cached environments.
+double Chain::expectation_energy() {
+  Ctx& c = *ctx;
+  size_t mx = 1;
+  for (int k = 0; k <= n; ++k) {
+    const size_t cp = pad2i(chi[k]);
+    const int D = k < n ? mpo[k].l : 1;
+    mx = std::max(mx, cp * cp * static_cast<size_t>(D));
+  }
+  DevBuf e[2];
+  for (auto& b : e) {
+    b.reserve(mx);
+    ACHI_CUDA(cudaMemsetAsync(b.p, 0, sizeof(double) * mx, c.stream));
+  }
+  set_boundary_kernel<<<1, 1, 0, c.stream>>>(e[0].p);
+  ACHI_LAUNCHED(c);
+  int cur = 0;
+  for (int k = 0; k < n; ++k) {
+    ACHI_CUDA(cudaMemsetAsync(e[cur ^ 1].p, 0, sizeof(double) * mx, c.stream));
+    env_left(c, e[cur].p, site[k].p, pad2i(chi[k]), pad2i(chi[k + 1]), d, mpo[k].l, mpo[k].r,
+             mleft[k], e[cur ^ 1].p);
+    cur ^= 1;
+  }
+  double h = 0.0;
+  ACHI_CUDA(cudaMemcpyAsync(&h, e[cur].p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  return h;
 }
 
 void Chain::rebuild_envs() {  // Environment::rebuild(psi, mpo, 0), dmrg.cpp:51-56

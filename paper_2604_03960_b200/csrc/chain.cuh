@@ -27,6 +27,9 @@ struct VisitHost {
   int matvecs;
 };
 
+// canonicalize(psi, 0) on host site tensors (setup sized; mps.cpp:172-210)
+void canonicalize_left(std::vector<std::vector<double>>& sites, std::vector<int>& dims, int d);
+
 struct Chain {
   Ctx* ctx = nullptr;
   achi_ctx* owner = nullptr;
@@ -70,6 +73,7 @@ struct Chain {
 
   void create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g);
   void rebuild_envs();
+  double expectation_energy();
   void upload_sites(const std::vector<std::vector<double>>& host_sites);
   void visit(int bond, bool moving_right, int sweep, int slot);
   void sweep(int sweep_index, achi_sweep_record* rec, int32_t* chi_profile, double* entropy,

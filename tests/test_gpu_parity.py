@@ -476,3 +476,49 @@ def test_acceptance_criteria6_7(ctx, family):  # acceptance_main.cpp:206-273
         cfg.controller.beta_predict = beta
         r = ctx.run_dmrg(spec, cfg)
         assert abs(r["energy"] - r0["energy"]) <= 1e-8 and r["n_sweeps"] == r0["n_sweeps"]
+
+
+# ---------------- device setup / outputs ----------------
+
+def _run_chain(ctx, spec, cfg):
+    from paper_2604_03960_b200.api import Chain
+    ch = Chain(ctx, spec, cfg)
+    rec = None
+    for s in range(cfg.max_sweeps):
+        rec = ch.sweep(s)
+    return ch, rec
+
+
+def test_expectation_energy_and_snapshot_reload(ctx, oracle, tmp_path):
+    """expectation_energy (dmrg.cpp:284-298) on the device equals the last
+    eigenvalue when nothing is truncated (N=10, chi=32 = 2^5); a saved ACHI
+    snapshot reloaded into a fresh chain, and the same state in a random
+    non-canonical gauge reloaded with canonicalize, give the same energy."""
+    from paper_2604_03960_b200 import outputs
+    from paper_2604_03960_b200.api import Chain
+    spec = abi.model_spec(10)
+    cfg = abi.fixed_config(32, max_sweeps=3, eps_conv=1e-16)
+    ch, rec = _run_chain(ctx, spec, cfg)
+    e_last = rec["energy"]
+    e_state = ch.energy()
+    assert abs(e_state - e_last) <= 1e-10 * abs(e_last)
+    assert abs(e_state - oracle.exact_ground_energy(spec)) <= 1e-8
+    sites = ch.sites()
+    p = tmp_path / "psi.achi"
+    outputs.save_mps(sites, p)
+    fresh = Chain(ctx, spec, cfg)
+    fresh.load_state(outputs.load_mps(p))
+    assert abs(fresh.energy() - e_state) <= 1e-12 * abs(e_state)
+    # random gauge on every bond: A_k G_k, G_k^-1 A_k+1 (same state, not canonical)
+    rng = np.random.default_rng(7)
+    g = [s.copy() for s in sites]
+    for k in range(len(g) - 1):
+        chi = g[k].shape[2]
+        G = np.eye(chi) + 0.3 * rng.standard_normal((chi, chi))
+        g[k] = np.einsum("lsr,rq->lsq", g[k], G)
+        g[k + 1] = np.einsum("qr,rsx->qsx", np.linalg.inv(G), g[k + 1])
+    other = Chain(ctx, spec, cfg)
+    other.load_state(g, canonicalize=True)
+    assert abs(other.energy() - e_state) <= 1e-10 * abs(e_state)
+    r2 = other.sweep(3)
+    assert abs(r2["energy"] - e_last) <= 1e-10 * abs(e_last)
