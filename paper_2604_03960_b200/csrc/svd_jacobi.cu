@@ -245,7 +245,7 @@ __device__ void init_pair_tables(Small& sm) {
 // while a column a few orders above the noise floor (whose direction is only
 // defined to ~noise/|x|) no longer holds the stop test open forever.
 __device__ bool finish_gram(Small& sm, const double (&acc)[4], double z2, double ig2, double tol,
-                            int max_inner, bool cross = false) {
+                            int max_inner, bool cross = false, double skip_tol = 0.0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3, mt = warp >> 2, nt = warp & 3;
   {
@@ -292,7 +292,7 @@ __device__ bool finish_gram(Small& sm, const double (&acc)[4], double z2, double
     sm.red2[0] = sqrt(sqrt(w));
   }
   __syncthreads();
-  const bool rotate = sm.red[0] > tol;
+  const bool rotate = sm.red[0] > fmax(tol, skip_tol);
   if (rotate) inner_jacobi(sm, z2, tol, max_inner, cross);
   return rotate;
 }
@@ -307,6 +307,7 @@ struct ClArgs {
   double tol, stop_tol;
   const double* zero2;
   int cross_mode;          // inner schedule per round (see svd_device)
+  double skip_tol;         // block pairs whose cosines are all below this are not rotated
   double* jrec;            // [batch][MAX_SWEEPS*(nb-1)][npairs][32][32] or null
   unsigned char* jflag;    // [batch][MAX_SWEEPS*(nb-1)][npairs]
   long jstride;            // rounds capacity per batch item (MAX_SWEEPS*(nb-1))
@@ -421,7 +422,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_cluster_kernel(ClArgs a) {
       const bool cross = (a.cross_mode == 1 && sweep >= 1) || (a.cross_mode == 2 && (r & 1)) ||
                          (a.cross_mode == 3 && sweep >= 1 && (r & 1)) ||
                          (a.cross_mode == 4 && (r % 3) != 0) || (a.cross_mode == 5 && r != 0);
-      const bool rot = finish_gram(sm, acc, z2, ig2, a.tol, a.max_inner, cross);
+      const bool rot = finish_gram(sm, acc, z2, ig2, a.tol, a.max_inner, cross, a.skip_tol);
       const long long t2 = prof ? clock64() : 0;
       if (threadIdx.x == 0) meas_slot[sweep % 3] = fmax(meas_slot[sweep % 3], sm.red2[0]);
       if (a.jrec) {
@@ -1009,8 +1010,12 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
       const char* e = std::getenv("ACHI_JACOBI_CROSS");
       return e ? std::atoi(e) : 4;
     }();
+    static const double skip_tol = [] {
+      const char* e = std::getenv("ACHI_JACOBI_SKIP");
+      return e ? std::atof(e) : 0.0;
+    }();
     ClArgs a{G, ldg, gstride, mg, rows_pad, nb, npairs, max_inner, tol, stop_tol, zero2, cross_mode,
-             jrec, jflag, jstride, sweeps_dev, nullptr};
+             skip_tol, jrec, jflag, jstride, sweeps_dev, nullptr};
     static const bool prof_on = std::getenv("ACHI_JACOBI_PROF") != nullptr;
     static DevArr<long long> profbuf;
     if (prof_on) {
