@@ -516,33 +516,49 @@ __global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) 
   const unsigned long long c2 = prof ? clock64() : 0;
   orth_reduce(a.pa, nv, coef);
   // pass 2: w <- w - Q h1 ; h2 partials
+  double nrm1 = 0.0;  // ||w'||^2 partial, reduced with the second dots
   for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
     double v = a.w[x];
     for (int i = 0; i < nv; ++i) v -= coef[i] * a.Q[i * a.stride + x];
     a.w[x] = v;
+    nrm1 += v * v;
   }
+  nrm1 = block_sum(nrm1, red);
+  if (threadIdx.x == 0) a.pb[static_cast<long>(nv) * gridDim.x + blockIdx.x] = nrm1;
   __syncthreads();
   orth_partials(a.Q, a.stride, nv, a.w, b0, b1, a.pb, sh);
   const double alpha_j = coef[nv - 1];
   grid.sync();
-  orth_reduce(a.pb, nv, coef);
-  // pass 3: w <- w - Q h2 ; ||w||^2 partials
+  orth_reduce(a.pb, nv + 1, coef);
+  // beta_j = ||w' - Q h2|| = sqrt(||w'||^2 - ||h2||^2) (Q orthonormal) when the
+  // second projection is small against w' (always, short of an invariant
+  // subspace); otherwise the norm is formed explicitly after one more barrier.
+  // Every block evaluates the same reduced values: the branch is grid-uniform.
+  double h2sq = 0.0;
+  for (int i = 0; i < nv; ++i) h2sq = fma(coef[i], coef[i], h2sq);
+  const double wn2 = coef[nv];
+  const bool pyth = h2sq <= 0.25 * wn2;
+  __shared__ double bn_s;
   double nrm = 0.0;
+  // pass 3: w <- w - Q h2 (and ||w||^2 partials on the explicit path)
   for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
     double v = a.w[x];
     for (int i = 0; i < nv; ++i) v -= coef[i] * a.Q[i * a.stride + x];
     a.w[x] = v;
     nrm += v * v;
   }
-  nrm = block_sum(nrm, red);
-  if (threadIdx.x == 0) a.pc[blockIdx.x] = nrm;
-  grid.sync();
-  const unsigned long long c3 = prof ? clock64() : 0;
-  __shared__ double bn_s;
-  if (threadIdx.x < 32) {
-    const double t = grid_sum(a.pc, threadIdx.x);
-    if (threadIdx.x == 0) bn_s = sqrt(t);
+  if (!pyth) {
+    nrm = block_sum(nrm, red);
+    if (threadIdx.x == 0) a.pc[blockIdx.x] = nrm;
+    grid.sync();
+    if (threadIdx.x < 32) {
+      const double t = grid_sum(a.pc, threadIdx.x);
+      if (threadIdx.x == 0) bn_s = sqrt(t);
+    }
+  } else if (threadIdx.x == 0) {
+    bn_s = sqrt(fmax(wn2 - h2sq, 0.0));
   }
+  const unsigned long long c3 = prof ? clock64() : 0;
   __syncthreads();
   const double bn = bn_s;
   // q_{j+1} = w / beta_j (unused when the step converges or breaks down)
