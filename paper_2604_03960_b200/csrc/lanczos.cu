@@ -474,6 +474,22 @@ __device__ void orth_partials(const double* Q, long stride, int nv, const double
   __syncthreads();
 }
 
+// w[x] - sum_i coef[i] Q[i][x], i ascending; the loads of 8 basis vectors are
+// issued together (the subtraction order, and so every bit, is unchanged)
+__device__ __forceinline__ double project_out(const double* Q, long stride, int nv, const double* coef,
+                                              double v, long x) {
+  int i = 0;
+  for (; i + 8 <= nv; i += 8) {
+    double q[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) q[u] = Q[(i + u) * stride + x];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v -= coef[i + u] * q[u];
+  }
+  for (; i < nv; ++i) v -= coef[i] * Q[i * stride + x];
+  return v;
+}
+
 // sum over blocks of part[v][0..grid) in a fixed order (lane-strided partial
 // sums, then a fixed shuffle tree): identical in every block
 __device__ __forceinline__ double grid_sum(const double* p, int lane) {
@@ -518,8 +534,7 @@ __global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) 
   // pass 2: w <- w - Q h1 ; h2 partials
   double nrm1 = 0.0;  // ||w'||^2 partial, reduced with the second dots
   for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
-    double v = a.w[x];
-    for (int i = 0; i < nv; ++i) v -= coef[i] * a.Q[i * a.stride + x];
+    const double v = project_out(a.Q, a.stride, nv, coef, a.w[x], x);
     a.w[x] = v;
     nrm1 += v * v;
   }
@@ -542,8 +557,7 @@ __global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) 
   double nrm = 0.0;
   // pass 3: w <- w - Q h2 (and ||w||^2 partials on the explicit path)
   for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
-    double v = a.w[x];
-    for (int i = 0; i < nv; ++i) v -= coef[i] * a.Q[i * a.stride + x];
+    const double v = project_out(a.Q, a.stride, nv, coef, a.w[x], x);
     a.w[x] = v;
     nrm += v * v;
   }
