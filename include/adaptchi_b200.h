@@ -149,6 +149,12 @@ typedef struct achi_chain achi_chain;
 
 int achi_ctx_create(int device, achi_ctx** out);
 int achi_ctx_destroy(achi_ctx* ctx);
+/* Cap the CTAs of the context's grid-wide (cooperative) kernels, 0 = none.  For
+ * several contexts sharing one GPU (chains of an ensemble in flight): each
+ * context's Lanczos orthogonalisation and fused H_eff then fit beside the
+ * others' instead of serialising.  Reduction orders follow the grid, so results
+ * are deterministic per cap and agree across caps to rounding. */
+int achi_ctx_set_grid_cap(achi_ctx* ctx, int max_ctas);
 /* copies the last error message (NUL-terminated, truncated to len) */
 int achi_last_error(const achi_ctx* ctx, char* buf, size_t len);
 /* EigenNonConvergence::best_residual of the last error (errors.hpp:302-306) */

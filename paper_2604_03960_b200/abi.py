@@ -148,6 +148,7 @@ def load():
         "achi_timer_start": (C.c_int, [vp]),
         "achi_timer_stop": (C.c_int, [vp, dp]),
         "achi_flush_l2": (C.c_int, [vp, C.c_size_t]),
+        "achi_ctx_set_grid_cap": (C.c_int, [vp, C.c_int]),
         "achi_chain_create": (C.c_int, [vp, P(ModelSpec), P(DmrgConfig), P(vp)]),
         "achi_chain_destroy": (C.c_int, [vp]),
         "achi_chain_sweep": (C.c_int, [vp, C.c_int, P(SweepRecord), P(i32), dp,

@@ -108,6 +108,11 @@ class Context:
     def flush_l2(self, nbytes=256 << 20):
         self._check(self.lib.achi_flush_l2(self.h, C.c_size_t(nbytes)))
 
+    def set_grid_cap(self, max_ctas):
+        """Cap this context's cooperative-kernel grids (0 = none): for several
+        contexts sharing one GPU."""
+        self._check(self.lib.achi_ctx_set_grid_cap(self.h, int(max_ctas)))
+
     # ---- local kernels (host buffers) ----
     def apply_effective_hamiltonian(self, L, W1, W2, R, theta):
         """dmrg.cpp:58-71; L (chl,D1,chl), W (D,d,d,D'), R (chr,D3,chr), theta (chl,d,d,chr)."""

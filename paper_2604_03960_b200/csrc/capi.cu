@@ -101,6 +101,13 @@ int achi_ctx_create(int device, achi_ctx** out) {
   });
 }
 
+int achi_ctx_set_grid_cap(achi_ctx* ctx, int max_ctas) {
+  return guard(ctx, [&] {
+    if (max_ctas < 0) fail(ACHI_E_INVALID_CONFIG, "grid cap must be >= 0");
+    ctx->c.grid_cap = max_ctas;
+  });
+}
+
 int achi_ctx_destroy(achi_ctx* ctx) {
   if (!ctx) return ACHI_OK;
   cudaSetDevice(ctx->c.device);

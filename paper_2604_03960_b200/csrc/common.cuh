@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -193,6 +194,12 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
   int num_sms = 148;
+  // cap on the CTAs of this context's cooperative kernels (0: none); several
+  // contexts sharing a GPU (ensemble chains in flight) each get a share
+  int grid_cap = 0;
+  int cap_grid(long want) const {
+    return static_cast<int>(grid_cap > 0 ? std::min<long>(want, grid_cap) : want);
+  }
   std::string last_error;
   double last_residual = 0;
   // scratch

@@ -63,7 +63,7 @@ void heff_apply_small(Ctx& ctx, const HeffOps& op, const double* theta, double* 
   }
   const long itemsA = cdiv(op.chl, HS_TM / op.D1) * cdiv(op.chr, HS_JRB);
   const long itemsB = cdiv(M2, HS_TM) * cdiv(N2, HS_TN) * op.D3;
-  const int grid = static_cast<int>(std::max<long>(1, std::min<long>(std::max(itemsA, itemsB), max_blocks)));
+  const int grid = std::max(1, ctx.cap_grid(std::min<long>(std::max(itemsA, itemsB), max_blocks)));
   HsArgs a{op.L, op.R, theta, out, X, part, op.mix, op.chl, op.chr, op.d, op.D1, op.D3};
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(grid);

@@ -780,7 +780,8 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
   }
   // fixed for a given n: the chunking (and so every reduction order) is deterministic
   // (about one element per thread up to two CTAs per SM: the passes are latency-bound)
-  const int orth_grid = static_cast<int>(std::max<long>(1, std::min<long>(cdiv(n, ORTH_THREADS), orth_max)));
+  const int orth_grid =
+      std::max(1, ctx.cap_grid(std::min<long>(cdiv(n, ORTH_THREADS), orth_max)));
   const size_t need_part = static_cast<size_t>(129) * orth_grid + 64;
   if (ws.partials.cap < need_part) {
     for (auto& g : ws.graphs) g.reset();

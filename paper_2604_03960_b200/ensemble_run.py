@@ -68,11 +68,19 @@ class Dist:
             self.dist.destroy_process_group()
 
 
-def run_workers(units, inflight, work, device_index):
+def run_workers(units, inflight, work, device_index, grid_share=True):
     """Run work(ctx, unit) for `units` on `inflight` host threads, each with its own
-    context (stream).  Returns ({unit: record}, max device seconds over workers)."""
+    context (stream).  With grid_share, each context's cooperative kernels are capped
+    at its share of the GPU (2 CTAs per SM / inflight) so the chains in flight run
+    side by side.  Returns ({unit: record}, max device seconds over workers)."""
     from .api import Context
     queue = list(units)
+    nthreads = max(1, min(inflight, len(queue)))
+    try:
+        import torch
+        sms = torch.cuda.get_device_properties(device_index).multi_processor_count
+    except Exception:  # noqa: BLE001 - no torch/GPU: B200 default
+        sms = 148
     lock = threading.Lock()
     results, times, errors = {}, [], []
     start = threading.Barrier(max(1, min(inflight, len(queue))))
@@ -80,6 +88,8 @@ def run_workers(units, inflight, work, device_index):
     def worker():
         try:
             ctx = Context(device_index)
+            if grid_share and nthreads > 1:
+                ctx.set_grid_cap(max(8, 2 * sms // nthreads))
             start.wait()
             ctx.timer_start()
             while True:
@@ -96,7 +106,7 @@ def run_workers(units, inflight, work, device_index):
             errors.append(e)
             start.abort()
 
-    threads = [threading.Thread(target=worker) for _ in range(max(1, min(inflight, len(queue))))]
+    threads = [threading.Thread(target=worker) for _ in range(nthreads)]
     for t in threads:
         t.start()
     for t in threads:
@@ -119,7 +129,7 @@ def job_c4(args, dist):
                 float(r["converged"])]
 
     dist.barrier()
-    res, secs = run_workers(mine, args.inflight, work, dist.local)
+    res, secs = run_workers(mine, args.inflight, work, dist.local, not args.no_grid_share)
     job_s = dist.max(secs)
     width = 5
     out = gather_records_from(res, width, args.chains, plan, dist)
@@ -149,7 +159,7 @@ def job_c2(args, dist):
         return [float(s[0]), float(s[-1]), abs(float((s * s).sum()) - fro) / fro, sweeps]
 
     dist.barrier()
-    res, secs = run_workers(mine, args.inflight, work, dist.local)
+    res, secs = run_workers(mine, args.inflight, work, dist.local, not args.no_grid_share)
     job_s = dist.max(secs)
     out = gather_records_from(res, 4, args.batch, plan, dist)
     return job_s, out, {"unit": "SVDs/s", "units": args.batch,
@@ -178,6 +188,8 @@ def main(argv=None):
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--svd-chi", type=int, default=256)
     ap.add_argument("--inflight", type=int, default=4)
+    ap.add_argument("--no-grid-share", action="store_true",
+                    help="do not cap each in-flight context's cooperative grids")
     args = ap.parse_args(argv)
     dist = Dist()
     t0 = time.perf_counter()
