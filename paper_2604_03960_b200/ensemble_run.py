@@ -68,11 +68,12 @@ class Dist:
             self.dist.destroy_process_group()
 
 
-def run_workers(units, inflight, work, device_index, grid_share=True):
+def run_workers(units, inflight, work, device_index, grid_share=False):
     """Run work(ctx, unit) for `units` on `inflight` host threads, each with its own
     context (stream).  With grid_share, each context's cooperative kernels are capped
-    at its share of the GPU (2 CTAs per SM / inflight) so the chains in flight run
-    side by side.  Returns ({unit: record}, max device seconds over workers)."""
+    at its share of the GPU (2 CTAs per SM / inflight); measured slower than letting
+    the chains' kernels interleave uncapped (profiles/ensemble_r01b.txt), so off by
+    default.  Returns ({unit: record}, max device seconds over workers)."""
     from .api import Context
     queue = list(units)
     nthreads = max(1, min(inflight, len(queue)))
@@ -129,7 +130,7 @@ def job_c4(args, dist):
                 float(r["converged"])]
 
     dist.barrier()
-    res, secs = run_workers(mine, args.inflight, work, dist.local, not args.no_grid_share)
+    res, secs = run_workers(mine, args.inflight, work, dist.local, args.grid_share)
     job_s = dist.max(secs)
     width = 5
     out = gather_records_from(res, width, args.chains, plan, dist)
@@ -159,7 +160,7 @@ def job_c2(args, dist):
         return [float(s[0]), float(s[-1]), abs(float((s * s).sum()) - fro) / fro, sweeps]
 
     dist.barrier()
-    res, secs = run_workers(mine, args.inflight, work, dist.local, not args.no_grid_share)
+    res, secs = run_workers(mine, args.inflight, work, dist.local, args.grid_share)
     job_s = dist.max(secs)
     out = gather_records_from(res, 4, args.batch, plan, dist)
     return job_s, out, {"unit": "SVDs/s", "units": args.batch,
@@ -188,8 +189,8 @@ def main(argv=None):
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--svd-chi", type=int, default=256)
     ap.add_argument("--inflight", type=int, default=4)
-    ap.add_argument("--no-grid-share", action="store_true",
-                    help="do not cap each in-flight context's cooperative grids")
+    ap.add_argument("--grid-share", action="store_true",
+                    help="cap each in-flight context's cooperative grids at its share of the GPU")
     args = ap.parse_args(argv)
     dist = Dist()
     t0 = time.perf_counter()

@@ -86,7 +86,7 @@ def _runner_worker(rank, world, port, q):
                       WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
     from paper_2604_03960_b200 import ensemble_run
 
-    def fake_workers(units, inflight, work, device_index, grid_share=True):
+    def fake_workers(units, inflight, work, device_index, grid_share=False):
         # deterministic per-unit records and a per-rank "device time"
         return {u: [float(u), -0.4 - 0.001 * u, 5.0, 100.0, 1.0] for u in units}, 1.0 + rank
 
