@@ -231,8 +231,10 @@ __device__ void factor_panel(PqSmem& sm, const PqArgs& a, int p) {
       piv[q] = (i > j && i < nr) ? sm.A[c][i] : 0.0;
       xn = fma(piv[q], piv[q], xn);
     }
+    const long long pc0 = prof ? clock64() : 0;
     const double alpha = sm.A[c][j];
     xn = warp_sum(xn);
+    const long long pc1 = prof ? clock64() : 0;
     double tau = 0.0, sc = 0.0, beta = alpha;
     if (xn > 0.0) {
       const double nrm = sqrt(fma(alpha, alpha, xn));
@@ -240,6 +242,7 @@ __device__ void factor_panel(PqSmem& sm, const PqArgs& a, int p) {
       tau = (beta - alpha) / beta;
       sc = 1.0 / (alpha - beta);
     }
+    const long long pc2 = prof ? clock64() : 0;
     if (threadIdx.x == 0) sm.tau[c] = tau;
     // v = (1 at row j, sc * x below), zero above; a <- a - tau (v^T a) v
     double v[PQ_NQ];
@@ -256,6 +259,7 @@ __device__ void factor_panel(PqSmem& sm, const PqArgs& a, int p) {
         for (int m = 0; m < 4; ++m) d[m] = fma(v[q], col[m][q], d[m]);
 #pragma unroll
       for (int m = 0; m < 4; ++m) d[m] = warp_sum(d[m]);
+      if (prof) a.prof[11] += clock64() - pc2;
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         const int cc = warp + 8 * m;
@@ -292,7 +296,15 @@ __device__ void factor_panel(PqSmem& sm, const PqArgs& a, int p) {
           }
         }
     }
+    const long long pc3 = prof ? clock64() : 0;
     __syncthreads();
+    if (prof) {
+      const long long pc4 = clock64();
+      a.prof[9] += pc1 - pc0;   // alpha load + norm warp reduction
+      a.prof[10] += pc2 - pc1;  // sqrt / divisions
+      a.prof[12] += pc3 - pc2;  // dots, reductions, updates, publish (warp 0)
+      a.prof[13] += pc4 - pc3;  // barrier
+    }
   }
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
@@ -483,8 +495,8 @@ void qr_precond(Ctx& ctx, double* G, long ldg, int mr, int ng, int nr, int pad_m
   static DevArr<long long> profbuf;
   PqArgs a{G, ldg, mr, ng, nr, pad_mod, pad_lim, std::min(nr, mr), V0, nullptr};
   if (prof_on) {
-    a.prof = profbuf.reserve(12);
-    ACHI_CUDA(cudaMemsetAsync(a.prof, 0, 12 * sizeof(long long), ctx.stream));
+    a.prof = profbuf.reserve(16);
+    ACHI_CUDA(cudaMemsetAsync(a.prof, 0, 16 * sizeof(long long), ctx.stream));
   }
   const int ncta = (std::max(mr, nr) + PQ_B - 1) / PQ_B;
   cudaLaunchConfig_t lc = {};
@@ -502,11 +514,11 @@ void qr_precond(Ctx& ctx, double* G, long ldg, int mr, int ng, int nr, int pad_m
   ACHI_CUDA(cudaLaunchKernelEx(&lc, qr_precond_kernel, a));
   ACHI_LAUNCHED(ctx);
   if (prof_on) {
-    long long h[12];
+    long long h[16];
     ACHI_CUDA(cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
     ctx.sync();
     std::fprintf(stderr, "[qr-precond] mr=%d nr=%d ctas=%d cycles(CTA1): wait %lld stage %lld columns %lld "
-                 "factor %lld qrows %lld tail %lld | panel1 loop %lld loop+Y %lld loop+T %lld\n", mr, nr, ncta, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[8], h[7]);
+                 "factor %lld qrows %lld tail %lld | panel1 loop %lld loop+Y %lld loop+T %lld | per panel-1 loop: norm %lld sqrtdiv %lld dots %lld work %lld bar %lld\n", mr, nr, ncta, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[8], h[7], h[9], h[10], h[11], h[12], h[13]);
   }
 }
 
