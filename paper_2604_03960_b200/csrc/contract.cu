@@ -180,7 +180,11 @@ void heff_apply(Ctx& ctx, const HeffOps& op, const double* theta, double* out) {
     const char* e = std::getenv("ACHI_HEFF_SMALL");
     return !(e && e[0] == '0');
   }();
-  if (small_on && heff_small_applicable(op)) {
+  static const int small_max = [] {  // largest chi on the fused path (crossover with the TMA path)
+    const char* e = std::getenv("ACHI_HEFF_SMALL_MAX");
+    return e ? std::atoi(e) : 256;
+  }();
+  if (small_on && std::max(op.chl, op.chr) <= small_max && heff_small_applicable(op)) {
     heff_apply_small(ctx, op, theta, out);
     return;
   }

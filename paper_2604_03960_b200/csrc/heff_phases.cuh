@@ -12,8 +12,10 @@ namespace hs {
 constexpr int HS_THREADS = 256;
 constexpr int HS_TM = 32;        // tile rows
 constexpr int HS_TN = 64;        // tile cols
-constexpr int HS_KMAX = 128;     // max contraction length (chl for A, chr for B)
-constexpr int HS_LD = HS_KMAX + 4;
+constexpr int HS_KMAX = 128;     // contraction length bound of the small instantiation
+constexpr int HS_KMAX_WIDE = 256; // ... and of the wide one (chi 129..256)
+template <int K>
+__host__ __device__ constexpr int hs_ld() { return K + 4; }
 constexpr int HS_MAXW = 64;      // max MPO mixing inputs/outputs (D d^2)
 constexpr int HS_MAXNNZ = 512;
 
@@ -39,7 +41,9 @@ __device__ __forceinline__ void mma16x8x4(double (&c)[4], double a0, double a1, 
 // C (32 x 64) = As (32 x K, row-major, ld HS_LD) * Bs^T (Bs: 64 x K, ld HS_LD);
 // warp w: rows 16 (w / 4), cols 16 (w % 4) = two n8 tiles.  Returns the
 // warp's accumulators for the store.
+template <int KM>
 __device__ __forceinline__ void tile_mma(const double* As, const double* Bs, int K, double (&acc)[2][4]) {
+  constexpr int HS_LD = hs_ld<KM>();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int mr = (warp >> 2) * 16, nc = (warp & 3) * 16;
@@ -98,8 +102,10 @@ constexpr int HS_JRB = 16;  // jr per phase-A tile (d = 2)
 
 // A: Y[((bl,s'),e), jr] = sum_{(a,s)} W12[(s',e),(a,s)] sum_jl L[(bl,a),jl] theta[jl,(s,jr)]
 // The GEMM tile is staged in shared memory and mixed there (no X buffer).
+template <int KM>
 __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const double* theta,
                                         double* As, double* Bs, int blk, int nblk) {
+  constexpr int HS_LD = hs_ld<KM>(), RG = HS_THREADS / KM;  // row groups of the K-major loads
   const int t = threadIdx.x;
   const int chl = a.chl, chr = a.chr, dd = a.d * a.d, D1 = a.D1, D3 = a.D3;
   const int N1 = dd * chr, blb = phase_a_blb(a), rows = blb * D1;
@@ -109,39 +115,45 @@ __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const
     const int bl0 = (item / tn) * blb, jr0 = (item % tn) * HS_JRB;
     __syncthreads();
     {
-      // As[m][k] = L[bl0*D1 + m][k] (m < blb*D1): thread -> (k = t % 128, rows t / 128 + 2u);
+      // As[m][k] = L[bl0*D1 + m][k] (m < blb*D1): thread -> (k = t % KM, rows t / KM + RG u);
       // every load of a thread is issued before its stores
-      const int k = t & (HS_KMAX - 1), r0 = t >> 7;
-      double v[HS_TM / 2];
+      const int k = t % KM, r0 = t / KM;
+      double v[HS_TM / RG];
 #pragma unroll
-      for (int u = 0; u < HS_TM / 2; ++u) {
-        const int m = r0 + 2 * u;
+      for (int u = 0; u < HS_TM / RG; ++u) {
+        const int m = r0 + RG * u;
         v[u] = (m < rows && bl0 * D1 + m < chl * D1 && k < chl)
                    ? a.L[static_cast<long>(bl0 * D1 + m) * chl + k]
                    : 0.0;
       }
       if (k < K4)
 #pragma unroll
-        for (int u = 0; u < HS_TM / 2; ++u) As[(r0 + 2 * u) * HS_LD + k] = v[u];
+        for (int u = 0; u < HS_TM / RG; ++u) As[(r0 + RG * u) * HS_LD + k] = v[u];
     }
     {
-      // Bs[n][k] = theta[k][s*chr + jr0 + q], n = s*16 + q: thread -> (n = t % 64, k = t / 64 + 4u)
+      // Bs[n][k] = theta[k][s*chr + jr0 + q], n = s*16 + q: thread -> (n = t % 64, k = t / 64 + 4u),
+      // in chunks of 32 loads
       const int n = t & (HS_TN - 1), kq = t >> 6;
       const int s = n / HS_JRB, jr = jr0 + (n % HS_JRB);
       const bool ok = s < dd && jr < chr;
-      double v[HS_KMAX / 4];
 #pragma unroll
-      for (int u = 0; u < HS_KMAX / 4; ++u) {
-        const int k = kq + 4 * u;
-        v[u] = (ok && k < chl) ? theta[static_cast<long>(k) * N1 + s * chr + jr] : 0.0;
+      for (int h = 0; h < KM / 128; ++h) {
+        double v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const int k = kq + 4 * (32 * h + u);
+          v[u] = (ok && k < chl) ? theta[static_cast<long>(k) * N1 + s * chr + jr] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const int k = kq + 4 * (32 * h + u);
+          if (k < K4) Bs[n * HS_LD + k] = v[u];
+        }
       }
-#pragma unroll
-      for (int u = 0; u < HS_KMAX / 4; ++u)
-        if (kq + 4 * u < K4) Bs[n * HS_LD + kq + 4 * u] = v[u];
     }
     __syncthreads();
     double acc[2][4];
-    tile_mma(As, Bs, chl, acc);
+    tile_mma<KM>(As, Bs, chl, acc);
     __syncthreads();
     // stage the 32 x 64 tile (rows (bl, a), cols (s, q)) into As, then mix
     tile_store(acc, As, HS_LD, 0, 0, HS_TM, HS_TN);
@@ -165,7 +177,9 @@ __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const
 }
 
 // B: P_e[(bl,s'), br] = sum_jr Y[(bl,s'),(e,jr)] R[br,(e,jr)]  (one item per e: split-K)
+template <int KM>
 __device__ __forceinline__ void phase_b(const HsArgs& a, double* As, double* Bs, int blk, int nblk) {
+  constexpr int HS_LD = hs_ld<KM>(), RG = HS_THREADS / KM;
   const int t = threadIdx.x;
   const int chl = a.chl, chr = a.chr, dd = a.d * a.d, D3 = a.D3;
   const int M2 = chl * dd, N2 = chr;
@@ -177,34 +191,37 @@ __device__ __forceinline__ void phase_b(const HsArgs& a, double* As, double* Bs,
     const int m0 = (rest / tn) * HS_TM, n0 = (rest % tn) * HS_TN;
     __syncthreads();
     {
-      // As[m][jr] = Y[(m0+m), e, jr]: thread -> (jr = t % 128, rows t / 128 + 2u)
-      const int jr = t & (HS_KMAX - 1), r0 = t >> 7;
-      double v[HS_TM / 2];
+      // As[m][jr] = Y[(m0+m), e, jr]: thread -> (jr = t % KM, rows t / KM + RG u)
+      const int jr = t % KM, r0 = t / KM;
+      double v[HS_TM / RG];
 #pragma unroll
-      for (int u = 0; u < HS_TM / 2; ++u) {
-        const int row = m0 + r0 + 2 * u;
+      for (int u = 0; u < HS_TM / RG; ++u) {
+        const int row = m0 + r0 + RG * u;
         v[u] = (row < M2 && jr < chr) ? a.X[(static_cast<long>(row) * D3 + e) * chr + jr] : 0.0;
       }
       if (jr < K4)
 #pragma unroll
-        for (int u = 0; u < HS_TM / 2; ++u) As[(r0 + 2 * u) * HS_LD + jr] = v[u];
+        for (int u = 0; u < HS_TM / RG; ++u) As[(r0 + RG * u) * HS_LD + jr] = v[u];
     }
     {
-      // Bs[n][jr] = R[n0+n][e][jr]: thread -> (jr = t % 128, n = t / 128 + 2u)
-      const int jr = t & (HS_KMAX - 1), q0 = t >> 7;
-      double v[HS_TN / 2];
+      // Bs[n][jr] = R[n0+n][e][jr]: thread -> (jr = t % KM, n = t / KM + RG u), chunks of 32
+      const int jr = t % KM, q0 = t / KM;
 #pragma unroll
-      for (int u = 0; u < HS_TN / 2; ++u) {
-        const int n = q0 + 2 * u;
-        v[u] = (n0 + n < N2 && jr < chr) ? a.R[(static_cast<long>(n0 + n) * D3 + e) * chr + jr] : 0.0;
+      for (int h = 0; h < HS_TN / RG / 32; ++h) {
+        double v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const int n = q0 + RG * (32 * h + u);
+          v[u] = (n0 + n < N2 && jr < chr) ? a.R[(static_cast<long>(n0 + n) * D3 + e) * chr + jr] : 0.0;
+        }
+        if (jr < K4)
+#pragma unroll
+          for (int u = 0; u < 32; ++u) Bs[(q0 + RG * (32 * h + u)) * HS_LD + jr] = v[u];
       }
-      if (jr < K4)
-#pragma unroll
-        for (int u = 0; u < HS_TN / 2; ++u) Bs[(q0 + 2 * u) * HS_LD + jr] = v[u];
     }
     __syncthreads();
     double acc[2][4];
-    tile_mma(As, Bs, chr, acc);
+    tile_mma<KM>(As, Bs, chr, acc);
     tile_store(acc, a.part + static_cast<long>(e) * M2 * N2, N2, m0, n0, M2, N2);
   }
 }
@@ -222,7 +239,8 @@ __device__ __forceinline__ void phase_c(const HsArgs& a, double* out, int blk, i
   }
 }
 
-inline size_t smem_bytes() { return sizeof(double) * (HS_TM + HS_TN) * HS_LD; }
+template <int KM>
+inline size_t smem_bytes() { return sizeof(double) * (HS_TM + HS_TN) * hs_ld<KM>(); }
 
 }  // namespace hs
 }  // namespace achi

@@ -26,39 +26,33 @@ namespace {
 
 using namespace hs;
 
+template <int KM>
 __global__ void __launch_bounds__(HS_THREADS) heff_small_kernel(HsArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
-  double* As = reinterpret_cast<double*>(dyn);  // [32][HS_LD]
-  double* Bs = As + HS_TM * HS_LD;              // [64][HS_LD]
+  double* As = reinterpret_cast<double*>(dyn);  // [32][LD]
+  double* Bs = As + HS_TM * hs_ld<KM>();        // [64][LD]
   __shared__ MixSmem w;
   cg::grid_group grid = cg::this_grid();
   load_mix(a.mix, w);
   __syncthreads();
-  phase_a(a, w, a.theta, As, Bs, blockIdx.x, gridDim.x);
+  phase_a<KM>(a, w, a.theta, As, Bs, blockIdx.x, gridDim.x);
   grid.sync();
-  phase_b(a, As, Bs, blockIdx.x, gridDim.x);
+  phase_b<KM>(a, As, Bs, blockIdx.x, gridDim.x);
   grid.sync();
   phase_c(a, a.out, blockIdx.x, gridDim.x);
 }
 
-}  // namespace
-bool heff_small_applicable(const HeffOps& op) {
-  return op.d == 2 && op.D1 >= 1 && op.D1 <= HS_TM && op.chl <= HS_KMAX && op.chr <= HS_KMAX &&
-         op.mix.nin <= HS_MAXW && op.mix.nout <= HS_MAXW && op.mix.nnz <= HS_MAXNNZ;
-}
-
-void heff_apply_small(Ctx& ctx, const HeffOps& op, const double* theta, double* out) {
+template <int KM>
+void launch_small(Ctx& ctx, const HeffOps& op, const double* theta, double* out, double* X, double* part) {
   const int dd = op.d * op.d;
   const long M2 = static_cast<long>(op.chl) * dd, N2 = op.chr;
-  double* X = ctx.ws_a.reserve(static_cast<size_t>(M2 * op.D3 * N2));  // Y
-  double* part = ctx.ws_b.reserve(static_cast<size_t>(op.D3 * M2 * N2));
   static int max_blocks = 0;
-  const size_t smem = smem_bytes();
+  const size_t smem = smem_bytes<KM>();
   if (max_blocks == 0) {
-    ACHI_CUDA(cudaFuncSetAttribute(heff_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ACHI_CUDA(cudaFuncSetAttribute(heff_small_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
     int per_sm = 0;
-    ACHI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heff_small_kernel, HS_THREADS, smem));
+    ACHI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heff_small_kernel<KM>, HS_THREADS, smem));
     max_blocks = std::max(1, per_sm) * ctx.num_sms;
   }
   const long itemsA = cdiv(op.chl, HS_TM / op.D1) * cdiv(op.chr, HS_JRB);
@@ -75,8 +69,27 @@ void heff_apply_small(Ctx& ctx, const HeffOps& op, const double* theta, double* 
   at[0].val.cooperative = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  ACHI_CUDA(cudaLaunchKernelEx(&lc, heff_small_kernel, a));
+  ACHI_CUDA(cudaLaunchKernelEx(&lc, heff_small_kernel<KM>, a));
   ACHI_LAUNCHED(ctx);
+}
+
+}  // namespace
+
+bool heff_small_applicable(const HeffOps& op) {
+  return op.d == 2 && op.D1 >= 1 && op.D1 <= HS_TM && op.chl <= HS_KMAX_WIDE &&
+         op.chr <= HS_KMAX_WIDE && op.mix.nin <= HS_MAXW && op.mix.nout <= HS_MAXW &&
+         op.mix.nnz <= HS_MAXNNZ;
+}
+
+void heff_apply_small(Ctx& ctx, const HeffOps& op, const double* theta, double* out) {
+  const int dd = op.d * op.d;
+  const long M2 = static_cast<long>(op.chl) * dd, N2 = op.chr;
+  double* X = ctx.ws_a.reserve(static_cast<size_t>(M2 * op.D3 * N2));  // Y
+  double* part = ctx.ws_b.reserve(static_cast<size_t>(op.D3 * M2 * N2));
+  if (op.chl <= HS_KMAX && op.chr <= HS_KMAX)
+    launch_small<HS_KMAX>(ctx, op, theta, out, X, part);
+  else
+    launch_small<HS_KMAX_WIDE>(ctx, op, theta, out, X, part);
 }
 
 }  // namespace achi

@@ -43,8 +43,9 @@ constexpr int JT = 256;       // threads per CTA
 constexpr int JCH = 64;       // rows per chunk (stream mode)
 constexpr int JLD = JCH + 4;  // conflict-free DMMA fragment loads
 constexpr int SLD = JW + 4;
-constexpr int CL_ROWS = 256;  // cluster mode: max working rows
-constexpr int CL_MAXP = 8;    // cluster mode: max block pairs (portable cluster size)
+constexpr int CL_ROWS = 384;  // cluster mode: max working rows (shared memory bound)
+constexpr int CL_MAXP = 16;   // cluster mode: max block pairs (non-portable cluster of 16)
+constexpr int CL_MAXP_DB = 8; // V replay double-buffers the rotations up to this many pairs
 constexpr int MAX_SWEEPS = 40;
 constexpr int RP_ROWS = 2;    // V replay: rows of V per CTA
 constexpr double EPS = 2.220446049250313e-16;
@@ -493,8 +494,9 @@ __global__ void __launch_bounds__(JT) v_replay_kernel(double* V, long vstride, i
                                                       long jstride, const int* __restrict__ sweeps,
                                                       const double* __restrict__ v0) {
   extern __shared__ __align__(16) unsigned char dyn[];
-  double* Js = reinterpret_cast<double*>(dyn);                    // [2][npairs][32*32]
-  double* Vs = Js + 2L * npairs * JW * JW;                         // [2][RP_ROWS][ng]
+  const bool dbuf = npairs <= CL_MAXP_DB;                          // prefetch the next round
+  double* Js = reinterpret_cast<double*>(dyn);                    // [1 or 2][npairs][32*32]
+  double* Vs = Js + (dbuf ? 2L : 1L) * npairs * JW * JW;           // [2][RP_ROWS][ng]
   const int b = blockIdx.y;
   const int r0 = blockIdx.x * RP_ROWS;
   const int rounds = nb - 1;
@@ -518,12 +520,18 @@ __global__ void __launch_bounds__(JT) v_replay_kernel(double* V, long vstride, i
   cp_commit();
   int cur = 0;
   for (long rg = 0; rg < total; ++rg) {
-    if (rg + 1 < total) stage(rg + 1, (rg + 1) & 1);
-    cp_commit();
-    cp_wait<1>();
+    if (dbuf) {
+      if (rg + 1 < total) stage(rg + 1, (rg + 1) & 1);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      if (rg > 0) stage(rg, 0);  // the buffer was released by the barrier closing round rg-1
+      cp_commit();
+      cp_wait<0>();
+    }
     __syncthreads();
     const int r = static_cast<int>(rg % rounds);
-    const double* J = Js + static_cast<long>(rg & 1) * npairs * JW * JW;
+    const double* J = Js + (dbuf ? static_cast<long>(rg & 1) * npairs * JW * JW : 0L);
     const double* vin = Vs + cur * RP_ROWS * ng;
     double* vout = Vs + (cur ^ 1) * RP_ROWS * ng;
     for (int c = threadIdx.x; c < ng; c += JT) {
@@ -870,8 +878,9 @@ size_t stream_smem() { return sizeof(Chunk) * STREAM_STAGES + sizeof(Small) + 16
 size_t cluster_smem(int rows_pad) {
   return sizeof(double) * 2 * JW * (rows_pad + 4) + sizeof(Small) + 16;
 }
-size_t replay_smem(int npairs, int ng) {
-  return sizeof(double) * (2L * npairs * JW * JW + 2L * RP_ROWS * ng);
+size_t replay_smem(int npairs, int ng) {  // rotations double-buffered up to CL_MAXP_DB pairs
+  const long jbufs = npairs <= CL_MAXP_DB ? 2 : 1;
+  return sizeof(double) * (jbufs * npairs * JW * JW + 2L * RP_ROWS * ng);
 }
 
 }  // namespace
@@ -915,7 +924,33 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   int* sweeps_host = ws.sweeps_host.reserve(nsw);
   const int nb = ng / JB;  // even (ng multiple of 32)
   const int npairs = nb / 2;
-  const bool cluster = ldg <= CL_ROWS && npairs <= CL_MAXP;
+  bool cluster = ldg <= CL_ROWS && npairs <= CL_MAXP;
+  if (cluster && npairs > 8) {
+    // clusters beyond the portable 8 CTAs: only if the device can place one
+    static int placeable[CL_MAXP + 1] = {};
+    if (placeable[npairs] == 0) {
+      ACHI_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      ACHI_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(cluster_smem(CL_ROWS))));
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(npairs);
+      q.blockDim = dim3(JT);
+      q.dynamicSmemBytes = cluster_smem(CL_ROWS);
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = npairs;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      int nclusters = 0;
+      placeable[npairs] =
+          (cudaOccupancyMaxActiveClusters(&nclusters, jacobi_cluster_kernel, &q) == cudaSuccess &&
+           nclusters > 0) ? 1 : -1;
+      cudaGetLastError();
+    }
+    cluster = placeable[npairs] > 0;
+  }
   // pad columns: rows side -> columns >= m_true (theta rows (l,s1), padded l last);
   // cols side with padding -> columns (s2, jr) with jr >= chr_true (d = 2 on the padded path)
   int pad_mod = ng, pad_lim = rows ? m_true : n_true;
@@ -996,7 +1031,8 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     if (V) {
       // sized once for the largest cluster problem (40 MB): growing it with
       // chi went through the pool's slow path (up to ~20-90 ms per growth)
-      const size_t cap = static_cast<size_t>(MAX_SWEEPS) * (2 * CL_MAXP - 1) * CL_MAXP;
+      const int pc = npairs <= 8 ? 8 : CL_MAXP;  // 40 MB, or 162 MB once wider clusters occur
+      const size_t cap = static_cast<size_t>(MAX_SWEEPS) * (2 * pc - 1) * pc;
       const size_t need = static_cast<size_t>(batch) * jstride * npairs;
       jrec = ws.jrec.reserve(std::max(need, cap) * JW * JW);
       jflag = ws.jflag.reserve(std::max(need, cap));
@@ -1052,8 +1088,10 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
       const size_t rs = replay_smem(npairs, ng);
       static bool rattr = false;
       if (!rattr) {
-        ACHI_CUDA(cudaFuncSetAttribute(v_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(replay_smem(CL_MAXP, CL_MAXP * JW))));
+        ACHI_CUDA(cudaFuncSetAttribute(
+            v_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            static_cast<int>(std::max(replay_smem(CL_MAXP_DB, CL_MAXP_DB * JW),
+                                      replay_smem(CL_MAXP, CL_MAXP * JW)))));
         rattr = true;
       }
       dim3 grid(cdiv(ng, RP_ROWS), batch);

@@ -108,10 +108,12 @@ def test_env_updates_match_oracle(ctx, oracle, chl, chn):
 
 @pytest.mark.parametrize("shape", [(2, 2), (8, 8), (6, 3), (3, 6), (1, 5), (5, 1), (12, 9),
                                    (64, 64), (100, 37), (96, 256), (512, 512),
-                                   # cluster-mode edges: one block pair, C3-sized, the
-                                   # 256x256 limit, and just past it (stream mode)
+                                   # cluster-mode edges: one block pair, C3-sized, portable
+                                   # clusters (<= 8 pairs), non-portable clusters up to 16
+                                   # pairs / 384 rows, and past them (stream mode)
                                    (32, 32), (33, 40), (200, 218), (256, 256), (257, 256),
-                                   (256, 300)])
+                                   (256, 300), (320, 330), (384, 384), (385, 384), (300, 512),
+                                   (600, 300)])
 def test_svd_matches_oracle(ctx, oracle, shape):
     rng = np.random.default_rng(sum(shape))
     m = rng.standard_normal(shape)
@@ -403,6 +405,19 @@ def test_dmrg_large_chi_paths(ctx, oracle):
     (real-gauge restatement of run_dmrg)."""
     spec = abi.model_spec(20)
     cfg = abi.fixed_config(256, max_sweeps=5)  # chi grows by up to d^2 per sweep from Neel
+    g = ctx.run_dmrg(spec, cfg)
+    o = oracle.run_dmrg(spec, cfg)
+    compare_runs(g, o)
+    assert max(g["chi_profiles"][-1]) > 128
+
+
+@pytest.mark.slow
+def test_dmrg_wide_cluster_svd(ctx, oracle):
+    """Fixed chi = 160 at N = 18: centre-bond working matrices 320 wide take the
+    non-portable cluster SVD (10 block pairs); energies and chi profiles against the
+    oracle."""
+    spec = abi.model_spec(18)
+    cfg = abi.fixed_config(160, max_sweeps=5)
     g = ctx.run_dmrg(spec, cfg)
     o = oracle.run_dmrg(spec, cfg)
     compare_runs(g, o)
