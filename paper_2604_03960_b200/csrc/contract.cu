@@ -180,9 +180,12 @@ void heff_apply(Ctx& ctx, const HeffOps& op, const double* theta, double* out) {
     const char* e = std::getenv("ACHI_HEFF_SMALL");
     return !(e && e[0] == '0');
   }();
-  static const int small_max = [] {  // largest chi on the fused path (crossover with the TMA path)
+  // largest chi on the fused path: the wide instantiation (chi 129..256) measured
+  // slower than the TMA GEMM path (53/70/127 vs 43/49/102 us at chi 160/192/256,
+  // profiles/heff_study_r01.txt), so the crossover stays at 128 unless overridden
+  static const int small_max = [] {
     const char* e = std::getenv("ACHI_HEFF_SMALL_MAX");
-    return e ? std::atoi(e) : 256;
+    return e ? std::atoi(e) : 128;
   }();
   if (small_on && std::max(op.chl, op.chr) <= small_max && heff_small_applicable(op)) {
     heff_apply_small(ctx, op, theta, out);
