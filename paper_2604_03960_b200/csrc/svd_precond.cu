@@ -66,6 +66,17 @@ __device__ __forceinline__ int coord(const PqArgs& a, int i) {
   return (i / a.pad_lim) * a.pad_mod + (i % a.pad_lim);
 }
 
+// 1/x from the FP64 reciprocal estimate and two Newton steps (to rounding;
+// the reflector stays orthogonal to working precision), off the DDIV slow path
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -239,8 +250,8 @@ __device__ void factor_panel(PqSmem& sm, const PqArgs& a, int p) {
     if (xn > 0.0) {
       const double nrm = sqrt(fma(alpha, alpha, xn));
       beta = alpha >= 0.0 ? -nrm : nrm;
-      tau = (beta - alpha) / beta;
-      sc = 1.0 / (alpha - beta);
+      tau = (beta - alpha) * rcp_nr(beta);
+      sc = rcp_nr(alpha - beta);
     }
     const long long pc2 = prof ? clock64() : 0;
     if (threadIdx.x == 0) sm.tau[c] = tau;
