@@ -405,7 +405,7 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   c.acc.begin(EventAcc::kMatvec, c.stream);  // the whole eigensolve (matvecs + orthogonalisation)
   EigsOut eig = eigs_lowest(
       c, lz, [&](const double* in, double* out) { heff_apply(c, op, in, out); }, nvec, dim, theta.p,
-      cfg.eig_tol, cfg.eig_max_iter, vec.p, 2 * b + (right ? 1 : 0), key);
+      cfg.eig_tol, cfg.eig_max_iter, vec.p, 2 * b + (right ? 1 : 0), key, &op);
   c.acc.end(c.stream, eig.matvecs * mv_flops);
   const auto t1 = clk::now();
   const SvdSide side = right ? SvdSide::kRows : SvdSide::kCols;

@@ -243,4 +243,11 @@ template <int KM>
 inline size_t smem_bytes() { return sizeof(double) * (HS_TM + HS_TN) * hs_ld<KM>(); }
 
 }  // namespace hs
+
+// Arguments of the fused small-chi matvec (KM = 128) for theta -> out, with its
+// workspaces reserved; false when the op takes another path (heff_small.cu).
+// items = max(phase-A, phase-B work items).
+bool heff_small_fusable(Ctx& ctx, const HeffOps& op, const double* theta, double* out, hs::HsArgs* args,
+                        long* items);
+
 }  // namespace achi

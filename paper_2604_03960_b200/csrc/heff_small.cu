@@ -16,6 +16,9 @@
 // Every sum runs in a fixed order: the result is deterministic.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "heff_phases.cuh"
 
 namespace cg = cooperative_groups;
@@ -79,6 +82,24 @@ bool heff_small_applicable(const HeffOps& op) {
   return op.d == 2 && op.D1 >= 1 && op.D1 <= HS_TM && op.chl <= HS_KMAX_WIDE &&
          op.chr <= HS_KMAX_WIDE && op.mix.nin <= HS_MAXW && op.mix.nout <= HS_MAXW &&
          op.mix.nnz <= HS_MAXNNZ;
+}
+
+bool heff_small_fusable(Ctx& ctx, const HeffOps& op, const double* theta, double* out, HsArgs* args,
+                        long* items) {
+  static const bool small_on = [] {
+    const char* e = std::getenv("ACHI_HEFF_SMALL");
+    return !(e && e[0] == '0');
+  }();
+  if (!small_on || std::max(op.chl, op.chr) > HS_KMAX || !heff_small_applicable(op)) return false;
+  const int dd = op.d * op.d;
+  const long M2 = static_cast<long>(op.chl) * dd, N2 = op.chr;
+  double* X = ctx.ws_a.reserve(static_cast<size_t>(M2 * op.D3 * N2));
+  double* part = ctx.ws_b.reserve(static_cast<size_t>(op.D3 * M2 * N2));
+  *args = HsArgs{op.L, op.R, theta, out, X, part, op.mix, op.chl, op.chr, op.d, op.D1, op.D3};
+  const long itemsA = cdiv(op.chl, HS_TM / op.D1) * cdiv(op.chr, HS_JRB);
+  const long itemsB = cdiv(M2, HS_TM) * cdiv(N2, HS_TN) * op.D3;
+  *items = std::max(itemsA, itemsB);
+  return true;
 }
 
 void heff_apply_small(Ctx& ctx, const HeffOps& op, const double* theta, double* out) {

@@ -8,6 +8,7 @@
 #include <limits>
 
 #include "lanczos.cuh"
+#include "heff_phases.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -514,7 +515,7 @@ __device__ void orth_reduce(const double* part, int nv, double* coef) {
 // Step j, part 1 (every CTA of a cooperative grid): w <- w - Q (Q^T w) twice,
 // beta_j = ||w||, q_{j+1} = w / beta_j into the basis and into qcur (the next
 // matvec input); block 0 stores alpha_j, beta_j.
-__global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) {
+__device__ void orth_step(const OrthArgs& a) {
   __shared__ double sh[ORTH_THREADS / 32][65];
   __shared__ double coef[64];
   __shared__ double red[32];
@@ -601,7 +602,9 @@ __global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) 
 // the reference's step decision (linalg.cpp:141-148), which advances ctl->j or
 // ends the loop.  In the graph it runs concurrently with the speculative
 // matvec of q_{j+1} (wasted only on the last step of a cycle).
-__global__ void __launch_bounds__(ORTH_THREADS) lanczos_tridiag_kernel(OrthArgs a) {
+__global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) { orth_step(a); }
+
+__device__ void tridiag_step(const OrthArgs& a) {
   __shared__ double sa[LANCZOS_BLOCK], sb[LANCZOS_BLOCK], sbb[LANCZOS_BLOCK];
   __shared__ double th_s, sc_s;
   __shared__ TwistScratch tw;
@@ -662,6 +665,56 @@ __global__ void __launch_bounds__(ORTH_THREADS) lanczos_tridiag_kernel(OrthArgs 
     if (!stop) c.j = j + 1;
     if (a.in_graph) cudaGraphSetConditional(a.loop, stop ? 0u : 1u);
   }
+}
+
+__global__ void __launch_bounds__(ORTH_THREADS) lanczos_tridiag_kernel(OrthArgs a) { tridiag_step(a); }
+
+// One Lanczos step for chi <= 128 as ONE cooperative launch (the graph body):
+// the orthogonalisation on every CTA, one grid barrier, then CTA 0 solves the
+// tridiagonal problem and takes the step decision while the other CTAs run
+// the fused H_eff matvec of q_{j+1} (heff_phases.cuh) with barriers over
+// themselves only.  Replaces orth -> fork(tridiag || heff) -> join: two
+// cooperative launches and the fork/join edges per step.
+struct FusedStepArgs {
+  OrthArgs o;
+  hs::HsArgs h;
+  unsigned* bar;  // arrival counter of the matvec CTAs (reset by CTA 0 each launch)
+};
+
+__device__ __forceinline__ void sub_grid_sync(unsigned* ctr, unsigned n, unsigned& target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    target += n;
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    while (*reinterpret_cast<volatile unsigned*>(ctr) < target) __nanosleep(20);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(ORTH_THREADS) lanczos_step_small_kernel(FusedStepArgs f) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ hs::MixSmem w;
+  cg::grid_group grid = cg::this_grid();
+  orth_step(f.o);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *f.bar = 0u;
+  grid.sync();
+  if (blockIdx.x == 0) {
+    tridiag_step(f.o);
+    return;
+  }
+  double* As = reinterpret_cast<double*>(dyn);
+  double* Bs = As + hs::HS_TM * hs::hs_ld<hs::HS_KMAX>();
+  hs::load_mix(f.h.mix, w);
+  __syncthreads();
+  const int blk = blockIdx.x - 1, nblk = gridDim.x - 1;
+  unsigned target = 0;
+  hs::phase_a<hs::HS_KMAX>(f.h, w, f.h.theta, As, Bs, blk, nblk);
+  sub_grid_sync(f.bar, static_cast<unsigned>(nblk), target);
+  hs::phase_b<hs::HS_KMAX>(f.h, As, Bs, blk, nblk);
+  sub_grid_sync(f.bar, static_cast<unsigned>(nblk), target);
+  hs::phase_c(f.h, f.h.out, blk, nblk);
 }
 
 struct Kernels {
@@ -753,7 +806,7 @@ void device_scale(Ctx& ctx, double* dst, const double* src, long n, const double
 
 EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long dim,
                     const double* v0, double tol, int max_iter, double* out, int graph_slot,
-                    uint64_t graph_key) {
+                    uint64_t graph_key, const HeffOps* small_op) {
   ws.reserve(n);
   Kernels K{ctx, ws, n, red_blocks(ctx, n)};
   double* misc = ws.misc();
@@ -780,8 +833,38 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
   }
   // fixed for a given n: the chunking (and so every reduction order) is deterministic
   // (about one element per thread up to two CTAs per SM: the passes are latency-bound)
+  static const bool use_graph = [] {
+    const char* e = std::getenv("ACHI_LANCZOS_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  // ACHI_LANCZOS_FUSED=1 (opt-in): for chi <= 128 in graph mode the whole step is
+  // one cooperative launch (lanczos_step_small_kernel) over max(orthogonalisation
+  // grid, matvec items + 1) CTAs.  Measured slower on C3 (Lanczos 0.134 vs 0.122
+  // s/sweep at sweep 7): one CTA per SM for the combined kernel and a smaller
+  // matvec grid cost more than the launch and fork/join it saves.
+  static const bool fused_on = [] {
+    const char* e = std::getenv("ACHI_LANCZOS_FUSED");
+    return e && e[0] == '1';
+  }();
+  hs::HsArgs fused_h{};
+  long fused_items = 0;
+  const bool fused = use_graph && fused_on && small_op &&
+                     heff_small_fusable(ctx, *small_op, ws.qcur.p, ws.w.p, &fused_h, &fused_items);
+  static int fused_max = 0;
+  if (fused && fused_max == 0) {
+    const size_t fsm = hs::smem_bytes<hs::HS_KMAX>();
+    ACHI_CUDA(cudaFuncSetAttribute(lanczos_step_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(fsm)));
+    int per_sm = 0;
+    ACHI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lanczos_step_small_kernel,
+                                                            ORTH_THREADS, fsm));
+    fused_max = std::max(1, per_sm) * ctx.num_sms;
+  }
   const int orth_grid =
-      std::max(1, ctx.cap_grid(std::min<long>(cdiv(n, ORTH_THREADS), orth_max)));
+      fused ? std::max(2, ctx.cap_grid(std::min<long>(
+                              std::max<long>(cdiv(n, ORTH_THREADS), fused_items + 1), fused_max)))
+            : std::max(1, ctx.cap_grid(std::min<long>(cdiv(n, ORTH_THREADS), orth_max)));
+  if (fused) ws.bar.reserve(1);
   const size_t need_part = static_cast<size_t>(129) * orth_grid + 64;
   if (ws.partials.cap < need_part) {
     for (auto& g : ws.graphs) g.reset();
@@ -791,10 +874,6 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
   // ---- the inner loop as a graph: WHILE { apply(qcur -> w); orth + decide } ----
   // ACHI_LANCZOS_GRAPH=0 steps the same kernels from the host instead (ncu cannot
   // profile kernel nodes of graphs with conditional nodes).
-  static const bool use_graph = [] {
-    const char* e = std::getenv("ACHI_LANCZOS_GRAPH");
-    return !(e && e[0] == '0');
-  }();
   // ACHI_LANCZOS_PROF=1: clock64 phase split of the fused step, printed every 200 calls
   static const bool prof_on = std::getenv("ACHI_LANCZOS_PROF") != nullptr;
   static DevArr<unsigned long long> prof_buf;
@@ -816,11 +895,14 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
                  prof_h.p[5], prof_h.p[6] / s, orth_grid, prof_h.p[0] / s, prof_h.p[1] / s,
                  prof_h.p[2] / s, prof_h.p[3] / s, prof_h.p[4] / s, prof_h.p[7] / s);
   }
+  auto orth_args = [&](cudaGraphConditionalHandle handle, int in_graph) {
+    return OrthArgs{ws.q(0), ws.stride, ws.w.p, n,
+                    ws.partials.p, ws.partials.p + 64L * orth_grid, ws.partials.p + 128L * orth_grid,
+                    ws.alpha(), ws.beta(), ws.s(), ws.qcur.p, K.dev_status(), ws.ctl.p, handle, in_graph,
+                    prof_on ? prof_buf.p : nullptr};
+  };
   auto launch_orth = [&](cudaGraphConditionalHandle handle, int in_graph) {
-    OrthArgs oa{ws.q(0), ws.stride, ws.w.p, n,
-                ws.partials.p, ws.partials.p + 64L * orth_grid, ws.partials.p + 128L * orth_grid,
-                ws.alpha(), ws.beta(), ws.s(), ws.qcur.p, K.dev_status(), ws.ctl.p, handle, in_graph,
-                prof_on ? prof_buf.p : nullptr};
+    const OrthArgs oa = orth_args(handle, in_graph);
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(orth_grid);
     lc.blockDim = dim3(ORTH_THREADS);
@@ -846,7 +928,8 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
   if (graph_slot >= 0 && static_cast<size_t>(graph_slot) >= ws.graphs.size())
     ws.graphs.resize(static_cast<size_t>(graph_slot) + 1);
   LanczosGraph& lg = graph_slot >= 0 ? ws.graphs[static_cast<size_t>(graph_slot)] : local;
-  const uint64_t key = graph_key ^ (static_cast<uint64_t>(n) << 40) ^ static_cast<uint64_t>(orth_grid);
+  const uint64_t key = graph_key ^ (static_cast<uint64_t>(n) << 40) ^ static_cast<uint64_t>(orth_grid) ^
+                       (fused ? 0x5a5a000000000000ull : 0ull);
   static thread_local long builds = 0, updates = 0;
   static thread_local double build_s = 0.0;
   if (prof_on && prof_calls % 200 == 0)
@@ -876,15 +959,31 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
     ACHI_CUDA(cudaStreamBeginCaptureToGraph(ctx.stream, body, nullptr, nullptr, 0,
                                             cudaStreamCaptureModeRelaxed));
     try {
-      // orthogonalise step j; then the tridiagonal/decision kernel on the aux
-      // stream runs concurrently with the (speculative) matvec of q_{j+1}
-      const OrthArgs oa = launch_orth(handle, 1);
-      ACHI_CUDA(cudaEventRecord(ctx.ev_fork, ctx.stream));
-      ACHI_CUDA(cudaStreamWaitEvent(ctx.aux, ctx.ev_fork, 0));
-      launch_tridiag(oa, ctx.aux);
-      ACHI_CUDA(cudaEventRecord(ctx.ev_join, ctx.aux));
-      apply(ws.qcur.p, ws.w.p);
-      ACHI_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_join, 0));
+      if (fused) {
+        FusedStepArgs fa{orth_args(handle, 1), fused_h, ws.bar.p};
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(orth_grid);
+        lc.blockDim = dim3(ORTH_THREADS);
+        lc.dynamicSmemBytes = hs::smem_bytes<hs::HS_KMAX>();
+        lc.stream = ctx.stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        ACHI_CUDA(cudaLaunchKernelEx(&lc, lanczos_step_small_kernel, fa));
+        ACHI_LAUNCHED(ctx);
+      } else {
+        // orthogonalise step j; then the tridiagonal/decision kernel on the aux
+        // stream runs concurrently with the (speculative) matvec of q_{j+1}
+        const OrthArgs oa = launch_orth(handle, 1);
+        ACHI_CUDA(cudaEventRecord(ctx.ev_fork, ctx.stream));
+        ACHI_CUDA(cudaStreamWaitEvent(ctx.aux, ctx.ev_fork, 0));
+        launch_tridiag(oa, ctx.aux);
+        ACHI_CUDA(cudaEventRecord(ctx.ev_join, ctx.aux));
+        apply(ws.qcur.p, ws.w.p);
+        ACHI_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_join, 0));
+      }
     } catch (...) {
       cudaGraph_t dummy;
       cudaStreamEndCapture(ctx.stream, &dummy);

@@ -12,6 +12,10 @@
 #include "common.cuh"
 
 namespace achi {
+struct HeffOps;  // contract.cuh
+}
+
+namespace achi {
 
 constexpr int LANCZOS_BLOCK = 48;  // linalg.cpp:113
 
@@ -44,6 +48,7 @@ struct LanczosWs {
   DevBuf partials;
   DevBuf scal;    // alpha[64] beta[64] h1[64] h2[64] s[64] misc[64]
   DevArr<LanczosCtl> ctl;
+  DevArr<unsigned> bar;  // sub-grid barrier counter of the fused small-chi step
   PinnedArr<LanczosCtl> ctl_h;
   std::vector<LanczosGraph> graphs;
   long stride = 0;
@@ -81,7 +86,8 @@ using ApplyFn = std::function<void(const double* in, double* out)>;
 // whenever apply's kernels, shapes or buffers do); -1 builds a one-off graph.
 EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long dim,
                     const double* v0, double tol, int max_iter, double* out,
-                    int graph_slot = -1, uint64_t graph_key = 0);
+                    int graph_slot = -1, uint64_t graph_key = 0,
+                    const HeffOps* small_op = nullptr);
 
 // Deterministic device reductions used across the hot path.
 // sum_i x_i^2 -> *result (device)
