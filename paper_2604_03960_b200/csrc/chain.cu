@@ -438,6 +438,10 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
     vk.valid = true;
   }
   c.acc.end(c.stream, 0.0);
+  // the fused bond selection is queued behind the SVD; one host sync serves both
+  bond_select(c, sr.sigma, sr.r_true, cfg, states.p, b, sweep_index, right ? 1 : 0,
+              trace.p + slot, visits.p + slot, bout.p);
+  ACHI_CUDA(cudaMemcpyAsync(bout_h.p, bout.p, sizeof(BondOut), cudaMemcpyDeviceToHost, c.stream));
   c.sync();
   c.acc.resolve();
   auto write_dump = [&] {
@@ -475,10 +479,6 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
                    "(%d Jacobi sweeps, warm %d)\n", sweep_index, b, right ? "R" : "L", chl, chr,
                    lz_ms, svd_ms, svd_sweeps, warm ? 1 : 0);
   }
-  bond_select(c, sr.sigma, sr.r_true, cfg, states.p, b, sweep_index, right ? 1 : 0,
-              trace.p + slot, visits.p + slot, bout.p);
-  ACHI_CUDA(cudaMemcpyAsync(bout_h.p, bout.p, sizeof(BondOut), cudaMemcpyDeviceToHost, c.stream));
-  c.sync();
   const BondOut bo = *bout_h.p;
   const auto t3 = clk::now();
   if (bo.err == ACHI_E_DEGENERATE_SPECTRUM) fail(bo.err, "dmrg: zero two-site block");
