@@ -426,14 +426,6 @@ __global__ void __launch_bounds__(JT, 1) jacobi_cluster_kernel(ClArgs a) {
       const bool rot = finish_gram(sm, acc, z2, ig2, a.tol, a.max_inner, cross, a.skip_tol);
       const long long t2 = prof ? clock64() : 0;
       if (threadIdx.x == 0) meas_slot[sweep % 3] = fmax(meas_slot[sweep % 3], sm.red2[0]);
-      if (a.jrec) {
-        const long slot = (b * a.jstride + rg) * a.npairs + p;
-        if (threadIdx.x == 0) a.jflag[slot] = rot ? 1 : 0;
-        if (rot) {
-          double* jr = a.jrec + slot * (JW * JW);
-          for (int idx = threadIdx.x; idx < JW * JW; idx += JT) jr[idx] = sm.J[idx / JW][idx % JW];
-        }
-      }
       // next-round owners of blocks ba (slot a) and bb (slot b)
       const int rn = r + 1 < rounds ? r + 1 : 0;
       int pa, sa, pb, sb;
@@ -446,13 +438,24 @@ __global__ void __launch_bounds__(JT, 1) jacobi_cluster_kernel(ClArgs a) {
       rotate_resident(X, cld, a.rows_pad, sm, rot, dst_a, dst_b);
       const long long t4 = prof ? clock64() : 0;
       buf ^= 1;
-      cl.sync();
+      // split cluster barrier: the rotation record goes to global memory while
+      // the other CTAs finish their stores (J is only rewritten next round)
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      if (a.jrec) {
+        const long slot = (b * a.jstride + rg) * a.npairs + p;
+        if (threadIdx.x == 0) a.jflag[slot] = rot ? 1 : 0;
+        if (rot) {
+          double* jr = a.jrec + slot * (JW * JW);
+          for (int idx = threadIdx.x; idx < JW * JW; idx += JT) jr[idx] = sm.J[idx / JW][idx % JW];
+        }
+      }
+      asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
       if (prof) {
         a.prof[0] += t1 - t0;           // gram
         a.prof[1] += t2 - t1;           // measure + inner Jacobi
-        a.prof[2] += t3 - t2;           // J record
+        a.prof[2] += t3 - t2;           // next-owner lookup
         a.prof[3] += t4 - t3;           // rotate + remote store
-        a.prof[4] += clock64() - t4;    // cluster barrier
+        a.prof[4] += clock64() - t4;    // J record + cluster barrier
         a.prof[5] += 1;
         a.prof[6] += rot ? 1 : 0;
       }
