@@ -588,6 +588,9 @@ struct PersArgs {
   const double* zero2;
   unsigned long long* conv;  // [MAX_SWEEPS] per-sweep max measure (whole launch)
   int* sweeps_out;
+  int rsplit;                // CTAs per block pair, each streaming a slice of the rows
+  double* gpart;             // [pairs in launch][rsplit][32*32] partial Grams (rsplit > 1)
+  unsigned* pcnt;            // [pairs in launch] arrival counters (zeroed per launch)
 };
 
 // cp.async chunk loads: rows [r0, r0+64) of the 32 pair columns -> X[col][row]
@@ -659,24 +662,34 @@ __device__ __forceinline__ void rotate_chunk(Chunk& X, const Small& sm) {
 // bandwidth-bound and need the memory-level parallelism)
 constexpr int STREAM_STAGES = 4;
 
-__device__ void stream_rotate(Chunk* X, double* M, long ld, int rows, int ca, int cb, const Small& sm) {
-  const int nch = (rows + JCH - 1) / JCH;
+// rotate chunks [k0, k1) of the pair columns of M (rows x ..., ld) by sm.J
+__device__ void stream_rotate(Chunk* X, double* M, long ld, int rows, int k0, int k1, int ca, int cb,
+                              const Small& sm) {
   for (int k = 0; k < STREAM_STAGES - 1; ++k) {
-    if (k < nch) load_chunk_async(X[k], M, ld, rows, k * JCH, ca, cb);
+    if (k0 + k < k1) load_chunk_async(X[k], M, ld, rows, (k0 + k) * JCH, ca, cb);
     cp_commit();
   }
-  for (int k = 0; k < nch; ++k) {
+  for (int k = 0; k < k1 - k0; ++k) {
     const int kn = k + STREAM_STAGES - 1;
-    if (kn < nch) load_chunk_async(X[kn % STREAM_STAGES], M, ld, rows, kn * JCH, ca, cb);
+    if (k0 + kn < k1) load_chunk_async(X[kn % STREAM_STAGES], M, ld, rows, (k0 + kn) * JCH, ca, cb);
     cp_commit();
     cp_wait<STREAM_STAGES - 1>();
     __syncthreads();
     rotate_chunk(X[k % STREAM_STAGES], sm);
-    store_chunk(X[k % STREAM_STAGES], M, ld, rows, k * JCH, ca, cb);
+    store_chunk(X[k % STREAM_STAGES], M, ld, rows, (k0 + k) * JCH, ca, cb);
     __syncthreads();
   }
 }
 
+// One cooperative launch for the whole iteration.  Each block pair is owned by
+// rsplit CTAs (adjacent blockIdx), CTA h streaming the h-th slice of the row
+// chunks of G and of V: the rows of a block pair are independent under the
+// rotation, only the 32x32 Gram couples them.  The CTAs of a pair publish
+// their partial Grams to global memory, wait for each other on a per-pair
+// arrival counter (co-resident: cooperative launch) and sum the partials in
+// the same fixed order, so every CTA of the pair derives bit-identical
+// rotations.  Splitting the rows puts 2-8x more CTAs (and bytes in flight) on
+// a matrix that has fewer block pairs than the GPU has SMs.
 __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
   extern __shared__ __align__(16) unsigned char dyn[];
   Chunk* X = reinterpret_cast<Chunk*>(dyn);
@@ -684,11 +697,17 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
   init_pair_tables(sm);
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
-  const int p = blockIdx.x % a.npairs, b = a.batch0 + blockIdx.x / a.npairs;
+  const int R = a.rsplit;
+  const int h = blockIdx.x % R, pl = blockIdx.x / R;  // pl: pair index within the launch
+  const int p = pl % a.npairs, b = a.batch0 + pl / a.npairs;
   double* G = a.G + b * a.gstride;
   double* V = a.V ? a.V + b * a.vstride : nullptr;
   const double z2 = a.zero2[2 * b], ig2 = a.zero2[2 * b + 1];
-  const int nch = (a.mg + JCH - 1) / JCH;
+  const int nch = (a.mg + JCH - 1) / JCH, nchv = (a.vrows + JCH - 1) / JCH;
+  const int g0 = h * nch / R, g1 = (h + 1) * nch / R;
+  const int v0 = h * nchv / R, v1 = (h + 1) * nchv / R;
+  double* mypart = R > 1 ? a.gpart + (static_cast<long>(pl) * R + h) * (JW * JW) : nullptr;
+  unsigned gen = 0;
   int sweep = 0;
   for (; sweep < MAX_SWEEPS; ++sweep) {
     for (int round = 0; round < a.nb - 1; ++round) {
@@ -697,24 +716,45 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
       const int ca = ba * JB, cb = bb * JB;
       double acc[4] = {0, 0, 0, 0};
       for (int k = 0; k < STREAM_STAGES - 1; ++k) {
-        if (k < nch) load_chunk_async(X[k], G, a.ldg, a.mg, k * JCH, ca, cb);
+        if (g0 + k < g1) load_chunk_async(X[k], G, a.ldg, a.mg, (g0 + k) * JCH, ca, cb);
         cp_commit();
       }
-      for (int k = 0; k < nch; ++k) {
+      for (int k = 0; k < g1 - g0; ++k) {
         const int kn = k + STREAM_STAGES - 1;
-        if (kn < nch) load_chunk_async(X[kn % STREAM_STAGES], G, a.ldg, a.mg, kn * JCH, ca, cb);
+        if (g0 + kn < g1) load_chunk_async(X[kn % STREAM_STAGES], G, a.ldg, a.mg, (g0 + kn) * JCH, ca, cb);
         cp_commit();
         cp_wait<STREAM_STAGES - 1>();
         __syncthreads();
         gram_chunk(X[k % STREAM_STAGES], acc);
         __syncthreads();
       }
+      if (R > 1) {
+        // publish the partial Gram, wait for the pair's other CTAs, fixed-order sum
+#pragma unroll
+        for (int i = 0; i < 4; ++i) __stcg(mypart + i * JT + threadIdx.x, acc[i]);
+        __threadfence();
+        __syncthreads();
+        ++gen;
+        if (threadIdx.x == 0) {
+          atomicAdd(&a.pcnt[pl], 1u);
+          while (*reinterpret_cast<volatile unsigned*>(&a.pcnt[pl]) < gen * R) __nanosleep(32);
+          __threadfence();
+        }
+        __syncthreads();
+        const double* base = a.gpart + static_cast<long>(pl) * R * (JW * JW);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double t = __ldcg(base + i * JT + threadIdx.x);
+          for (int q = 1; q < R; ++q) t += __ldcg(base + q * (JW * JW) + i * JT + threadIdx.x);
+          acc[i] = t;
+        }
+      }
       const bool rot = finish_gram(sm, acc, z2, ig2, a.tol, a.max_inner);
-      if (threadIdx.x == 0)
+      if (threadIdx.x == 0 && h == 0)
         atomicMax(&a.conv[sweep], static_cast<unsigned long long>(__double_as_longlong(sm.red2[0])));
       if (rot) {
-        stream_rotate(X, G, a.ldg, a.mg, ca, cb, sm);
-        if (V) stream_rotate(X, V, a.ldv, a.vrows, ca, cb, sm);
+        stream_rotate(X, G, a.ldg, a.mg, g0, g1, ca, cb, sm);
+        if (V) stream_rotate(X, V, a.ldv, a.vrows, v0, v1, ca, cb, sm);
       }
       grid.sync();
     }
@@ -1117,13 +1157,40 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     }
     if (npairs > mb) fail(ACHI_E_SIZE_GUARD, "svd: matrix too wide for one cooperative launch");
     const int per_launch = std::max(1, mb / npairs);
-    for (int b0 = 0; b0 < batch; b0 += per_launch, ++launches) {
-      const int nbat = std::min(per_launch, batch - b0);
+    // row split: the largest power of two (<= 8) that still fits the launch's
+    // block pairs on the resident CTAs and leaves every CTA >= 4 row chunks
+    // (ACHI_SVD_RSPLIT forces a value for studies)
+    static const int rs_env = [] {
+      const char* e = std::getenv("ACHI_SVD_RSPLIT");
+      return e ? std::max(1, std::atoi(e)) : 0;
+    }();
+    const int pairs0 = npairs * std::min(per_launch, batch);
+    int rsplit = 1;
+    if (rs_env) {
+      rsplit = rs_env;
+    } else {
+      const int nch = static_cast<int>(cdiv(mg, JCH));
+      while (rsplit < 8 && pairs0 * rsplit * 2 <= mb && nch / (rsplit * 2) >= 4) rsplit *= 2;
+    }
+    if (npairs * rsplit > mb) fail(ACHI_E_SIZE_GUARD, "svd: row split exceeds the resident CTAs");
+    const int per_launch_r = std::max(1, mb / (npairs * rsplit));
+    double* gpart = nullptr;
+    unsigned* pcnt = nullptr;
+    if (rsplit > 1) {
+      const int pairs_max = npairs * std::min(per_launch_r, batch);
+      gpart = ws.gpart.reserve(static_cast<size_t>(pairs_max) * rsplit * JW * JW);
+      pcnt = ws.pcnt.reserve(static_cast<size_t>(pairs_max));
+    }
+    for (int b0 = 0; b0 < batch; b0 += per_launch_r, ++launches) {
+      const int nbat = std::min(per_launch_r, batch - b0);
       ACHI_CUDA(cudaMemsetAsync(conv, 0, sizeof(unsigned long long) * MAX_SWEEPS, ctx.stream));
+      if (pcnt) ACHI_CUDA(cudaMemsetAsync(pcnt, 0, sizeof(unsigned) * npairs * nbat, ctx.stream));
       PersArgs a{G, ldg, gstride, mg, V, ng, vstride, ng, nb, npairs, b0,
-                 max_inner, tol, stop_tol, zero2, conv, sweeps_dev + (launches % nsw)};
+                 max_inner, tol, stop_tol, zero2, conv, sweeps_dev + (launches % nsw),
+                 rsplit, gpart, pcnt};
       void* args[] = {&a};
-      ACHI_CUDA(cudaLaunchCooperativeKernel(kern, dim3(npairs * nbat), dim3(JT), args, smem, ctx.stream));
+      ACHI_CUDA(cudaLaunchCooperativeKernel(kern, dim3(npairs * nbat * rsplit), dim3(JT), args, smem,
+                                            ctx.stream));
       ACHI_LAUNCHED(ctx);
     }
     launches = std::min(launches, nsw);

@@ -22,6 +22,8 @@ struct SvdWs {
   DevArr<int> perm;
   DevArr<double> sign;
   DevArr<unsigned long long> conv;
+  DevArr<double> gpart;         // stream mode, row split: partial Grams
+  DevArr<unsigned> pcnt;        // stream mode, row split: per-pair arrival counters
   DevArr<int> sweeps;
   PinnedArr<int> sweeps_host;
 };
