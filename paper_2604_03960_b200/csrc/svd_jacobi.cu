@@ -1170,7 +1170,8 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
       rsplit = rs_env;
     } else {
       const int nch = static_cast<int>(cdiv(mg, JCH));
-      while (rsplit < 8 && pairs0 * rsplit * 2 <= mb && nch / (rsplit * 2) >= 4) rsplit *= 2;
+      const int room = ctx.cap_grid(mb);  // a context sharing the GPU keeps to its share
+      while (rsplit < 8 && pairs0 * rsplit * 2 <= room && nch / (rsplit * 2) >= 4) rsplit *= 2;
     }
     if (npairs * rsplit > mb) fail(ACHI_E_SIZE_GUARD, "svd: row split exceeds the resident CTAs");
     const int per_launch_r = std::max(1, mb / (npairs * rsplit));
