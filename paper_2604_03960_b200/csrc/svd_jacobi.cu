@@ -591,6 +591,7 @@ struct PersArgs {
   int rsplit;                // CTAs per block pair, each streaming a slice of the rows
   double* gpart;             // [pairs in launch][rsplit][32*32] partial Grams (rsplit > 1)
   unsigned* pcnt;            // [pairs in launch] arrival counters (zeroed per launch)
+  int cross_mode;            // 4: two of every three rounds sweep only the cross-block pairs
 };
 
 // cp.async chunk loads: rows [r0, r0+64) of the 32 pair columns -> X[col][row]
@@ -609,10 +610,17 @@ __device__ __forceinline__ void load_chunk_async(Chunk& X, const double* M, long
 
 __device__ __forceinline__ void store_chunk(const Chunk& X, double* M, long ld, int rows, int r0,
                                             int ca, int cb) {
-  for (int idx = threadIdx.x; idx < JW * JCH; idx += JT) {
-    const int c = idx / JCH, r = idx - c * JCH;
+#pragma unroll
+  for (int it = 0; it < JW * JCH / 2 / JT; ++it) {
+    const int idx = threadIdx.x + it * JT;
+    const int c = idx / (JCH / 2), r = 2 * (idx - c * (JCH / 2));
     const int col = c < JB ? ca + c : cb + c - JB;
-    if (r0 + r < rows) M[col * ld + r0 + r] = X[c][r];
+    const double2 v = *reinterpret_cast<const double2*>(&X[c][r]);
+    double* dst = M + col * ld + r0 + r;
+    if (r0 + r + 1 < rows)
+      *reinterpret_cast<double2*>(dst) = v;
+    else if (r0 + r < rows)
+      dst[0] = v.x;
   }
 }
 
@@ -749,7 +757,8 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
           acc[i] = t;
         }
       }
-      const bool rot = finish_gram(sm, acc, z2, ig2, a.tol, a.max_inner);
+      const bool cross = a.cross_mode == 4 && (round % 3) != 0;
+      const bool rot = finish_gram(sm, acc, z2, ig2, a.tol, a.max_inner, cross);
       if (threadIdx.x == 0 && h == 0)
         atomicMax(&a.conv[sweep], static_cast<unsigned long long>(__double_as_longlong(sm.red2[0])));
       if (rot) {
@@ -1156,6 +1165,10 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
       if (mb < 1) fail(ACHI_E_CUDA, "svd: Jacobi kernel cannot be resident");
     }
     if (npairs > mb) fail(ACHI_E_SIZE_GUARD, "svd: matrix too wide for one cooperative launch");
+    static const int stream_cross = [] {  // ACHI_JACOBI_CROSS_STREAM: inner schedule (0 full, 4 cross)
+      const char* e = std::getenv("ACHI_JACOBI_CROSS_STREAM");
+      return e ? std::atoi(e) : 4;
+    }();
     const int per_launch = std::max(1, mb / npairs);
     // row split: the largest power of two (<= 8) that still fits the launch's
     // block pairs on the resident CTAs and leaves every CTA >= 4 row chunks
@@ -1188,7 +1201,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
       if (pcnt) ACHI_CUDA(cudaMemsetAsync(pcnt, 0, sizeof(unsigned) * npairs * nbat, ctx.stream));
       PersArgs a{G, ldg, gstride, mg, V, ng, vstride, ng, nb, npairs, b0,
                  max_inner, tol, stop_tol, zero2, conv, sweeps_dev + (launches % nsw),
-                 rsplit, gpart, pcnt};
+                 rsplit, gpart, pcnt, stream_cross};
       void* args[] = {&a};
       ACHI_CUDA(cudaLaunchCooperativeKernel(kern, dim3(npairs * nbat * rsplit), dim3(JT), args, smem,
                                             ctx.stream));
