@@ -671,20 +671,46 @@ __device__ __forceinline__ void rotate_chunk(Chunk& X, const Small& sm) {
 constexpr int STREAM_STAGES = 4;
 
 // rotate chunks [k0, k1) of the pair columns of M (rows x ..., ld) by sm.J
-__device__ void stream_rotate(Chunk* X, double* M, long ld, int rows, int k0, int k1, int ca, int cb,
-                              const Small& sm) {
-  for (int k = 0; k < STREAM_STAGES - 1; ++k) {
-    if (k0 + k < k1) load_chunk_async(X[k], M, ld, rows, (k0 + k) * JCH, ca, cb);
-    cp_commit();
+// The rotation of a round is one pipeline over the CTA's chunks of G and then
+// of V (chunk t < nG: G, else V), so V's first loads overlap G's last
+// rotations; its first STREAM_STAGES - 1 loads are issued before the inner
+// Jacobi (stream_rotate_prefetch) and overlap it.
+struct RotSeg {
+  double* G;
+  long ldg;
+  int mg, g0, nG;
+  double* V;
+  long ldv;
+  int vrows, v0, nV;
+};
+__device__ __forceinline__ void rot_chunk_io(const RotSeg& s, int t, double*& M, long& ld, int& rows, int& r0) {
+  if (t < s.nG) {
+    M = s.G; ld = s.ldg; rows = s.mg; r0 = (s.g0 + t) * JCH;
+  } else {
+    M = s.V; ld = s.ldv; rows = s.vrows; r0 = (s.v0 + t - s.nG) * JCH;
   }
-  for (int k = 0; k < k1 - k0; ++k) {
-    const int kn = k + STREAM_STAGES - 1;
-    if (k0 + kn < k1) load_chunk_async(X[kn % STREAM_STAGES], M, ld, rows, (k0 + kn) * JCH, ca, cb);
-    cp_commit();
+}
+__device__ __forceinline__ void rot_load(Chunk* X, const RotSeg& s, int t, int ca, int cb) {
+  if (t < s.nG + s.nV) {
+    double* M; long ld; int rows, r0;
+    rot_chunk_io(s, t, M, ld, rows, r0);
+    load_chunk_async(X[t % STREAM_STAGES], M, ld, rows, r0, ca, cb);
+  }
+  cp_commit();
+}
+__device__ void stream_rotate_prefetch(Chunk* X, const RotSeg& s, int ca, int cb) {
+  for (int k = 0; k < STREAM_STAGES - 1; ++k) rot_load(X, s, k, ca, cb);
+}
+__device__ void stream_rotate(Chunk* X, const RotSeg& s, int ca, int cb, const Small& sm) {
+  const int n = s.nG + s.nV;
+  for (int k = 0; k < n; ++k) {
+    rot_load(X, s, k + STREAM_STAGES - 1, ca, cb);
     cp_wait<STREAM_STAGES - 1>();
     __syncthreads();
     rotate_chunk(X[k % STREAM_STAGES], sm);
-    store_chunk(X[k % STREAM_STAGES], M, ld, rows, (k0 + k) * JCH, ca, cb);
+    double* M; long ld; int rows, r0;
+    rot_chunk_io(s, k, M, ld, rows, r0);
+    store_chunk(X[k % STREAM_STAGES], M, ld, rows, r0, ca, cb);
     __syncthreads();
   }
 }
@@ -757,13 +783,17 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
           acc[i] = t;
         }
       }
+      const RotSeg seg{G, a.ldg, a.mg, g0, g1 - g0, V, a.ldv, a.vrows, v0, V ? v1 - v0 : 0};
+      stream_rotate_prefetch(X, seg, ca, cb);  // lands during the inner Jacobi
       const bool cross = a.cross_mode == 4 && (round % 3) != 0;
       const bool rot = finish_gram(sm, acc, z2, ig2, a.tol, a.max_inner, cross);
       if (threadIdx.x == 0 && h == 0)
         atomicMax(&a.conv[sweep], static_cast<unsigned long long>(__double_as_longlong(sm.red2[0])));
       if (rot) {
-        stream_rotate(X, G, a.ldg, a.mg, g0, g1, ca, cb, sm);
-        if (V) stream_rotate(X, V, a.ldv, a.vrows, v0, v1, ca, cb, sm);
+        stream_rotate(X, seg, ca, cb, sm);
+      } else {
+        cp_wait<0>();  // drain the unused prefetch before the buffers are reused
+        __syncthreads();
       }
       grid.sync();
     }
