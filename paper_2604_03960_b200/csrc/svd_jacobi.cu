@@ -1201,7 +1201,8 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     }();
     const int per_launch = std::max(1, mb / npairs);
     // row split: the largest power of two (<= 8) that still fits the launch's
-    // block pairs on the resident CTAs and leaves every CTA >= 4 row chunks
+    // block pairs on the resident CTAs and leaves every CTA >= 4 row chunks, or
+    // >= 1 chunk while the CTAs still fit one per SM
     // (ACHI_SVD_RSPLIT forces a value for studies)
     static const int rs_env = [] {
       const char* e = std::getenv("ACHI_SVD_RSPLIT");
@@ -1214,7 +1215,13 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     } else {
       const int nch = static_cast<int>(cdiv(mg, JCH));
       const int room = ctx.cap_grid(mb);  // a context sharing the GPU keeps to its share
-      while (rsplit < 8 && pairs0 * rsplit * 2 <= room && nch / (rsplit * 2) >= 4) rsplit *= 2;
+      // (measured: 512^2 best at R=8 with one chunk per CTA on 128 SMs; 1024^2 at R=4,
+      // not R=8 on 256 CTAs; 2048^2 R=4 and 4096^2 R=2 on 256 CTAs)
+      auto more = [&](int r2) {
+        const int ctas = pairs0 * r2, per = nch / r2;
+        return ctas <= room && per >= 1 && (per >= 4 || ctas <= ctx.num_sms);
+      };
+      while (rsplit < 8 && more(rsplit * 2)) rsplit *= 2;
     }
     if (npairs * rsplit > mb) fail(ACHI_E_SIZE_GUARD, "svd: row split exceeds the resident CTAs");
     const int per_launch_r = std::max(1, mb / (npairs * rsplit));
