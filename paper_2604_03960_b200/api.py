@@ -145,12 +145,21 @@ class Context:
                                                    _dp(W), _dp(out)))
         return out
 
-    def svd_full(self, a):
-        """linalg.cpp:67-70 on the GPU Jacobi kernel: returns (u, sigma, vt, sweeps)."""
+    def svd_full(self, a, out=None):
+        """linalg.cpp:67-70 on the GPU Jacobi kernel: returns (u, sigma, vt, sweeps).
+
+        out: optional caller-owned (u, sigma, vt) C-contiguous float64 arrays of
+        shapes (m, k), (k,), (k, n) (e.g. pinned host memory) written in place."""
         a = _f64(a)
         m, n = a.shape
         k = min(m, n)
-        s, u, vt = np.zeros(k), np.zeros((m, k)), np.zeros((k, n))
+        if out is None:
+            s, u, vt = np.zeros(k), np.zeros((m, k)), np.zeros((k, n))
+        else:
+            u, s, vt = out
+            for arr, shp in ((u, (m, k)), (s, (k,)), (vt, (k, n))):
+                if arr.dtype != np.float64 or arr.shape != shp or not arr.flags.c_contiguous:
+                    raise ValueError(f"svd_full: out array must be C-contiguous float64 {shp}")
         sw = C.c_int()
         self._check(self.lib.achi_svd(self.h, m, n, _dp(a), _dp(s), _dp(u), _dp(vt), C.byref(sw)))
         return u, s, vt, sw.value

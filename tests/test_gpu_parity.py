@@ -146,6 +146,20 @@ def test_svd_known_answers(ctx):  # test_linalg.cpp:38-55
         ctx.svd_full(bad)
 
 
+def test_svd_full_into_caller_buffers(ctx):
+    """svd_full(out=...) writes the same factors into caller-owned (pinned) host arrays."""
+    import torch
+    a = np.random.default_rng(5).standard_normal((40, 24))
+    pin = lambda *s: torch.zeros(*s, dtype=torch.float64, pin_memory=True).numpy()  # noqa: E731
+    out = (pin(40, 24), pin(24), pin(24, 24))
+    u, s, vt, _ = ctx.svd_full(a)
+    _, _, _, sw = ctx.svd_full(a, out=out)
+    assert sw > 0
+    assert np.array_equal(out[0], u) and np.array_equal(out[1], s) and np.array_equal(out[2], vt)
+    with pytest.raises(ValueError):
+        ctx.svd_full(a, out=(np.zeros((24, 40)), out[1], out[2]))
+
+
 def test_svd_batched(ctx, oracle):
     rng = np.random.default_rng(11)
     for shape in ((4, 128, 128), (3, 256, 200), (2, 300, 300)):
