@@ -68,12 +68,14 @@ class Dist:
             self.dist.destroy_process_group()
 
 
-def run_workers(units, inflight, work, device_index, grid_share=False):
+def run_workers(units, inflight, work, device_index, grid_share=False, warmup=None):
     """Run work(ctx, unit) for `units` on `inflight` host threads, each with its own
     context (stream).  With grid_share, each context's cooperative kernels are capped
     at its share of the GPU (2 CTAs per SM / inflight); measured slower than letting
     the chains' kernels interleave uncapped (profiles/ensemble_r01b.txt), so off by
-    default.  Returns ({unit: record}, max device seconds over workers)."""
+    default.  warmup(ctx), when given, runs once per worker before the timed region
+    (first-call module loads and workspace growth of a fresh context).
+    Returns ({unit: record}, max device seconds over workers)."""
     from .api import Context
     queue = list(units)
     nthreads = max(1, min(inflight, len(queue)))
@@ -91,6 +93,8 @@ def run_workers(units, inflight, work, device_index, grid_share=False):
             ctx = Context(device_index)
             if grid_share and nthreads > 1:
                 ctx.set_grid_cap(max(8, 2 * sms // nthreads))
+            if warmup is not None:
+                warmup(ctx)
             start.wait()
             ctx.timer_start()
             while True:
@@ -160,7 +164,9 @@ def job_c2(args, dist):
         return [float(s[0]), float(s[-1]), abs(float((s * s).sum()) - fro) / fro, sweeps]
 
     dist.barrier()
-    res, secs = run_workers(mine, args.inflight, work, dist.local, args.grid_share)
+    # one untimed SVD of the same shape per worker context (first-call costs)
+    warm = (lambda ctx: work(ctx, mine[0])) if mine else None
+    res, secs = run_workers(mine, args.inflight, work, dist.local, args.grid_share, warm)
     job_s = dist.max(secs)
     out = gather_records_from(res, 4, args.batch, plan, dist)
     return job_s, out, {"unit": "SVDs/s", "units": args.batch,
