@@ -74,32 +74,21 @@ def workload(max_sweeps):
 
 # ---------------------------------------------------------------- distributed
 class Dist:
+    """One process per GPU (torchrun env), NCCL process group for N > 1."""
+
     def __init__(self):
-        self.world = int(os.environ.get("WORLD_SIZE", "1"))
-        self.rank = int(os.environ.get("RANK", "0"))
-        self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        self.pg = None
-        if self.world > 1:
-            import torch
-            import torch.distributed as dist
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl")
-            self.dist, self.torch = dist, torch
+        from paper_2604_03960_b200.ensemble_run import Dist as EDist
+        self.e = EDist()
+        self.world, self.rank, self.local = self.e.world, self.e.rank, self.e.local
 
     def barrier(self):
-        if self.world > 1:
-            self.dist.barrier()
+        self.e.barrier()
 
     def max(self, x):
-        if self.world == 1:
-            return x
-        t = self.torch.tensor([float(x)], device="cuda")
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
-        return float(t.item())
+        return self.e.max(float(x))
 
     def close(self):
-        if self.world > 1:
-            self.dist.destroy_process_group()
+        self.e.close()
 
 
 # ---------------------------------------------------------------- clocks
@@ -165,6 +154,63 @@ def visit_cost_model(visits, chi_profile):
         env = 4.0 * 5 * 2 * max(chl, chr_) * v.kept * (max(chl, chr_) + v.kept)
         cost.append(v.matvecs * mv_flops(chl, chr_) + svd + env)
     return np.array(cost)
+
+
+def host_info():
+    """nproc and the CPU model of the host the CPU legs ran on."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "threads_usable": cpu_threads(), "cpu_model": model}
+
+
+def cpu_svd_timings(n, threads_all, reps_all=3, budget_s=240.0):
+    """The reference's svd_full (linalg.cpp:67-70: thin SVD, U, sigma, V^T, then
+    fix_phases) timed on the oracle (LAPACK gesdd, bundled OpenBLAS), as
+    cmd_svd_bench does it (bench.cpp:635-668: random Gaussian n x n, complex as
+    the reference literal, upper median of the repetitions), in complex128 and in
+    real FP64, on all host threads and on one thread.  The one-thread legs run a
+    single repetition each and are skipped (reported as null) once the budget is
+    spent."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(1234)
+    a_r = rng.standard_normal((n, n))
+    a_c = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    t_start = time.perf_counter()
+    out = {}
+
+    def timed(kind, threads, reps):
+        O.set_threads(threads)
+        runs = []
+        for _ in range(reps):
+            t = time.perf_counter()
+            if kind == "c128":
+                O.svd_complex_sigma(a_c)
+            else:
+                O.svd(a_r)
+            runs.append(time.perf_counter() - t)
+        runs.sort()
+        return round(runs[len(runs) // 2] * 1e3, 1)
+
+    for kind in ("f64", "c128"):
+        out[f"{kind}_{threads_all}t_ms"] = timed(kind, threads_all, reps_all)
+    for kind in ("f64", "c128"):
+        if time.perf_counter() - t_start > budget_s:
+            out[f"{kind}_1t_ms"] = None
+            continue
+        out[f"{kind}_1t_ms"] = timed(kind, 1, 1)
+    O.set_threads(threads_all)
+    out["note"] = (f"oracle svd_full (gesdd + fix_phases) on a random {n}x{n} matrix; "
+                   f"{threads_all} threads: upper median of {reps_all}; 1 thread: one run "
+                   f"(null: skipped, {budget_s:.0f} s budget)")
+    out["seconds_spent"] = round(time.perf_counter() - t_start, 1)
+    return out
 
 
 def cpu_threads():
@@ -261,28 +307,118 @@ def run_ours(args, dist):
     if not args.skip_svd:
         log("svd part")
         out.update(svd_part(ctx, args))
-    # K1 at the large-chi end of the metric's range (chi_max = 1024): device-resident H_eff
+    # K1 at the large-chi end of the metric's range (chi_max = 1024), measured inside a
+    # real sweep: N=100, fixed chi=1024 (every bond 10..89 at chi=1024 from sweep 5 on)
+    if not args.skip_heff_insweep:
+        log("heff in-sweep (N=100, fixed chi=1024)")
+        out["roofline_heff_chi1024"] = heff_insweep(ctx, args)
     from paper_2604_03960_b200.api import heff_bench
     ms, tf = heff_bench(ctx, 1024, 10)
-    out["roofline_heff_chi1024"] = {
-        "bound": "tensor", "kernel": "H_eff matvec (dmma_gemm_kernel x2 + mpo_mix_kernel)",
-        "achieved": round(tf, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-        "frac": round(tf / FP64_PEAK_TFLOPS, 4), "ms_per_matvec": round(ms, 4),
-        "work_def": "2*D*d^2*chi^2*(2*chi)+4*D^2*d^3*chi^2 flops, chi=1024, D=5, d=2",
-        "peak_source": "measured DMMA peak (profiles/fp64_peak_r01.txt)"}
+    out["heff_chi1024_microbench"] = {
+        "achieved": round(tf, 3), "unit": "TFLOP/s", "frac": round(tf / FP64_PEAK_TFLOPS, 4),
+        "ms_per_matvec": round(ms, 4),
+        "note": "achi_heff_bench: random chi=1024 operands, device-resident, 10 matvecs"}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         log("cpu baseline")
         out["cpu_baseline"] = cpu_baseline_sample(spec, cfg, ch, last)
+        if not args.skip_svd:
+            log("cpu svd baseline")
+            cb = cpu_svd_timings(2 * args.svd_chi, cpu_threads(), budget_s=args.cpu_svd_budget_s)
+            out["cpu_baseline"]["svd_chi2048"] = cb
+            thr = cpu_threads()
+            out["svd_chi2048_cpu_ms"] = {k: v for k, v in cb.items() if k.endswith("_ms")}
+            if cb.get(f"c128_{thr}t_ms") and "svd_chi2048_ms" in out:
+                out["svd_chi2048_speedup"] = {
+                    k.replace("_ms", ""): round(v / out["svd_chi2048_ms"], 2)
+                    for k, v in cb.items() if k.endswith("_ms") and v}
+    ch.close()
     ctx.close()
+    if not args.skip_shards:
+        out.update(shard_jobs(args, dist))
     return out
+
+
+def shard_jobs(args, dist):
+    """The naturally sharded workloads at this run's N GPUs:
+    C4 (64-chain XXZ ensemble, LPT plan, chains in flight per GPU, one NCCL
+    all_gather of the per-chain records) and C2 (a batch of isolated chi=1024
+    SVDs, round robin, one all_gather).  Whole-job throughput, device time (CUDA
+    events per worker stream), max over ranks."""
+    from paper_2604_03960_b200 import ensemble_run as E
+    res = {}
+    ns = argparse.Namespace(chains=args.c4_chains, n=N_SITES, jz_max=2.0, chi_max=CHI_MAX,
+                            eps=EPS_TRUNC, sweeps=10, inflight=4, grid_share=False,
+                            batch=args.c2_batch, svd_chi=args.c2_chi)
+    log("c4 ensemble")
+    job_s, table, meta = E.job_c4(ns, dist.e)
+    if table is not None and dist.rank == 0:
+        t = np.asarray(table)
+        res["c4_chains_per_s"] = round(args.c4_chains / job_s, 4)
+        res["c4"] = {"chains": args.c4_chains, "device_s": round(job_s, 3),
+                     "converged": int(t[:, 4].sum()), "max_chi": int(t[:, 3].max()),
+                     "e_per_site_jz1": float(t[np.argmin(np.abs(t[:, 0] - 1.0)), 1]),
+                     "workload": meta["config"]["workload"], "plan": meta["config"]["plan"],
+                     "inflight_per_gpu": 4, "scaling": "strong (fixed 64 chains)"}
+    log("c2 batch")
+    job_s, table, meta = E.job_c2(ns, dist.e)
+    if table is not None and dist.rank == 0:
+        t = np.asarray(table)
+        res["c2_svds_per_s"] = round(args.c2_batch / job_s, 4)
+        res["c2"] = {"batch": args.c2_batch, "n": 2 * args.c2_chi, "device_s": round(job_s, 3),
+                     "max_sum_sigma2_relerr": float(t[:, 2].max()),
+                     "workload": meta["config"]["workload"], "plan": "round robin",
+                     "scaling": "strong (fixed batch)"}
+    return res
+
+
+def heff_insweep(ctx, args):
+    """H_eff TFLOP/s inside a real sweep at chi = 1024: Heisenberg
+    N=100, fixed chi_max=1024 from the Neel state (chi grows x4 per sweep and reaches
+    1024 on bonds 10..89 in sweep 5).  Sweep `args.heff_sweep` is measured with the
+    Lanczos stepped from the host so that every H_eff application is bracketed by
+    CUDA events on the library stream (phase "heff"; flops per matvec
+    2 D d^2 chl chr (chl+chr) + 4 D^2 d^3 chl chr at each visit's own shape)."""
+    from paper_2604_03960_b200.api import Chain
+    s_idx = args.heff_sweep
+    spec = abi.model_spec(N_SITES, convention=abi.SPIN_HALF)
+    cfg = abi.fixed_config(CHI_MAX, max_sweeps=s_idx + 1, eps_conv=1e-300)
+    ctx.set_lanczos_graph(0)
+    ch = Chain(ctx, spec, cfg)
+    try:
+        for s in range(s_idx):
+            ch.sweep(s)
+        ctx.device_times(enable=True, reset=True)
+        ctx.timer_start()
+        r = ch.sweep(s_idx)
+        sweep_ms = ctx.timer_stop()
+        ph = ctx.device_times(enable=False)
+    finally:
+        ch.close()
+        ctx.set_lanczos_graph(-1)
+    h = ph["heff"]
+    tf = h["work"] / max(h["ms"], 1e-9) / 1e9
+    chi = r["chi_profile"]
+    return {"bound": "tensor",
+            "kernel": "H_eff matvec in a real sweep (dmma_gemm_kernel x2 + mpo_mix_kernel; "
+                      "heff_small_kernel at the chain ends)",
+            "achieved": round(tf, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": round(tf / FP64_PEAK_TFLOPS, 4), "traffic": None,
+            "matvecs": h["launches"], "heff_ms": round(h["ms"], 2),
+            "sweep_ms": round(sweep_ms, 1), "phases_ms": {k: round(v["ms"], 1) for k, v in ph.items()},
+            "bonds_at_chi1024": int((chi == 1024).sum()),
+            "workload": f"N=100 Heisenberg S=1/2, fixed chi=1024, sweep {s_idx} of a Neel start",
+            "work_def": "sum over the sweep's matvecs of 2*D*d^2*chl*chr*(chl+chr)+4*D^2*d^3*chl*chr "
+                        "flops / sum of their CUDA-event times",
+            "peak_source": "measured DMMA peak (profiles/fp64_peak_r01.txt)"}
 
 
 def svd_part(ctx, args):
     """Truncated-SVD half of the metric: random 4096x4096 FP64 theta (chi=2048)."""
     import torch
     n = 2 * args.svd_chi
-    g = torch.Generator(device="cuda").manual_seed(1234)
-    a = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+    # the matrix tests/golden/svd_sigma_large.json pins (sigma vs LAPACK dgesdd,
+    # tests/test_golden_long.py): numpy default_rng(1234), uploaded once
+    a = torch.from_numpy(np.random.default_rng(1234).standard_normal((n, n))).cuda()
     s = torch.empty(n, dtype=torch.float64, device="cuda")
     u = torch.empty(n, n, dtype=torch.float64, device="cuda")
     vt = torch.empty(n, n, dtype=torch.float64, device="cuda")
@@ -351,11 +487,18 @@ def cpu_baseline_sample(spec, cfg, ch, last):
     c_sample = visit_cost_model(sample, chi).sum()
     c_full = visit_cost_model(last["visits"], chi).sum()
     est = float(secs.sum()) * c_full / c_sample
+    secs_r, mvs_r = O.time_visits_from_state(spec, cfg, sites, states, first, count,
+                                             complex_mode=False)
+    est_r = float(secs_r.sum()) * c_full / c_sample
     return {"value": round(est, 3), "unit": "s/sweep", "cores": threads, "kind": "port",
             "sample": f"{count} right-moving visits (bonds {first}..{first + count - 1}) of the "
                       f"steady-state sweep on the oracle (complex128, OpenBLAS {threads} threads): "
                       f"{secs.sum():.2f} s, extrapolated to all {2 * (N_SITES - 1)} visits by FLOP "
-                      f"model (matvecs x H_eff flops + SVD + env)"}
+                      f"model (matvecs x H_eff flops + SVD + env)",
+            "real_fp64": {"value": round(est_r, 3), "unit": "s/sweep",
+                          "sample": f"the same {count} visits in the real gauge (FP64, the GPU "
+                                    f"path's arithmetic): {secs_r.sum():.2f} s, same extrapolation"},
+            "host": host_info()}
 
 
 # ---------------------------------------------------------------- reference arm
@@ -385,6 +528,21 @@ def run_reference(args, dist):
     sample = (f"sweeps {W}..{W + len(walls) - 1} of the C3 run, full sweeps, complex128, "
               f"OpenBLAS {threads} threads" + (f" (stopped after {len(walls)} of {K} steps: "
                                                f"{args.ref_budget_s:.0f} s budget)" if budget_hit else ""))
+    # the same sweeps in the real gauge (FP64: the GPU path's arithmetic), budgeted
+    real_walls = []
+    if not args.skip_real:
+        ch = O.OracleChain(spec, cfg, complex_mode=False)
+        for s_ in range(W):
+            ch.sweep(s_)
+        t0 = time.perf_counter()
+        for i in range(len(walls)):
+            rec_r, _ = ch.sweep(W + i)
+            real_walls.append(rec_r.wall_time)
+            if time.perf_counter() - t0 > args.real_budget_s:
+                break
+        ch.close()
+    svd = None if args.skip_svd else cpu_svd_timings(2 * args.svd_chi, threads, reps_all=3,
+                                                      budget_s=0.0)
     return {"metric": METRIC, "value": round(v, 4), "unit": "s/sweep", "impl": "reference",
             "n_gpus": dist.world, "steps": len(walls), "warmup": W,
             "ms_per_step": round(v * 1e3, 2), "higher_is_better": False, "scaling": "weak",
@@ -393,6 +551,14 @@ def run_reference(args, dist):
                                    "eps_trunc=1e-10", "n": N_SITES, "chi_max": CHI_MAX},
             "e_per_site": rec.energy / N_SITES, "chi_max_seen": int(chi.max()),
             "sweep_s": [round(w, 4) for w in walls],
+            "real_fp64": None if not real_walls else {
+                "value": round(float(np.mean(real_walls)), 4), "unit": "s/sweep",
+                "sweeps": f"{W}..{W + len(real_walls) - 1}",
+                "sweep_s": [round(w, 4) for w in real_walls],
+                "note": "same run in the real gauge (identical energies and chi profiles to 1e-12)"},
+            "svd_chi2048_ms": None if svd is None else svd[f"c128_{threads}t_ms"],
+            "svd_chi2048_cpu_ms": svd,
+            "host": host_info(),
             "cpu_baseline": {"value": round(v, 4), "unit": "s/sweep", "cores": threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": round(v, 4), "unit": "s/sweep", "h2d_bytes_per_step": 0,
@@ -410,7 +576,16 @@ def main():
     ap.add_argument("--svd-reps", type=int, default=3)
     ap.add_argument("--skip-svd", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-budget-s", type=float, default=180.0)
+    ap.add_argument("--ref-budget-s", type=float, default=600.0)
+    ap.add_argument("--cpu-svd-budget-s", type=float, default=150.0)
+    ap.add_argument("--skip-shards", action="store_true")
+    ap.add_argument("--skip-heff-insweep", action="store_true")
+    ap.add_argument("--heff-sweep", type=int, default=5)
+    ap.add_argument("--skip-real", action="store_true")
+    ap.add_argument("--real-budget-s", type=float, default=100.0)
+    ap.add_argument("--c4-chains", type=int, default=64)
+    ap.add_argument("--c2-batch", type=int, default=64)
+    ap.add_argument("--c2-chi", type=int, default=1024)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: W >= 3

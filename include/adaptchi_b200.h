@@ -172,7 +172,17 @@ int achi_flush_l2(achi_ctx* ctx, size_t bytes);
  * (phases: 0 H_eff matvec, 1 SVD, 2 environment update).  enable turns the
  * accounting on/off (-1 leaves it); reset zeroes it.  out9 (may be NULL) =
  * {ms[3], algorithmic work[3] (flops, bytes, flops), launches[3]}. */
+/* Lanczos inner loop of this context's chains: 1 = one conditional CUDA graph
+ * per (bond, direction) (default), 0 = stepped from the host (same kernels and
+ * arithmetic; every launch visible to profilers and to phase 3 of
+ * achi_device_times_ex), -1 = the process default (ACHI_LANCZOS_GRAPH). */
+int achi_ctx_set_lanczos_graph(achi_ctx* ctx, int mode);
 int achi_device_times(achi_ctx* ctx, int enable, int reset, double* out9);
+/* Same, for the first n_phases (<= 4) phases: 3 = H_eff applications alone
+ * (recorded around each matvec outside graph capture, so they are seen with
+ * ACHI_LANCZOS_GRAPH=0 or for the Lanczos matvecs issued from the host).
+ * out = {ms[n], work[n] (flops, bytes, flops, flops), launches[n]}. */
+int achi_device_times_ex(achi_ctx* ctx, int enable, int reset, double* out, int n_phases);
 
 /* ---- DMRG (dmrg.hpp:40-90, dmrg.cpp:216-282) ---- */
 /* run_dmrg setup: validate, build_mpo (real gauge), Neel product state,

@@ -172,6 +172,8 @@ def load():
         "achi_svd_batched_device": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                               C.c_void_p, P(C.c_int)]),
         "achi_device_times": (C.c_int, [vp, C.c_int, C.c_int, dp]),
+        "achi_device_times_ex": (C.c_int, [vp, C.c_int, C.c_int, dp, C.c_int]),
+        "achi_ctx_set_lanczos_graph": (C.c_int, [vp, C.c_int]),
         "achi_bond_select": (C.c_int, [vp, P(DmrgConfig), C.c_int, dp, P(BondState),
                                        C.c_int, C.c_int, P(TraceRow), P(VisitRecord)]),
         "achi_eigs_lowest_dense": (C.c_int, [vp, C.c_int, dp, dp, d, C.c_int, dp, dp,

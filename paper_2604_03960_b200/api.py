@@ -84,11 +84,12 @@ class Context:
 
     def device_times(self, enable=None, reset=False):
         """Per-phase CUDA-event device time: dict phase -> (ms, work, launches)."""
-        out = np.zeros(9)
+        names = ("matvec", "svd", "env", "heff")
+        n = len(names)
+        out = np.zeros(3 * n)
         e = -1 if enable is None else int(bool(enable))
-        self._check(self.lib.achi_device_times(self.h, e, int(bool(reset)), _dp(out)))
-        names = ("matvec", "svd", "env")
-        return {k: dict(ms=out[i], work=out[3 + i], launches=int(out[6 + i]))
+        self._check(self.lib.achi_device_times_ex(self.h, e, int(bool(reset)), _dp(out), n))
+        return {k: dict(ms=out[i], work=out[n + i], launches=int(out[2 * n + i]))
                 for i, k in enumerate(names)}
 
     def svd_batched_device(self, d_a_ptr, batch, m, n, d_sigma_ptr):
@@ -104,6 +105,12 @@ class Context:
         self._check(self.lib.achi_svd_device(self.h, m, n, C.c_void_p(d_a_ptr), C.c_void_p(d_sigma_ptr),
                                              C.c_void_p(d_u_ptr), C.c_void_p(d_vt_ptr), C.byref(sw)))
         return sw.value
+
+    def set_lanczos_graph(self, mode):
+        """1: Lanczos inner loop as a conditional CUDA graph (default); 0: stepped
+        from the host (every kernel visible to ncu and to the per-matvec H_eff
+        accounting, phase "heff" of device_times); -1: process default."""
+        self._check(self.lib.achi_ctx_set_lanczos_graph(self.h, int(mode)))
 
     def flush_l2(self, nbytes=256 << 20):
         self._check(self.lib.achi_flush_l2(self.h, C.c_size_t(nbytes)))

@@ -312,12 +312,11 @@ void bond_select(Ctx& ctx, const double* sigma, int r, const achi_dmrg_config& c
                  achi_bond_state* states, int bond, int sweep, int moving_right,
                  achi_trace_row* trace_slot, achi_visit_record* visit_slot, BondOut* out) {
   const size_t smem = sizeof(double) * (static_cast<size_t>(r) + 1 + BS_THREADS);
-  static bool attr = false;
-  if (!attr) {
+  per_device_once("bond_select_kernel", ctx.device, [] {
     ACHI_CUDA(cudaFuncSetAttribute(bond_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    200 * 1024));
-    attr = true;
-  }
+    return 1;
+  });
   if (smem > 200 * 1024) fail(ACHI_E_SIZE_GUARD, "bond_select: spectrum too long");
   bond_select_kernel<<<1, BS_THREADS, smem, ctx.stream>>>(sigma, r, cfg, states, bond, sweep,
                                                           moving_right, trace_slot, visit_slot, out);
@@ -327,12 +326,11 @@ void bond_select(Ctx& ctx, const double* sigma, int r, const achi_dmrg_config& c
 void spectrum_stats(Ctx& ctx, const double* sigma, int r, int kept, double eps, double* out,
                     int* err) {
   const size_t smem = sizeof(double) * (static_cast<size_t>(r) + 1 + BS_THREADS);
-  static bool attr = false;
-  if (!attr) {
+  per_device_once("spectrum_stats_kernel", ctx.device, [] {
     ACHI_CUDA(cudaFuncSetAttribute(spectrum_stats_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+    return 1;
+  });
   if (smem > 200 * 1024) fail(ACHI_E_SIZE_GUARD, "spectrum_stats: spectrum too long");
   spectrum_stats_kernel<<<1, BS_THREADS, smem, ctx.stream>>>(sigma, r, kept, eps, out, err);
   ACHI_LAUNCHED(ctx);

@@ -12,6 +12,8 @@ namespace {
 int guard(achi_ctx* ctx, const std::function<void()>& f) {
   AllocStream as(ctx ? ctx->c.stream : nullptr);
   try {
+    // a thread may drive contexts on several GPUs, or one created elsewhere
+    if (ctx) ACHI_CUDA(cudaSetDevice(ctx->c.device));
     f();
     if (ctx) ctx->c.last_error.clear();
     return ACHI_OK;
@@ -170,16 +172,25 @@ int achi_flush_l2(achi_ctx* ctx, size_t bytes) {
   });
 }
 
+int achi_ctx_set_lanczos_graph(achi_ctx* ctx, int mode) {
+  return guard(ctx, [&] { ctx->c.lanczos_graph = mode < 0 ? -1 : (mode ? 1 : 0); });
+}
+
 int achi_device_times(achi_ctx* ctx, int enable, int reset, double* out9) {
+  return achi_device_times_ex(ctx, enable, reset, out9, 3);
+}
+
+int achi_device_times_ex(achi_ctx* ctx, int enable, int reset, double* out, int n_phases) {
   return guard(ctx, [&] {
+    if (n_phases < 0 || n_phases > EventAcc::kNumTags) fail(ACHI_E_INVALID_CONFIG, "device_times: n_phases");
     EventAcc& a = ctx->c.acc;
     ctx->c.sync();
     a.resolve();
-    if (out9)
-      for (int t = 0; t < EventAcc::kNumTags; ++t) {
-        out9[t] = a.ms[t];
-        out9[3 + t] = a.work[t];
-        out9[6 + t] = static_cast<double>(a.count[t]);
+    if (out)
+      for (int t = 0; t < n_phases; ++t) {
+        out[t] = a.ms[t];
+        out[n_phases + t] = a.work[t];
+        out[2 * n_phases + t] = static_cast<double>(a.count[t]);
       }
     if (reset)
       for (int t = 0; t < EventAcc::kNumTags; ++t) a.ms[t] = a.work[t] = 0, a.count[t] = 0;

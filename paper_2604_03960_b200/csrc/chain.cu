@@ -403,10 +403,18 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
                      reinterpret_cast<uint64_t>(c.ws_split.p)})
     key = (key ^ v) * 1099511628211ull;
   c.acc.begin(EventAcc::kMatvec, c.stream);  // the whole eigensolve (matvecs + orthogonalisation)
-  EigsOut eig = eigs_lowest(
-      c, lz, [&](const double* in, double* out) { heff_apply(c, op, in, out); }, nvec, dim, theta.p,
+  // graph mode: enqueued without a host wait; read back with the bond selection below
+  eigs_lowest_async(
+      c, lz,
+      [&](const double* in, double* out) {
+        c.acc.begin(EventAcc::kHeff, c.stream);  // skipped while the Lanczos graph is captured
+        heff_apply(c, op, in, out);
+        c.acc.end(c.stream, mv_flops);
+      },
+      nvec, dim, theta.p,
       cfg.eig_tol, cfg.eig_max_iter, vec.p, 2 * b + (right ? 1 : 0), key, &op);
-  c.acc.end(c.stream, eig.matvecs * mv_flops);
+  c.acc.end(c.stream, 0.0);  // flops added once the matvec count is known
+  if (profile) c.sync();
   const auto t1 = clk::now();
   const SvdSide side = right ? SvdSide::kRows : SvdSide::kCols;
   c.acc.begin(EventAcc::kSvd, c.stream);
@@ -442,8 +450,10 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   bond_select(c, sr.sigma, sr.r_true, cfg, states.p, b, sweep_index, right ? 1 : 0,
               trace.p + slot, visits.p + slot, bout.p);
   ACHI_CUDA(cudaMemcpyAsync(bout_h.p, bout.p, sizeof(BondOut), cudaMemcpyDeviceToHost, c.stream));
-  c.sync();
+  c.sync();  // the one host wait of the visit: eigensolve outcome, SVD sweeps, kept rank
   c.acc.resolve();
+  const EigsOut eig = eigs_finish(c, lz);  // throws EigenNonConvergence / InvalidMatrix
+  if (c.acc.enabled) c.acc.work[EventAcc::kMatvec] += eig.matvecs * mv_flops;
   auto write_dump = [&] {
     if (FILE* f = std::fopen(dump_path, "wb")) {
       const int32_t hdr[6] = {sm_, sn_, smt, snt, right ? 1 : 0, warm ? 1 : 0};

@@ -7,8 +7,11 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/adaptchi_b200.h"
@@ -145,14 +148,18 @@ struct LanczosStatus {
 
 // Device-time accounting: event pairs recorded on the context stream around a
 // phase, resolved (after a sync the caller already pays) into per-tag totals.
+// Phases nest (kHeff, the H_eff applications, sits inside kMatvec, the whole
+// eigensolve); nothing is recorded while the stream is being captured.
 struct EventAcc {
-  enum Tag { kMatvec = 0, kSvd = 1, kEnv = 2, kNumTags = 3 };
+  enum Tag { kMatvec = 0, kSvd = 1, kEnv = 2, kHeff = 3, kNumTags = 4 };
   std::vector<cudaEvent_t> pool;
-  std::vector<std::pair<int, int>> open;  // (tag, index of start event)
+  std::vector<std::pair<int, int>> stack;  // open phases: (tag, index of start event)
+  struct Closed { int tag, start, stop; };
+  std::vector<Closed> closed;
   size_t used = 0;
-  double ms[kNumTags] = {0, 0, 0};
-  double work[kNumTags] = {0, 0, 0};  // algorithmic flops or bytes
-  long count[kNumTags] = {0, 0, 0};
+  double ms[kNumTags] = {0, 0, 0, 0};
+  double work[kNumTags] = {0, 0, 0, 0};  // algorithmic flops or bytes
+  long count[kNumTags] = {0, 0, 0, 0};
   bool enabled = false;
   cudaEvent_t next() {
     if (used == pool.size()) {
@@ -162,26 +169,40 @@ struct EventAcc {
     }
     return pool[used++];
   }
+  static bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    return cs != cudaStreamCaptureStatusNone;
+  }
   void begin(int tag, cudaStream_t s) {
     if (!enabled) return;
+    if (capturing(s)) {
+      stack.emplace_back(tag, -1);
+      return;
+    }
     const int i = static_cast<int>(used);
     cudaEventRecord(next(), s);
-    open.emplace_back(tag, i);
+    stack.emplace_back(tag, i);
   }
   void end(cudaStream_t s, double w) {
-    if (!enabled) return;
+    if (!enabled || stack.empty()) return;
+    const auto [tag, i] = stack.back();
+    stack.pop_back();
+    if (i < 0) return;
+    const int j = static_cast<int>(used);
     cudaEventRecord(next(), s);
-    work[open.back().first] += w;
-    count[open.back().first] += 1;
+    closed.push_back(Closed{tag, i, j});
+    work[tag] += w;
+    count[tag] += 1;
   }
   // call after a stream sync: fold all closed pairs into the totals
   void resolve() {
-    for (auto& [tag, i] : open) {
+    for (const Closed& c : closed) {
       float f = 0;
-      if (cudaEventElapsedTime(&f, pool[i], pool[i + 1]) == cudaSuccess) ms[tag] += f;
+      if (cudaEventElapsedTime(&f, pool[c.start], pool[c.stop]) == cudaSuccess) ms[c.tag] += f;
     }
-    open.clear();
-    used = 0;
+    closed.clear();
+    if (stack.empty()) used = 0;
   }
   ~EventAcc() {
     for (auto e : pool) cudaEventDestroy(e);
@@ -197,6 +218,10 @@ struct Ctx {
   // cap on the CTAs of this context's cooperative kernels (0: none); several
   // contexts sharing a GPU (ensemble chains in flight) each get a share
   int grid_cap = 0;
+  // Lanczos inner loop as a conditional CUDA graph (1), stepped from the host
+  // (0: every kernel visible to ncu and to the per-matvec event accounting),
+  // or the process default (-1: ACHI_LANCZOS_GRAPH, on unless "0")
+  int lanczos_graph = -1;
   int cap_grid(long want) const {
     return static_cast<int>(grid_cap > 0 ? std::min<long>(want, grid_cap) : want);
   }
@@ -216,6 +241,22 @@ struct Ctx {
   DevBuf flush;
   void sync() { ACHI_CUDA(cudaStreamSynchronize(stream)); }
 };
+
+// One-time per-device setup (kernel attributes, occupancy-derived grid sizes),
+// thread-safe and keyed by (site, device): a second GPU gets its own
+// attributes, and concurrent contexts on worker threads do not race.
+template <class F>
+int per_device_once(const std::string& site, int device, F&& f) {
+  static std::mutex mu;
+  static std::map<std::pair<std::string, int>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_pair(site, device);
+  const auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const int v = f();
+  cache.emplace(key, v);
+  return v;
+}
 
 inline size_t pad2(size_t x) { return x + (x & 1); }
 inline int pad2i(int x) { return x + (x & 1); }

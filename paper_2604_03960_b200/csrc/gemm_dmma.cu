@@ -55,11 +55,11 @@ void launch(Ctx& ctx, int M, int N, int K, const Operand& A, const Operand& B, d
             long ldc, int splits) {
   using G = Cfg<BM, BN, WTM, WTN, STAGES, AM, BMJ>;
   auto kern = dmma_gemm_kernel<BM, BN, WTM, WTN, STAGES, AM, BMJ>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  per_device_once(std::string("dmma_gemm_kernel:") + std::to_string(reinterpret_cast<uintptr_t>(
+                      reinterpret_cast<const void*>(kern))), ctx.device, [&] {
     ACHI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
-    attr_set = true;
-  }
+    return 1;
+  });
   CUtensorMap ma = AM == Major::kK ? make_map(A.ptr, M, K, A.ld, BM) : make_map(A.ptr, K, M, A.ld, 16);
   CUtensorMap mb = BMJ == Major::kK ? make_map(B.ptr, N, K, B.ld, BN) : make_map(B.ptr, K, N, B.ld, 16);
   const int kt_total = cdiv(K, BK);

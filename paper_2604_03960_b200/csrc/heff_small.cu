@@ -49,15 +49,14 @@ template <int KM>
 void launch_small(Ctx& ctx, const HeffOps& op, const double* theta, double* out, double* X, double* part) {
   const int dd = op.d * op.d;
   const long M2 = static_cast<long>(op.chl) * dd, N2 = op.chr;
-  static int max_blocks = 0;
   const size_t smem = smem_bytes<KM>();
-  if (max_blocks == 0) {
+  const int max_blocks = per_device_once("heff_small_kernel:" + std::to_string(KM), ctx.device, [&] {
     ACHI_CUDA(cudaFuncSetAttribute(heff_small_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
     int per_sm = 0;
     ACHI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heff_small_kernel<KM>, HS_THREADS, smem));
-    max_blocks = std::max(1, per_sm) * ctx.num_sms;
-  }
+    return std::max(1, per_sm) * ctx.num_sms;
+  });
   const long itemsA = cdiv(op.chl, HS_TM / op.D1) * cdiv(op.chr, HS_JRB);
   const long itemsB = cdiv(M2, HS_TM) * cdiv(N2, HS_TN) * op.D3;
   const int grid = std::max(1, ctx.cap_grid(std::min<long>(std::max(itemsA, itemsB), max_blocks)));

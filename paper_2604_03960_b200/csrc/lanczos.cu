@@ -104,11 +104,14 @@ __global__ void __launch_bounds__(RED_THREADS) reduce_partials_kernel(
 }
 
 // dst[x] = src[x] + sign * sum_v coef[v] * Q_v[x]; partials[b] = sum_chunk dst^2
+// (nv_ctl non-null: nv = nv_ctl->j + 1, the basis size the device loop reached)
 __global__ void __launch_bounds__(RED_THREADS) multi_axpy_kernel(
     const double* __restrict__ Q, long stride, int nv, const double* __restrict__ coef, double sign,
-    const double* src, double* dst, long n, double* __restrict__ partials) {
+    const double* src, double* dst, long n, double* __restrict__ partials,
+    const LanczosCtl* __restrict__ nv_ctl = nullptr) {
   __shared__ double c[64];
   __shared__ double sh[32];
+  if (nv_ctl) nv = nv_ctl->j + 1;
   for (int v = threadIdx.x; v < nv; v += blockDim.x) c[v] = sign * coef[v];
   __syncthreads();
   const long base = static_cast<long>(blockIdx.x) * CHUNK + threadIdx.x;
@@ -406,6 +409,86 @@ __global__ void __launch_bounds__(RED_THREADS) residual_kernel(const double* __r
     st->ev = *ev;
     st->res = res;
     misc[1] = res > 0 ? 1e-8 / res : 0.0;
+  }
+}
+
+// ---- the restart loop on the device (graph mode) ----
+// Prologue of an eigensolve: misc[2] = ||v0||^2 (reduced before); misc[3] =
+// ||v0||; control reset; the restart loop runs only for a valid v0
+// (linalg.cpp:109-111: InvalidMatrix otherwise).
+__global__ void eig_init_kernel(double* misc, LanczosCtl* ctl, int block, int max_iter, double tol,
+                                cudaGraphConditionalHandle outer) {
+  const double n2 = misc[2];
+  const bool ok = n2 > 0;  // false for NaN too
+  misc[3] = ok ? sqrt(n2) : 1.0;
+  *ctl = LanczosCtl{0, 0, block, max_iter, 0, 0, ok ? 0 : LZ_BAD_V0, 0, tol, INFINITY};
+  cudaGraphSetConditional(outer, ok && max_iter > 0 ? 1u : 0u);
+}
+
+// Start of a restart cycle (linalg.cpp:126): j = 0, the inner loop armed.
+__global__ void eig_cycle_kernel(LanczosCtl* ctl, cudaGraphConditionalHandle inner) {
+  ctl->j = 0;
+  ctl->cycles += 1;
+  ctl->flags &= ~LZ_BREAKDOWN;
+  cudaGraphSetConditional(inner, 1u);
+}
+
+// Explicit residual check and restart decision (linalg.cpp:156-169), after
+// w = H ritz, ev = ritz.w, tmp = w - ev ritz (its norm partials):
+// converged -> stop; max_iter reached -> stop, EigenNonConvergence with the
+// best residual; otherwise restart from the Ritz vector, on breakdown from
+// ritz + 1e-8 tmp / ||tmp|| (misc[1] = that coefficient, else 0).
+__global__ void __launch_bounds__(RED_THREADS) eig_decide_kernel(const double* __restrict__ partials,
+                                                                 int nblocks, const double* ev,
+                                                                 double* misc, LanczosStatus* st,
+                                                                 LanczosCtl* ctl,
+                                                                 cudaGraphConditionalHandle outer) {
+  __shared__ double sh[32];
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) v += partials[b];
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) {
+    const double res = sqrt(v), e = *ev;
+    st->ev = e;
+    st->res = res;
+    LanczosCtl& c = *ctl;
+    c.matvecs += 1;  // the Ritz vector's matvec
+    c.best = fmin(c.best, res);
+    const bool breakdown = st->bnorm <= 1e-14 * fmax(1.0, fabs(st->theta));
+    const bool converged = res <= c.tol * fmax(1.0, fabs(e));
+    misc[1] = (!converged && breakdown && res > 0) ? 1e-8 / res : 0.0;
+    bool again = false;
+    if (converged) {
+      c.flags |= LZ_CONVERGED;
+    } else {
+      if (breakdown) c.flags |= LZ_BREAKDOWN;
+      if (c.matvecs >= c.max_iter)
+        c.flags |= LZ_NONCONVERGED;
+      else
+        again = true;
+    }
+    cudaGraphSetConditional(outer, again ? 1u : 0u);
+  }
+}
+
+// Converged: out = ritz (when out is another buffer).  Restarting: q_0 =
+// ritz, or on breakdown q_0 = (ritz + 1e-8 tmp/||tmp||) / ||.|| (q_0 holds the
+// sum and *nrm its norm).
+__global__ void eig_restart_kernel(double* __restrict__ q0, const double* __restrict__ ritz,
+                                   double* out, long n, const double* __restrict__ nrm,
+                                   const LanczosCtl* __restrict__ ctl) {
+  const int flags = ctl->flags;
+  const bool conv = flags & LZ_CONVERGED, brk = flags & LZ_BREAKDOWN;
+  if (conv && out == ritz) return;
+  const double f = brk ? 1.0 / *nrm : 0.0;
+  for (long x = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; x < n;
+       x += static_cast<long>(gridDim.x) * blockDim.x) {
+    if (conv)
+      out[x] = ritz[x];
+    else if (brk)
+      q0[x] = q0[x] * f;
+    else
+      q0[x] = ritz[x];
   }
 }
 
@@ -731,9 +814,9 @@ struct Kernels {
   }
   // dst = src + sign * Q c ; norm partials -> ws.partials (first nb entries)
   void axpy(const double* Q, int nv, const double* c, double sign, const double* src, double* dst,
-            bool norm) {
+            bool norm, const LanczosCtl* nv_ctl = nullptr) {
     multi_axpy_kernel<<<nb, RED_THREADS, 0, ctx.stream>>>(Q, ws.stride, nv, c, sign, src, dst, n,
-                                                          norm ? ws.partials.p : nullptr);
+                                                          norm ? ws.partials.p : nullptr, nv_ctl);
     ACHI_LAUNCHED(ctx);
   }
   void scale(double* dst, const double* src, const double* s, bool invert) {
@@ -786,6 +869,7 @@ void LanczosWs::reserve(long n) {
     scal.reserve(512);
     ctl.reserve(1);
     ctl_h.reserve(1);
+    res_h.reserve(1);
   }
 }
 
@@ -804,39 +888,27 @@ void device_scale(Ctx& ctx, double* dst, const double* src, long n, const double
   ACHI_LAUNCHED(ctx);
 }
 
-EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long dim,
-                    const double* v0, double tol, int max_iter, double* out, int graph_slot,
-                    uint64_t graph_key, const HeffOps* small_op) {
+void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long dim,
+                       const double* v0, double tol, int max_iter, double* out, int graph_slot,
+                       uint64_t graph_key, const HeffOps* small_op) {
   ws.reserve(n);
   Kernels K{ctx, ws, n, red_blocks(ctx, n)};
   double* misc = ws.misc();
-  // n0 = ||v0||; q = v0 / n0
-  device_norm2(ctx, v0, n, misc + 2);
-  double h_n2;
-  ACHI_CUDA(cudaMemcpyAsync(&h_n2, misc + 2, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-  ctx.sync();
-  if (!(h_n2 > 0)) fail(ACHI_E_INVALID_MATRIX, "eigs_lowest: v0 must have norm > 0");
-  {
-    // misc[3] = sqrt(misc[2]) computed on device for bitwise consistency
-    const double nrm = std::sqrt(h_n2);
-    ACHI_CUDA(cudaMemcpyAsync(misc + 3, &nrm, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
-  }
-  K.scale(ws.q(0), v0, misc + 3, true);
-
   const int block = static_cast<int>(std::min<long>(dim, LANCZOS_BLOCK));
-  static int orth_max = 0;
-  if (orth_max == 0) {
+  const int orth_max = per_device_once("lanczos_orth_kernel", ctx.device, [&] {
     int per_sm = 0;
     ACHI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lanczos_orth_kernel,
                                                             ORTH_THREADS, 0));
-    orth_max = std::max(1, std::min(per_sm, 2)) * ctx.num_sms;
-  }
+    return std::max(1, std::min(per_sm, 2)) * ctx.num_sms;
+  });
   // fixed for a given n: the chunking (and so every reduction order) is deterministic
   // (about one element per thread up to two CTAs per SM: the passes are latency-bound)
-  static const bool use_graph = [] {
+  static const bool graph_default = [] {
     const char* e = std::getenv("ACHI_LANCZOS_GRAPH");
     return !(e && e[0] == '0');
   }();
+  const bool use_graph = ctx.lanczos_graph >= 0 ? ctx.lanczos_graph != 0 : graph_default;
+  ws.pend_graph = use_graph;
   // ACHI_LANCZOS_FUSED=1 (opt-in): for chi <= 128 in graph mode the whole step is
   // one cooperative launch (lanczos_step_small_kernel) over max(orthogonalisation
   // grid, matvec items + 1) CTAs.  Measured slower on C3 (Lanczos 0.134 vs 0.122
@@ -850,16 +922,15 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
   long fused_items = 0;
   const bool fused = use_graph && fused_on && small_op &&
                      heff_small_fusable(ctx, *small_op, ws.qcur.p, ws.w.p, &fused_h, &fused_items);
-  static int fused_max = 0;
-  if (fused && fused_max == 0) {
+  const int fused_max = !fused ? 0 : per_device_once("lanczos_step_small_kernel", ctx.device, [&] {
     const size_t fsm = hs::smem_bytes<hs::HS_KMAX>();
     ACHI_CUDA(cudaFuncSetAttribute(lanczos_step_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(fsm)));
     int per_sm = 0;
     ACHI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lanczos_step_small_kernel,
                                                             ORTH_THREADS, fsm));
-    fused_max = std::max(1, per_sm) * ctx.num_sms;
-  }
+    return std::max(1, per_sm) * ctx.num_sms;
+  });
   const int orth_grid =
       fused ? std::max(2, ctx.cap_grid(std::min<long>(
                               std::max<long>(cdiv(n, ORTH_THREADS), fused_items + 1), fused_max)))
@@ -929,13 +1000,106 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
     ws.graphs.resize(static_cast<size_t>(graph_slot) + 1);
   LanczosGraph& lg = graph_slot >= 0 ? ws.graphs[static_cast<size_t>(graph_slot)] : local;
   const uint64_t key = graph_key ^ (static_cast<uint64_t>(n) << 40) ^ static_cast<uint64_t>(orth_grid) ^
-                       (fused ? 0x5a5a000000000000ull : 0ull);
+                       (fused ? 0x5a5a000000000000ull : 0ull) ^
+                       (reinterpret_cast<uint64_t>(v0) * 0x9E3779B97F4A7C15ull) ^
+                       (reinterpret_cast<uint64_t>(out) * 0xC2B2AE3D27D4EB4Full) ^
+                       (static_cast<uint64_t>(block) << 32) ^ (static_cast<uint64_t>(max_iter) << 48) ^
+                       static_cast<uint64_t>(std::llround(-std::log10(std::max(tol, 1e-300)) * 1000.0)) << 20;
   static thread_local long builds = 0, updates = 0;
   static thread_local double build_s = 0.0;
   if (prof_on && prof_calls % 200 == 0)
     std::fprintf(stderr, "[lanczos] graph builds %ld (%ld by exec update), %.3f ms each\n", builds,
                  updates, builds ? 1e3 * build_s / builds : 0.0);
-  if (use_graph && (!lg.exec || lg.key != key)) {
+
+  if (!use_graph) {
+    // host-stepped (profiling mode): the same kernels, each decision read back
+    ws.pend_body = ws.pend_cycle = ws.pend_once = 0;
+    LanczosResult& R = *ws.res_h.p;
+    R = LanczosResult{};
+    R.ctl.best = std::numeric_limits<double>::infinity();
+    device_norm2(ctx, v0, n, misc + 2);
+    double h_n2;
+    ACHI_CUDA(cudaMemcpyAsync(&h_n2, misc + 2, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    if (!(h_n2 > 0)) {
+      R.ctl.flags = LZ_BAD_V0;
+      return;
+    }
+    {
+      const double nrm = std::sqrt(h_n2);
+      ACHI_CUDA(cudaMemcpyAsync(misc + 3, &nrm, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+    }
+    K.scale(ws.q(0), v0, misc + 3, true);
+    double best = std::numeric_limits<double>::infinity();
+    int matvecs = 0;
+    while (matvecs < max_iter) {
+      ACHI_CUDA(cudaMemcpyAsync(ws.qcur.p, ws.q(0), sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                                ctx.stream));
+      LanczosCtl* ch = ws.ctl_h.p;
+      *ch = LanczosCtl{0, matvecs, block, max_iter, 0, 0, 0, 0, tol, best};
+      ACHI_CUDA(cudaMemcpyAsync(ws.ctl.p, ch, sizeof(LanczosCtl), cudaMemcpyHostToDevice, ctx.stream));
+      apply(ws.qcur.p, ws.w.p);
+      for (int j = 0;;) {
+        launch_tridiag(launch_orth(0, 0), ctx.stream);
+        ACHI_CUDA(cudaMemcpyAsync(ch, ws.ctl.p, sizeof(LanczosCtl), cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+        if (ch->j == j) break;
+        j = ch->j;
+        apply(ws.qcur.p, ws.w.p);
+      }
+      const LanczosStatus st = K.read_status();  // syncs the stream
+      const LanczosCtl cs = *ch;
+      matvecs = cs.matvecs;
+      const int k = cs.j + 1;
+      const bool breakdown = st.bnorm <= 1e-14 * std::max(1.0, std::fabs(st.theta));
+      K.axpy(ws.q(0), k, ws.s(), 1.0, nullptr, ws.ritz.p, true);
+      K.norm_from_partials(misc + 4);
+      K.scale(ws.ritz.p, ws.ritz.p, misc + 4, true);
+      apply(ws.ritz.p, ws.w.p);
+      ++matvecs;
+      K.dots(ws.ritz.p, 1, ws.w.p, misc + 5);
+      K.axpy(ws.ritz.p, 1, misc + 5, -1.0, ws.w.p, ws.tmp.p, true);
+      residual_kernel<<<1, RED_THREADS, 0, ctx.stream>>>(ws.partials.p, K.nb, misc + 5, misc,
+                                                         K.dev_status());
+      ACHI_LAUNCHED(ctx);
+      const LanczosStatus rs = K.read_status();
+      best = std::min(best, rs.res);
+      R.st = rs;
+      R.ctl = cs;
+      R.ctl.matvecs = matvecs;
+      R.ctl.best = best;
+      if (rs.res <= tol * std::max(1.0, std::fabs(rs.ev))) {
+        if (out != ws.ritz.p)
+          ACHI_CUDA(cudaMemcpyAsync(out, ws.ritz.p, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                                    ctx.stream));
+        R.ctl.flags = LZ_CONVERGED;
+        return;
+      }
+      if (breakdown) {
+        // q = normalize(ritz + 1e-8 * tmp / ||tmp||)
+        K.axpy(ws.tmp.p, 1, misc + 1, 1.0, ws.ritz.p, ws.q(0), true);
+        K.norm_from_partials(misc + 4);
+        K.scale(ws.q(0), ws.q(0), misc + 4, true);
+      } else {
+        ACHI_CUDA(cudaMemcpyAsync(ws.q(0), ws.ritz.p, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                                  ctx.stream));
+      }
+    }
+    R.ctl.matvecs = matvecs;
+    R.ctl.best = best;
+    R.ctl.flags = LZ_NONCONVERGED;
+    return;
+  }
+
+  // ---- graph mode: the whole eigensolve as one graph ----
+  //   norm2(v0); init (decides whether the restart loop runs); q_0 = v0 / ||v0||
+  //   WHILE restart {
+  //     qcur = q_0; cycle init; w = H q_0
+  //     WHILE step { orthogonalise + (aux stream) tridiagonal/decision || w = H q_{j+1} }
+  //     ritz = normalize(Q s); w = H ritz; ev = ritz.w; tmp = w - ev ritz; decide;
+  //     q_0 = ritz or the breakdown restart vector; out = ritz once converged
+  //   }
+  if (!lg.exec || lg.key != key) {
     const auto tb = std::chrono::steady_clock::now();
     ++builds;
     // keep the executable graph: a graph of the same topology (another shape
@@ -945,22 +1109,62 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
     lg.exec = nullptr;
     lg.reset();
     ACHI_CUDA(cudaGraphCreate(&lg.graph, 0));
-    cudaGraphConditionalHandle handle;
-    ACHI_CUDA(cudaGraphConditionalHandleCreate(&handle, lg.graph, 1, cudaGraphCondAssignDefault));
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = handle;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t node;
-    ACHI_CUDA(cudaGraphAddNode(&node, lg.graph, nullptr, 0, &cp));
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
-    const int64_t l0 = ctx.launches;
-    ACHI_CUDA(cudaStreamBeginCaptureToGraph(ctx.stream, body, nullptr, nullptr, 0,
-                                            cudaStreamCaptureModeRelaxed));
+    int64_t l0 = ctx.launches;
+    std::vector<cudaGraphNode_t> leaves;
+    auto begin = [&](cudaGraph_t g, const cudaGraphNode_t* deps, size_t nd) {
+      ACHI_CUDA(cudaStreamBeginCaptureToGraph(ctx.stream, g, deps, nullptr, nd,
+                                              cudaStreamCaptureModeRelaxed));
+    };
+    auto finish = [&](bool want_leaves) {
+      if (want_leaves) {
+        cudaStreamCaptureStatus cs;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        ACHI_CUDA(cudaStreamGetCaptureInfo(ctx.stream, &cs, nullptr, nullptr, &deps, &nd));
+        leaves.assign(deps, deps + nd);
+      }
+      cudaGraph_t captured;
+      ACHI_CUDA(cudaStreamEndCapture(ctx.stream, &captured));
+    };
+    auto add_while = [&](cudaGraph_t parent, cudaGraphConditionalHandle h) {
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t node;
+      ACHI_CUDA(cudaGraphAddNode(&node, parent, leaves.data(), leaves.size(), &cp));
+      return std::make_pair(node, cp.conditional.phGraph_out[0]);
+    };
     try {
+      cudaGraphConditionalHandle outer, inner;
+      ACHI_CUDA(cudaGraphConditionalHandleCreate(&outer, lg.graph, 0, 0));
+      // prologue
+      begin(lg.graph, nullptr, 0);
+      device_norm2(ctx, v0, n, misc + 2);
+      eig_init_kernel<<<1, 1, 0, ctx.stream>>>(misc, ws.ctl.p, block, max_iter, tol, outer);
+      ACHI_LAUNCHED(ctx);
+      K.scale(ws.q(0), v0, misc + 3, true);
+      finish(true);
+      lg.once_launches = ctx.launches - l0;
+      auto [onode, obody] = add_while(lg.graph, outer);
+      (void)onode;
+      ACHI_CUDA(cudaGraphConditionalHandleCreate(&inner, obody, 0, 0));
+      // restart cycle, part 1
+      l0 = ctx.launches;
+      begin(obody, nullptr, 0);
+      ACHI_CUDA(cudaMemcpyAsync(ws.qcur.p, ws.q(0), sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                                ctx.stream));
+      eig_cycle_kernel<<<1, 1, 0, ctx.stream>>>(ws.ctl.p, inner);
+      ACHI_LAUNCHED(ctx);
+      apply(ws.qcur.p, ws.w.p);  // w = H q_0; every later step's matvec runs inside the loop
+      finish(true);
+      auto [inode, ibody] = add_while(obody, inner);
+      // inner loop body
+      const int64_t l1 = ctx.launches;
+      begin(ibody, nullptr, 0);
       if (fused) {
-        FusedStepArgs fa{orth_args(handle, 1), fused_h, ws.bar.p};
+        FusedStepArgs fa{orth_args(inner, 1), fused_h, ws.bar.p};
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(orth_grid);
         lc.blockDim = dim3(ORTH_THREADS);
@@ -976,7 +1180,7 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
       } else {
         // orthogonalise step j; then the tridiagonal/decision kernel on the aux
         // stream runs concurrently with the (speculative) matvec of q_{j+1}
-        const OrthArgs oa = launch_orth(handle, 1);
+        const OrthArgs oa = launch_orth(inner, 1);
         ACHI_CUDA(cudaEventRecord(ctx.ev_fork, ctx.stream));
         ACHI_CUDA(cudaStreamWaitEvent(ctx.aux, ctx.ev_fork, 0));
         launch_tridiag(oa, ctx.aux);
@@ -984,17 +1188,41 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
         apply(ws.qcur.p, ws.w.p);
         ACHI_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_join, 0));
       }
+      finish(false);
+      lg.body_launches = ctx.launches - l1;
+      // restart cycle, part 2: Ritz vector, explicit residual, restart decision
+      const int64_t l2 = ctx.launches;
+      begin(obody, &inode, 1);
+      K.axpy(ws.q(0), LANCZOS_BLOCK, ws.s(), 1.0, nullptr, ws.ritz.p, true, ws.ctl.p);
+      K.norm_from_partials(misc + 4);
+      K.scale(ws.ritz.p, ws.ritz.p, misc + 4, true);
+      apply(ws.ritz.p, ws.w.p);
+      K.dots(ws.ritz.p, 1, ws.w.p, misc + 5);
+      K.axpy(ws.ritz.p, 1, misc + 5, -1.0, ws.w.p, ws.tmp.p, true);
+      eig_decide_kernel<<<1, RED_THREADS, 0, ctx.stream>>>(ws.partials.p, K.nb, misc + 5, misc,
+                                                           K.dev_status(), ws.ctl.p, outer);
+      ACHI_LAUNCHED(ctx);
+      K.axpy(ws.tmp.p, 1, misc + 1, 1.0, ws.ritz.p, ws.q(0), true);
+      K.norm_from_partials(misc + 4);
+      {
+        const int blocks = static_cast<int>(std::min<long>(cdiv(n, 256), 4L * ctx.num_sms));
+        eig_restart_kernel<<<blocks, 256, 0, ctx.stream>>>(ws.q(0), ws.ritz.p, out, n, misc + 4,
+                                                           ws.ctl.p);
+        ACHI_LAUNCHED(ctx);
+      }
+      finish(false);
+      lg.cycle_launches = (l1 - l0) + (ctx.launches - l2);
     } catch (...) {
       cudaGraph_t dummy;
-      cudaStreamEndCapture(ctx.stream, &dummy);
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(ctx.stream, &cs);
+      if (cs != cudaStreamCaptureStatusNone) cudaStreamEndCapture(ctx.stream, &dummy);
+      cudaGetLastError();
       lg.reset();
       if (old_exec) cudaGraphExecDestroy(old_exec);
       throw;
     }
-    cudaGraph_t captured;
-    ACHI_CUDA(cudaStreamEndCapture(ctx.stream, &captured));
-    lg.body_launches = ctx.launches - l0;
-    ctx.launches = l0;  // counted per executed iteration below
+    ctx.launches -= lg.once_launches + lg.cycle_launches + lg.body_launches;  // counted per execution
     static const bool exec_update = [] {
       const char* e = std::getenv("ACHI_GRAPH_UPDATE");
       return !(e && e[0] == '0');
@@ -1017,70 +1245,40 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
     lg.key = key;
     build_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - tb).count();
   }
-
-  double best = std::numeric_limits<double>::infinity();
-  int matvecs = 0;
-  while (matvecs < max_iter) {
-    // one restart cycle (linalg.cpp:126-150): q_0 is in the basis; qcur = q_0
-    ACHI_CUDA(cudaMemcpyAsync(ws.qcur.p, ws.q(0), sizeof(double) * n, cudaMemcpyDeviceToDevice,
-                              ctx.stream));
-    LanczosCtl* ch = ws.ctl_h.p;
-    *ch = LanczosCtl{0, matvecs, block, max_iter, 0, 0, tol};
-    ACHI_CUDA(cudaMemcpyAsync(ws.ctl.p, ch, sizeof(LanczosCtl), cudaMemcpyHostToDevice, ctx.stream));
-    apply(ws.qcur.p, ws.w.p);  // w = H q_0; every later matvec runs inside the loop
-    if (use_graph) {
-      ACHI_CUDA(cudaGraphLaunch(lg.exec, ctx.stream));
-    } else {
-      for (int j = 0;;) {  // host-stepped: the tridiagonal kernel advances j unless the loop ends
-        launch_tridiag(launch_orth(0, 0), ctx.stream);
-        ACHI_CUDA(cudaMemcpyAsync(ch, ws.ctl.p, sizeof(LanczosCtl), cudaMemcpyDeviceToHost, ctx.stream));
-        ctx.sync();
-        if (ch->j == j) break;
-        j = ch->j;
-        apply(ws.qcur.p, ws.w.p);
-      }
-    }
-    ACHI_CUDA(cudaMemcpyAsync(ch, ws.ctl.p, sizeof(LanczosCtl), cudaMemcpyDeviceToHost, ctx.stream));
-    const LanczosStatus st = K.read_status();  // syncs the stream
-    const LanczosCtl cs = *ch;
-    if (use_graph) ctx.launches += lg.body_launches * cs.steps;
-    matvecs = cs.matvecs;
-    const int k = cs.j + 1;
-    const double theta = st.theta, bnorm = st.bnorm;
-    const bool breakdown = bnorm <= 1e-14 * std::max(1.0, std::fabs(theta));
-    // ritz = normalize(sum_i s_i q_i)
-    K.axpy(ws.q(0), k, ws.s(), 1.0, nullptr, ws.ritz.p, true);
-    K.norm_from_partials(misc + 4);
-    K.scale(ws.ritz.p, ws.ritz.p, misc + 4, true);
-    apply(ws.ritz.p, ws.w.p);
-    ++matvecs;
-    // ev = ritz . w ; tmp = w - ev ritz ; res = ||tmp||
-    K.dots(ws.ritz.p, 1, ws.w.p, misc + 5);
-    K.axpy(ws.ritz.p, 1, misc + 5, -1.0, ws.w.p, ws.tmp.p, true);
-    residual_kernel<<<1, RED_THREADS, 0, ctx.stream>>>(ws.partials.p, K.nb, misc + 5, misc,
-                                                       K.dev_status());
-    ACHI_LAUNCHED(ctx);
-    const LanczosStatus rs = K.read_status();
-    best = std::min(best, rs.res);
-    if (rs.res <= tol * std::max(1.0, std::fabs(rs.ev))) {
-      if (out != ws.ritz.p)
-        ACHI_CUDA(cudaMemcpyAsync(out, ws.ritz.p, sizeof(double) * n, cudaMemcpyDeviceToDevice,
-                                  ctx.stream));
-      return EigsOut{rs.ev, matvecs, rs.res};
-    }
-    if (breakdown) {
-      // q = normalize(ritz + 1e-8 * tmp / ||tmp||)
-      K.axpy(ws.tmp.p, 1, misc + 1, 1.0, ws.ritz.p, ws.q(0), true);
-      K.norm_from_partials(misc + 4);
-      K.scale(ws.q(0), ws.q(0), misc + 4, true);
-    } else {
-      ACHI_CUDA(cudaMemcpyAsync(ws.q(0), ws.ritz.p, sizeof(double) * n, cudaMemcpyDeviceToDevice,
-                                ctx.stream));
-    }
+  ACHI_CUDA(cudaGraphLaunch(lg.exec, ctx.stream));
+  LanczosResult* R = ws.res_h.p;
+  ACHI_CUDA(cudaMemcpyAsync(&R->ctl, ws.ctl.p, sizeof(LanczosCtl), cudaMemcpyDeviceToHost, ctx.stream));
+  ACHI_CUDA(cudaMemcpyAsync(&R->st, K.dev_status(), sizeof(LanczosStatus), cudaMemcpyDeviceToHost,
+                            ctx.stream));
+  ws.pend_body = lg.body_launches;
+  ws.pend_cycle = lg.cycle_launches;
+  ws.pend_once = lg.once_launches;
+  if (&lg == &local) {
+    // a one-off graph must outlive its execution
+    ctx.sync();
   }
-  Error e(ACHI_E_EIGEN_NONCONVERGENCE, "eigs_lowest: no convergence within max_iter");
-  e.residual = best;
-  throw e;
+}
+
+EigsOut eigs_finish(Ctx& ctx, LanczosWs& ws) {
+  const LanczosResult& R = *ws.res_h.p;
+  if (ws.pend_graph)
+    ctx.launches += ws.pend_once + ws.pend_cycle * R.ctl.cycles + ws.pend_body * R.ctl.steps;
+  ws.pend_graph = false;
+  if (R.ctl.flags & LZ_BAD_V0) fail(ACHI_E_INVALID_MATRIX, "eigs_lowest: v0 must have norm > 0");
+  if (!(R.ctl.flags & LZ_CONVERGED)) {
+    Error e(ACHI_E_EIGEN_NONCONVERGENCE, "eigs_lowest: no convergence within max_iter");
+    e.residual = R.ctl.best;
+    throw e;
+  }
+  return EigsOut{R.st.ev, R.ctl.matvecs, R.st.res};
+}
+
+EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long dim,
+                    const double* v0, double tol, int max_iter, double* out, int graph_slot,
+                    uint64_t graph_key, const HeffOps* small_op) {
+  eigs_lowest_async(ctx, ws, apply, n, dim, v0, tol, max_iter, out, graph_slot, graph_key, small_op);
+  ctx.sync();
+  return eigs_finish(ctx, ws);
 }
 
 }  // namespace achi

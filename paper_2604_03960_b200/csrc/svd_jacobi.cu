@@ -467,6 +467,9 @@ __global__ void __launch_bounds__(JT, 1) jacobi_cluster_kernel(ClArgs a) {
       break;
     }
   }
+  // no CTA may leave (and free its shared memory) while another is still
+  // reading its meas_slot in the stop reduction above
+  cl.sync();
   // after whole sweeps every block is back at its round-0 owner
   circle_pair_ns(nb, 0, p, ba, bb);
   const double* X = X0 + buf * bufsz;
@@ -1009,8 +1012,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   bool cluster = ldg <= CL_ROWS && npairs <= CL_MAXP;
   if (cluster && npairs > 8) {
     // clusters beyond the portable 8 CTAs: only if the device can place one
-    static int placeable[CL_MAXP + 1] = {};
-    if (placeable[npairs] == 0) {
+    const int placeable = per_device_once("jacobi_cluster_placeable:" + std::to_string(npairs), ctx.device, [&] {
       ACHI_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       ACHI_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(cluster_smem(CL_ROWS))));
@@ -1026,12 +1028,12 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
       q.attrs = qa;
       q.numAttrs = 1;
       int nclusters = 0;
-      placeable[npairs] =
-          (cudaOccupancyMaxActiveClusters(&nclusters, jacobi_cluster_kernel, &q) == cudaSuccess &&
-           nclusters > 0) ? 1 : -1;
+      const int ok = (cudaOccupancyMaxActiveClusters(&nclusters, jacobi_cluster_kernel, &q) == cudaSuccess &&
+                      nclusters > 0) ? 1 : -1;
       cudaGetLastError();
-    }
-    cluster = placeable[npairs] > 0;
+      return ok;
+    });
+    cluster = placeable > 0;
   }
   // pad columns: rows side -> columns >= m_true (theta rows (l,s1), padded l last);
   // cols side with padding -> columns (s2, jr) with jr >= chr_true (d = 2 on the padded path)
@@ -1101,12 +1103,11 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   if (cluster) {
     const int rows_pad = static_cast<int>(((ldg + 15) / 16) * 16);
     const size_t smem = cluster_smem(rows_pad);
-    static bool attr = false;
-    if (!attr) {
+    per_device_once("jacobi_cluster_kernel", ctx.device, [] {
       ACHI_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(cluster_smem(CL_ROWS))));
-      attr = true;
-    }
+      return 1;
+    });
     const long jstride = static_cast<long>(MAX_SWEEPS) * (nb - 1);
     double* jrec = nullptr;
     unsigned char* jflag = nullptr;
@@ -1168,14 +1169,13 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     launches = std::min(batch, nsw);
     if (V) {
       const size_t rs = replay_smem(npairs, ng);
-      static bool rattr = false;
-      if (!rattr) {
+      per_device_once("v_replay_kernel", ctx.device, [] {
         ACHI_CUDA(cudaFuncSetAttribute(
             v_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
             static_cast<int>(std::max(replay_smem(CL_MAXP_DB, CL_MAXP_DB * JW),
                                       replay_smem(CL_MAXP, CL_MAXP * JW)))));
-        rattr = true;
-      }
+        return 1;
+      });
       dim3 grid(cdiv(ng, RP_ROWS), batch);
       v_replay_kernel<<<grid, JT, rs, ctx.stream>>>(V, vstride, ng, nb, npairs, jrec, jflag, jstride,
                                                     sweeps_dev, v_init);
@@ -1185,15 +1185,14 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   } else {
     const size_t smem = stream_smem();
     void* kern = reinterpret_cast<void*>(jacobi_stream_kernel);
-    static int mb = 0;
-    if (mb == 0) {
+    const int mb = per_device_once("jacobi_stream_kernel", ctx.device, [&] {
       ACHI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
       int per_sm = 0;
       ACHI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, JT, smem));
-      mb = per_sm * ctx.num_sms;
-      if (mb < 1) fail(ACHI_E_CUDA, "svd: Jacobi kernel cannot be resident");
-    }
+      if (per_sm < 1) fail(ACHI_E_CUDA, "svd: Jacobi kernel cannot be resident");
+      return per_sm * ctx.num_sms;
+    });
     if (npairs > mb) fail(ACHI_E_SIZE_GUARD, "svd: matrix too wide for one cooperative launch");
     static const int stream_cross = [] {  // ACHI_JACOBI_CROSS_STREAM: inner schedule (0 full, 4 cross)
       const char* e = std::getenv("ACHI_JACOBI_CROSS_STREAM");

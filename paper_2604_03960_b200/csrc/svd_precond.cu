@@ -496,12 +496,11 @@ bool qr_precond_applicable(int mr, int nr) { return mr <= PQ_MAX && nr <= PQ_MAX
 void qr_precond(Ctx& ctx, double* G, long ldg, int mr, int ng, int nr, int pad_mod, int pad_lim,
                 double* V0) {
   if (!qr_precond_applicable(mr, nr)) fail(ACHI_E_INTERNAL, "qr_precond: shape beyond the cluster kernel");
-  static bool attr = false;
-  if (!attr) {
+  per_device_once("qr_precond_kernel", ctx.device, [] {
     ACHI_CUDA(cudaFuncSetAttribute(qr_precond_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(sizeof(PqSmem))));
-    attr = true;
-  }
+    return 1;
+  });
   static const bool prof_on = std::getenv("ACHI_QR_PROF") != nullptr;
   static DevArr<long long> profbuf;
   PqArgs a{G, ldg, mr, ng, nr, pad_mod, pad_lim, std::min(nr, mr), V0, nullptr};
