@@ -1102,6 +1102,8 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
   if (!lg.exec || lg.key != key) {
     const auto tb = std::chrono::steady_clock::now();
     ++builds;
+    // every buffer a captured kernel uses is sized before capture
+    ctx.red.reserve(static_cast<size_t>(red_blocks(ctx, n)) * 2 + 8);
     // keep the executable graph: a graph of the same topology (another shape
     // of this bond) is applied to it by cudaGraphExecUpdate, much cheaper than
     // a new instantiation; anything else re-instantiates
