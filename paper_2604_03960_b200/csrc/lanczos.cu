@@ -529,6 +529,7 @@ struct OrthArgs {
 
 constexpr int ORTH_THREADS = 256;
 
+template <int NT>
 __device__ void orth_partials(const double* Q, long stride, int nv, const double* w, long b0,
                               long b1, double* part, double (*sh)[65]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -552,7 +553,7 @@ __device__ void orth_partials(const double* Q, long stride, int nv, const double
   for (int v = threadIdx.x; v < nv; v += blockDim.x) {
     double t = 0.0;
 #pragma unroll
-    for (int w8 = 0; w8 < ORTH_THREADS / 32; ++w8) t += sh[w8][v];
+    for (int w8 = 0; w8 < NT / 32; ++w8) t += sh[w8][v];
     part[static_cast<long>(v) * gridDim.x + blockIdx.x] = t;  // [v][block]: coalesced reduce
   }
   __syncthreads();
@@ -583,9 +584,10 @@ __device__ __forceinline__ double grid_sum(const double* p, int lane) {
 }
 
 // every block: coef[v] = sum_b part[v][b]; one warp per coefficient
+template <int NT>
 __device__ void orth_reduce(const double* part, int nv, double* coef) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int v = warp; v < nv; v += ORTH_THREADS / 32) {
+  for (int v = warp; v < nv; v += NT / 32) {
     const double t = grid_sum(part + static_cast<long>(v) * gridDim.x, lane);
     if (lane == 0) coef[v] = t;
   }
@@ -598,11 +600,15 @@ __device__ void orth_reduce(const double* part, int nv, double* coef) {
 // Step j, part 1 (every CTA of a cooperative grid): w <- w - Q (Q^T w) twice,
 // beta_j = ||w||, q_{j+1} = w / beta_j into the basis and into qcur (the next
 // matvec input); block 0 stores alpha_j, beta_j.
-__device__ void orth_step(const OrthArgs& a) {
-  __shared__ double sh[ORTH_THREADS / 32][65];
+// NT threads per CTA of a cooperative grid.  (A one-cluster variant -- 8 or
+// 16 CTAs, hardware cluster barriers, a C-way all-reduce -- measured slower on
+// C3: 33k vs 25k cycles per step, the passes lose memory-level parallelism.)
+template <int NT>
+__device__ void orth_step_t(const OrthArgs& a) {
+  __shared__ double sh[NT / 32][65];
   __shared__ double coef[64];
   __shared__ double red[32];
-  cg::grid_group grid = cg::this_grid();
+  auto gsync = [] { cg::this_grid().sync(); };
   const int j = a.ctl->j;  // advanced only by the tridiagonal kernel, after this one
   const bool prof = a.prof && blockIdx.x == 0 && threadIdx.x == 0;
   const unsigned long long c0 = prof ? clock64() : 0;
@@ -610,11 +616,11 @@ __device__ void orth_step(const OrthArgs& a) {
   const long chunk = (a.n + gridDim.x - 1) / gridDim.x;
   const long b0 = static_cast<long>(blockIdx.x) * chunk, b1 = min(a.n, b0 + chunk);
   // pass 1: h1 = Q^T w
-  orth_partials(a.Q, a.stride, nv, a.w, b0, b1, a.pa, sh);
+  orth_partials<NT>(a.Q, a.stride, nv, a.w, b0, b1, a.pa, sh);
   const unsigned long long c1 = prof ? clock64() : 0;
-  grid.sync();
+  gsync();
   const unsigned long long c2 = prof ? clock64() : 0;
-  orth_reduce(a.pa, nv, coef);
+  orth_reduce<NT>(a.pa, nv, coef);
   // pass 2: w <- w - Q h1 ; h2 partials
   double nrm1 = 0.0;  // ||w'||^2 partial, reduced with the second dots
   for (long x = b0 + threadIdx.x; x < b1; x += blockDim.x) {
@@ -625,10 +631,10 @@ __device__ void orth_step(const OrthArgs& a) {
   nrm1 = block_sum(nrm1, red);
   if (threadIdx.x == 0) a.pb[static_cast<long>(nv) * gridDim.x + blockIdx.x] = nrm1;
   __syncthreads();
-  orth_partials(a.Q, a.stride, nv, a.w, b0, b1, a.pb, sh);
+  orth_partials<NT>(a.Q, a.stride, nv, a.w, b0, b1, a.pb, sh);
   const double alpha_j = coef[nv - 1];
-  grid.sync();
-  orth_reduce(a.pb, nv + 1, coef);
+  gsync();
+  orth_reduce<NT>(a.pb, nv + 1, coef);
   // beta_j = ||w' - Q h2|| = sqrt(||w'||^2 - ||h2||^2) (Q orthonormal) when the
   // second projection is small against w' (always, short of an invariant
   // subspace); otherwise the norm is formed explicitly after one more barrier.
@@ -648,7 +654,7 @@ __device__ void orth_step(const OrthArgs& a) {
   if (!pyth) {
     nrm = block_sum(nrm, red);
     if (threadIdx.x == 0) a.pc[blockIdx.x] = nrm;
-    grid.sync();
+    gsync();
     if (threadIdx.x < 32) {
       const double t = grid_sum(a.pc, threadIdx.x);
       if (threadIdx.x == 0) bn_s = sqrt(t);
@@ -685,6 +691,7 @@ __device__ void orth_step(const OrthArgs& a) {
 // the reference's step decision (linalg.cpp:141-148), which advances ctl->j or
 // ends the loop.  In the graph it runs concurrently with the speculative
 // matvec of q_{j+1} (wasted only on the last step of a cycle).
+__device__ void orth_step(const OrthArgs& a) { orth_step_t<ORTH_THREADS>(a); }
 __global__ void __launch_bounds__(ORTH_THREADS) lanczos_orth_kernel(OrthArgs a) { orth_step(a); }
 
 __device__ void tridiag_step(const OrthArgs& a) {
