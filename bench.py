@@ -179,11 +179,11 @@ def cpu_svd_timings(n, threads_all, reps_all=3, budget_s=240.0):
     single repetition each and are skipped (reported as null) once the budget is
     spent."""
     from oracle import oracle as O
-    rng = np.random.default_rng(1234)
-    a_r = rng.standard_normal((n, n))
-    a_c = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    a_r = np.random.default_rng(1234).standard_normal((n, n))
+    a_c = complex_literal(n)
     t_start = time.perf_counter()
     out = {}
+    sig = {}
 
     def timed(kind, threads, reps):
         O.set_threads(threads)
@@ -191,9 +191,9 @@ def cpu_svd_timings(n, threads_all, reps_all=3, budget_s=240.0):
         for _ in range(reps):
             t = time.perf_counter()
             if kind == "c128":
-                O.svd_complex_sigma(a_c)
+                sig["c128"] = O.svd_complex_sigma(a_c)
             else:
-                O.svd(a_r)
+                sig["f64"] = O.svd(a_r)[1]
             runs.append(time.perf_counter() - t)
         runs.sort()
         return round(runs[len(runs) // 2] * 1e3, 1)
@@ -210,7 +210,42 @@ def cpu_svd_timings(n, threads_all, reps_all=3, budget_s=240.0):
                    f"{threads_all} threads: upper median of {reps_all}; 1 thread: one run "
                    f"(null: skipped, {budget_s:.0f} s budget)")
     out["seconds_spent"] = round(time.perf_counter() - t_start, 1)
-    return out
+    return out, sig
+
+
+def complex_literal(n):
+    """The cmd_svd_bench matrix (bench.cpp:646-648): complex Gaussian, re and im ~ N(0, 1)
+    (numpy default_rng(4321) here, the reference draws from mt19937_64)."""
+    rng = np.random.default_rng(4321)
+    return rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+
+
+def svd_complex_part(ctx, args):
+    """The reference literal itself: complex n x n (n = 2 chi = 4096) svd_full on the
+    device (achi_svd_complex_device: the realified matrix on the Jacobi engine).  One
+    timed call after the data is resident (the call is seconds long)."""
+    import torch
+    n = 2 * args.svd_chi
+    a = torch.from_numpy(complex_literal(n)).cuda()
+    s = torch.empty(n, dtype=torch.float64, device="cuda")
+    u = torch.empty(n, n, dtype=torch.complex128, device="cuda")
+    vd = torch.empty(n, n, dtype=torch.complex128, device="cuda")
+    torch.cuda.synchronize()
+    ctx.flush_l2(256 << 20)
+    ctx.timer_start()
+    sweeps = ctx.svd_complex_device(a.data_ptr(), n, n, s.data_ptr(), u.data_ptr(), vd.data_ptr())
+    ms = ctx.timer_stop()
+    k = 64
+    rec = float(((u[:k] * s) @ vd - a[:k]).abs().max() / s[0])
+    fro = float((a.abs() ** 2).sum())
+    out = {"svd_chi2048_c128_ms": round(ms, 1), "svd_chi2048_c128_jacobi_sweeps": sweeps,
+           "svd_chi2048_c128_recon_err": rec,
+           "svd_chi2048_c128_sum_sigma2_relerr": abs(float((s * s).sum()) - fro) / fro,
+           "svd_chi2048_c128_note": "complex128 4096x4096 Gaussian (the cmd_svd_bench literal), "
+                                    "U, sigma, V^dagger on the device via the realified 8192x8192 "
+                                    "real Jacobi SVD"}
+    del a, u, vd
+    return out, s.cpu().numpy()
 
 
 def cpu_threads():
@@ -304,9 +339,14 @@ def run_ours(args, dist):
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
+    gpu_csig = None
     if not args.skip_svd:
         log("svd part")
         out.update(svd_part(ctx, args))
+        if not args.skip_complex_svd:
+            log("complex svd part")
+            cpart, gpu_csig = svd_complex_part(ctx, args)
+            out.update(cpart)
     # K1 at the large-chi end of the metric's range (chi_max = 1024), measured inside a
     # real sweep: N=100, fixed chi=1024 (every bond 10..89 at chi=1024 from sweep 5 on)
     if not args.skip_heff_insweep:
@@ -323,7 +363,11 @@ def run_ours(args, dist):
         out["cpu_baseline"] = cpu_baseline_sample(spec, cfg, ch, last)
         if not args.skip_svd:
             log("cpu svd baseline")
-            cb = cpu_svd_timings(2 * args.svd_chi, cpu_threads(), budget_s=args.cpu_svd_budget_s)
+            cb, cpu_sig = cpu_svd_timings(2 * args.svd_chi, cpu_threads(), budget_s=args.cpu_svd_budget_s)
+            if gpu_csig is not None and "c128" in cpu_sig:
+                # parity of the complex literal at full size: device vs the oracle's zgesdd
+                ref = cpu_sig["c128"]
+                out["svd_chi2048_c128_sigma_vs_zgesdd"] = float(np.abs(gpu_csig - ref).max() / ref[0])
             out["cpu_baseline"]["svd_chi2048"] = cb
             thr = cpu_threads()
             out["svd_chi2048_cpu_ms"] = {k: v for k, v in cb.items() if k.endswith("_ms")}
@@ -542,7 +586,7 @@ def run_reference(args, dist):
                 break
         ch.close()
     svd = None if args.skip_svd else cpu_svd_timings(2 * args.svd_chi, threads, reps_all=3,
-                                                      budget_s=0.0)
+                                                      budget_s=0.0)[0]
     return {"metric": METRIC, "value": round(v, 4), "unit": "s/sweep", "impl": "reference",
             "n_gpus": dist.world, "steps": len(walls), "warmup": W,
             "ms_per_step": round(v * 1e3, 2), "higher_is_better": False, "scaling": "weak",
@@ -579,6 +623,7 @@ def main():
     ap.add_argument("--ref-budget-s", type=float, default=600.0)
     ap.add_argument("--cpu-svd-budget-s", type=float, default=150.0)
     ap.add_argument("--skip-shards", action="store_true")
+    ap.add_argument("--skip-complex-svd", action="store_true")
     ap.add_argument("--skip-heff-insweep", action="store_true")
     ap.add_argument("--heff-sweep", type=int, default=5)
     ap.add_argument("--skip-real", action="store_true")

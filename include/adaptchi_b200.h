@@ -279,6 +279,21 @@ int achi_svd_batched_device(achi_ctx* ctx, int batch, int m, int n, const double
 int achi_svd_device(achi_ctx* ctx, int m, int n, const double* d_a, double* d_sigma,
                     double* d_u, double* d_vt, int* sweeps_out);
 
+/* Complex svd_full (linalg.cpp:11-48, 67-70; DenseMatrix = Eigen::MatrixXcd,
+ * tensor.hpp:15): a is m x n row-major complex128 as interleaved (re, im)
+ * doubles.  Outputs sigma[r] (non-increasing), u (m x r) and vdag = V^dagger
+ * (r x n), row-major interleaved, fix_phases applied (linalg.cpp:19-35: the
+ * first largest-|u| entry of each U column real and positive).  Computed on
+ * the real Jacobi engine through the realification [[Re, -Im], [Im, Re]]
+ * (svd_complex.cu).  Non-finite input -> ACHI_E_INVALID_MATRIX.  Replaces
+ * reference_svd for complex blocks, e.g. the cmd_svd_bench literal
+ * (bench.cpp:646-648). */
+int achi_svd_complex(achi_ctx* ctx, int m, int n, const double* a, double* sigma, double* u,
+                     double* vdag, int* sweeps_out);
+/* Same on device pointers (the caller guarantees finite input). */
+int achi_svd_complex_device(achi_ctx* ctx, int m, int n, const double* d_a, double* d_sigma,
+                            double* d_u, double* d_vdag, int* sweeps_out);
+
 /* Fused bond-select kernel (K7) on a host spectrum: entropy_from_spectrum
  * (mps.cpp:97-113), rank_for_discarded_weight (controller.cpp:134-148),
  * kept-rank logic (dmrg.cpp:113-136), controller_update
@@ -317,6 +332,20 @@ int achi_eigs_lowest_dense(achi_ctx* ctx, int dim, const double* h,
                            const double* v0, double tol, int max_iter,
                            double* eigenvalue, double* eigenvector,
                            int* matvecs, double* residual);
+
+/* eigs_lowest(const LinearMap&, dim, v0, tol, max_iter) (linalg.hpp:64-78,
+ * linalg.cpp:107-178) for an operator given as a host callback:
+ * fn(user, in, out, dim) must write out = H in for a real symmetric H (the
+ * host mirror passes complex Hermitian LinearMaps through their real
+ * 2 dim x 2 dim form).  The Lanczos iteration (basis, reorthogonalisation,
+ * tridiagonal solve, restarts) runs on the device, stepped from the host;
+ * every matvec copies the vector to the host, calls fn and copies the result
+ * back.  Errors as achi_eigs_lowest_dense; a non-finite operator output ->
+ * ACHI_E_INVALID_MATRIX. */
+typedef void (*achi_matvec_fn)(void* user, const double* in, double* out, int64_t dim);
+int achi_eigs_lowest_callback(achi_ctx* ctx, int dim, achi_matvec_fn fn, void* user, const double* v0,
+                              double tol, int max_iter, double* eigenvalue, double* eigenvector,
+                              int* matvecs, double* residual);
 
 #ifdef __cplusplus
 }

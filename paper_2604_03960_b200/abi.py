@@ -28,6 +28,10 @@ ERROR_NAMES = {
 }
 
 
+# achi_matvec_fn: void (*)(void* user, const double* in, double* out, int64_t dim)
+MATVEC_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64)
+
+
 class ModelSpec(C.Structure):
     _fields_ = [("family", C.c_int32), ("n", C.c_int32), ("jx", C.c_double),
                 ("jy", C.c_double), ("jz", C.c_double), ("h", C.c_double),
@@ -174,6 +178,11 @@ def load():
         "achi_device_times": (C.c_int, [vp, C.c_int, C.c_int, dp]),
         "achi_device_times_ex": (C.c_int, [vp, C.c_int, C.c_int, dp, C.c_int]),
         "achi_ctx_set_lanczos_graph": (C.c_int, [vp, C.c_int]),
+        "achi_svd_complex": (C.c_int, [vp, C.c_int, C.c_int, dp, dp, dp, dp, P(C.c_int)]),
+        "achi_eigs_lowest_callback": (C.c_int, [vp, C.c_int, MATVEC_FN, C.c_void_p, dp, d, C.c_int,
+                                                dp, dp, P(C.c_int), dp]),
+        "achi_svd_complex_device": (C.c_int, [vp, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                              C.c_void_p, C.c_void_p, P(C.c_int)]),
         "achi_bond_select": (C.c_int, [vp, P(DmrgConfig), C.c_int, dp, P(BondState),
                                        C.c_int, C.c_int, P(TraceRow), P(VisitRecord)]),
         "achi_eigs_lowest_dense": (C.c_int, [vp, C.c_int, dp, dp, d, C.c_int, dp, dp,

@@ -171,6 +171,31 @@ class Context:
         self._check(self.lib.achi_svd(self.h, m, n, _dp(a), _dp(s), _dp(u), _dp(vt), C.byref(sw)))
         return u, s, vt, sw.value
 
+    def svd_complex(self, a):
+        """Complex svd_full (linalg.cpp:67-70 on a MatrixXcd): returns (u, sigma, vdag)
+        with A = u diag(sigma) vdag, fix_phases applied."""
+        a = np.ascontiguousarray(a, dtype=np.complex128)
+        if a.ndim != 2:
+            raise AchiError(2, "svd: expected a matrix")
+        m, n = a.shape
+        r = min(m, n)
+        s = np.zeros(r)
+        u = np.zeros((m, r), np.complex128)
+        vd = np.zeros((r, n), np.complex128)
+        sw = C.c_int()
+        self._check(self.lib.achi_svd_complex(self.h, m, n, a.view(np.float64).ctypes.data_as(
+            C.POINTER(C.c_double)), _dp(s), u.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)),
+            vd.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)), C.byref(sw)))
+        return u, s, vd
+
+    def svd_complex_device(self, d_a_ptr, m, n, d_sigma_ptr, d_u_ptr, d_vdag_ptr):
+        """Device-pointer complex svd_full (interleaved complex128); returns Jacobi sweeps."""
+        sw = C.c_int()
+        self._check(self.lib.achi_svd_complex_device(self.h, m, n, C.c_void_p(d_a_ptr),
+                                                     C.c_void_p(d_sigma_ptr), C.c_void_p(d_u_ptr),
+                                                     C.c_void_p(d_vdag_ptr), C.byref(sw)))
+        return sw.value
+
     def svd_batched(self, a):
         a = _f64(a)
         b, m, n = a.shape
@@ -202,6 +227,33 @@ class Context:
         self._check(self.lib.achi_eigs_lowest_dense(self.h, dim, _dp(h), _dp(v0), C.c_double(tol),
                                                     max_iter, C.byref(ev), _dp(vec), C.byref(mv),
                                                     C.byref(res)))
+        return ev.value, vec, mv.value, res.value
+
+    def eigs_lowest(self, matvec, v0, tol=1e-10, max_iter=200):
+        """eigs_lowest(LinearMap, dim, v0, tol, max_iter) (linalg.hpp:64-78) with a host
+        operator: matvec(x) -> H x for a real symmetric H (numpy in, numpy out).  The
+        Lanczos runs on the device; each matvec round-trips through the host.
+        Returns (eigenvalue, eigenvector, matvec_count, residual)."""
+        v0 = _f64(v0).ravel()
+        dim = v0.size
+        err = []
+
+        def cb(_user, pin, pout, n):
+            try:
+                x = np.ctypeslib.as_array(pin, shape=(n,)).copy()
+                y = np.asarray(matvec(x), dtype=np.float64).ravel()
+                np.ctypeslib.as_array(pout, shape=(n,))[:] = y
+            except Exception as e:  # noqa: BLE001 - surfaced after the call
+                err.append(e)
+                np.ctypeslib.as_array(pout, shape=(n,))[:] = np.nan
+        fn = abi.MATVEC_FN(cb)
+        ev, mv, res = C.c_double(), C.c_int(), C.c_double()
+        vec = np.zeros(dim)
+        rc = self.lib.achi_eigs_lowest_callback(self.h, dim, fn, None, _dp(v0), tol, max_iter,
+                                                C.byref(ev), _dp(vec), C.byref(mv), C.byref(res))
+        if err:
+            raise err[0]
+        self._check(rc)
         return ev.value, vec, mv.value, res.value
 
     def dgemm(self, a, b, a_kmajor=True, b_kmajor=False):

@@ -512,6 +512,42 @@ int achi_svd_device(achi_ctx* ctx, int m, int n, const double* d_a, double* d_si
   });
 }
 
+int achi_svd_complex_device(achi_ctx* ctx, int m, int n, const double* d_a, double* d_sigma,
+                            double* d_u, double* d_vdag, int* sweeps_out) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    if (m < 1 || n < 1) fail(ACHI_E_INVALID_MATRIX, "svd: matrix must be at least 1x1");
+    SvdWs ws;
+    const int sw = svd_complex_device(c, ws, d_a, m, n, d_sigma, d_u, d_vdag);
+    if (sweeps_out) *sweeps_out = sw;
+  });
+}
+
+int achi_svd_complex(achi_ctx* ctx, int m, int n, const double* a, double* sigma, double* u,
+                     double* vdag, int* sweeps_out) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    if (m < 1 || n < 1) fail(ACHI_E_INVALID_MATRIX, "svd: matrix must be at least 1x1");
+    const size_t mn2 = 2 * static_cast<size_t>(m) * n;
+    for (size_t i = 0; i < mn2; ++i)
+      if (!std::isfinite(a[i])) fail(ACHI_E_INVALID_MATRIX, "svd: non-finite entries");
+    const int r = std::min(m, n);
+    DevBuf dA, dS, dU, dV;
+    dA.reserve(mn2);
+    dS.reserve(r);
+    dU.reserve(2 * static_cast<size_t>(m) * r);
+    dV.reserve(2 * static_cast<size_t>(r) * n);
+    h2d(c, dA.p, a, mn2);
+    SvdWs ws;
+    const int sw = svd_complex_device(c, ws, dA.p, m, n, dS.p, dU.p, dV.p);
+    if (sigma) d2h(c, sigma, dS.p, r);
+    if (u) d2h(c, u, dU.p, 2 * static_cast<size_t>(m) * r);
+    if (vdag) d2h(c, vdag, dV.p, 2 * static_cast<size_t>(r) * n);
+    c.sync();
+    if (sweeps_out) *sweeps_out = sw;
+  });
+}
+
 int achi_bond_select(achi_ctx* ctx, const achi_dmrg_config* cfg, int n_sigma, const double* sigma,
                      achi_bond_state* state, int sweep, int bond, achi_trace_row* row,
                      achi_visit_record* visit) {
@@ -639,6 +675,45 @@ int achi_eigs_lowest_dense(achi_ctx* ctx, int dim, const double* h, const double
         [&](const double* in, double* out) {
           dense_gemv_kernel<<<cdiv(dim, 8), 256, 0, c.stream>>>(dH.p, dim, in, out);
           ACHI_LAUNCHED(c);
+        },
+        dim, dim, dV.p, tol, max_iter, dO.p);
+    d2h(c, eigenvector, dO.p, dim);
+    c.sync();
+    *eigenvalue = e.eigenvalue;
+    *matvecs = e.matvecs;
+    *residual = e.residual;
+  });
+}
+
+int achi_eigs_lowest_callback(achi_ctx* ctx, int dim, achi_matvec_fn fn, void* user, const double* v0,
+                              double tol, int max_iter, double* eigenvalue, double* eigenvector,
+                              int* matvecs, double* residual) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    if (dim < 1 || !fn) fail(ACHI_E_INVALID_MATRIX, "eigs_lowest: dim >= 1 and an operator are required");
+    DevBuf dV, dO;
+    dV.reserve(dim);
+    dO.reserve(dim);
+    h2d(c, dV.p, v0, dim);
+    std::vector<double> hin(dim), hout(dim);
+    LanczosWs ws;
+    // the host operator cannot run inside a graph: this call steps the Lanczos from the host
+    struct GraphMode {
+      Ctx& c;
+      int prev;
+      ~GraphMode() { c.lanczos_graph = prev; }
+    } gm{c, c.lanczos_graph};
+    c.lanczos_graph = 0;
+    EigsOut e = eigs_lowest(
+        c, ws,
+        [&](const double* in, double* out) {
+          d2h(c, hin.data(), in, dim);
+          c.sync();
+          fn(user, hin.data(), hout.data(), dim);
+          for (int i = 0; i < dim; ++i)
+            if (!std::isfinite(hout[i])) fail(ACHI_E_INVALID_MATRIX, "eigs_lowest: operator returned non-finite values");
+          h2d(c, out, hout.data(), dim);
+          c.sync();
         },
         dim, dim, dV.p, tol, max_iter, dO.p);
     d2h(c, eigenvector, dO.p, dim);

@@ -1250,7 +1250,15 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     col_norm_kernel<<<grid, 256, 0, ctx.stream>>>(G, gstride, ldg, ng, ng_real, pad_mod, pad_lim,
                                                   sig, ng);
     ACHI_LAUNCHED(ctx);
-    sort_kernel<<<batch, 1024, sizeof(double) * ng, ctx.stream>>>(sig, ng, ng, sorted, perm);
+    const size_t sort_smem = sizeof(double) * ng;
+    if (sort_smem > 48 * 1024) {  // n > 6144 (e.g. the realified complex 4096^2 literal)
+      if (sort_smem > 200 * 1024) fail(ACHI_E_SIZE_GUARD, "svd: too many columns for the rank sort");
+      per_device_once("sort_kernel", ctx.device, [] {
+        ACHI_CUDA(cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        return 1;
+      });
+    }
+    sort_kernel<<<batch, 1024, sort_smem, ctx.stream>>>(sig, ng, ng, sorted, perm);
     ACHI_LAUNCHED(ctx);
   }
   ACHI_CUDA(cudaMemcpyAsync(sweeps_host, sweeps_dev, sizeof(int) * launches, cudaMemcpyDeviceToHost,

@@ -84,4 +84,10 @@ void svd_phase_signs(Ctx& ctx, SvdWs& ws, const SvdResultDev& r, int kept);
 // Gather thin factors to device row-major buffers: U (m_true x r) and VT (r x n_true).
 void svd_gather(Ctx& ctx, SvdWs& ws, const SvdResultDev& r, int k, double* U, double* VT);
 
+// Complex svd_full (svd_complex.cu): a (m x n row-major, interleaved re/im,
+// device); sigma (r = min(m,n), device), U (m x r) and V^dagger (r x n),
+// row-major interleaved, fix_phases applied.  Returns the Jacobi sweeps.
+int svd_complex_device(Ctx& ctx, SvdWs& ws, const double* a, int m, int n, double* sigma, double* U,
+                       double* Vd);
+
 }  // namespace achi

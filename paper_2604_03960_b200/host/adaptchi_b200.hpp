@@ -2,14 +2,18 @@
 //
 // Header-only, C++17.  Names, argument meaning, defaults and exception types
 // follow /root/reference/proj/include/adaptchi/{errors,models,controller,mps,
-// linalg,dmrg}.hpp so that reference-style code and tests compile against the
-// B200 backend with a changed include.  Eigen types are replaced by small
-// value types (DenseMatrix is a real column-major matrix: the device path is
-// real FP64).  Every computation runs on the GPU through
-// include/adaptchi_b200.h; there is no host fallback.
+// linalg,dmrg,tensor}.hpp so that reference-style code and tests compile
+// against the B200 backend with a changed include.  Eigen types are replaced
+// by small value types with the reference's scalar type: DenseMatrix is a
+// complex column-major matrix (Eigen::MatrixXcd), CVector a complex vector;
+// real-valued blocks take the real FP64 device path, complex ones the complex
+// device SVD / the realified Lanczos.  Every computation runs
+// on the GPU through include/adaptchi_b200.h; there is no host fallback.
 #pragma once
 
 #include <cmath>
+#include <complex>
+#include <functional>
 #include <memory>
 #include <ostream>
 #include <stdexcept>
@@ -85,12 +89,17 @@ inline void check(int rc) {
 
 }  // namespace b200
 
-// Real column-major dense matrix (stands in for Eigen::MatrixXcd, tensor.hpp:15).
+// tensor.hpp:14-17
+using Cplx = std::complex<double>;
+using CVector = std::vector<Cplx>;
+using RVector = std::vector<double>;
+
+// Complex column-major dense matrix (stands in for Eigen::MatrixXcd, tensor.hpp:15).
 struct DenseMatrix {
   long r = 0, c = 0;
-  std::vector<double> d;
+  std::vector<Cplx> d;
   DenseMatrix() = default;
-  DenseMatrix(long rows, long cols) : r(rows), c(cols), d(static_cast<size_t>(rows * cols), 0.0) {}
+  DenseMatrix(long rows, long cols) : r(rows), c(cols), d(static_cast<size_t>(rows * cols), Cplx(0, 0)) {}
   static DenseMatrix Identity(long n, long m) {
     DenseMatrix x(n, m);
     for (long i = 0; i < std::min(n, m); ++i) x(i, i) = 1.0;
@@ -98,22 +107,79 @@ struct DenseMatrix {
   }
   long rows() const { return r; }
   long cols() const { return c; }
-  double& operator()(long i, long j) { return d[static_cast<size_t>(i + j * r)]; }
-  double operator()(long i, long j) const { return d[static_cast<size_t>(i + j * r)]; }
-  std::vector<double> row_major() const {
+  Cplx& operator()(long i, long j) { return d[static_cast<size_t>(i + j * r)]; }
+  Cplx operator()(long i, long j) const { return d[static_cast<size_t>(i + j * r)]; }
+  bool is_real() const {
+    for (const Cplx& x : d)
+      if (x.imag() != 0.0) return false;
+    return true;
+  }
+  std::vector<double> real_row_major() const {
     std::vector<double> o(d.size());
     for (long i = 0; i < r; ++i)
-      for (long j = 0; j < c; ++j) o[static_cast<size_t>(i * c + j)] = (*this)(i, j);
+      for (long j = 0; j < c; ++j) o[static_cast<size_t>(i * c + j)] = (*this)(i, j).real();
     return o;
   }
-  static DenseMatrix from_row_major(long rows, long cols, const double* p) {
+  std::vector<double> interleaved_row_major() const {
+    std::vector<double> o(2 * d.size());
+    for (long i = 0; i < r; ++i)
+      for (long j = 0; j < c; ++j) {
+        o[static_cast<size_t>(2 * (i * c + j))] = (*this)(i, j).real();
+        o[static_cast<size_t>(2 * (i * c + j) + 1)] = (*this)(i, j).imag();
+      }
+    return o;
+  }
+  static DenseMatrix from_real_row_major(long rows, long cols, const double* p) {
     DenseMatrix x(rows, cols);
     for (long i = 0; i < rows; ++i)
       for (long j = 0; j < cols; ++j) x(i, j) = p[i * cols + j];
     return x;
   }
+  static DenseMatrix from_interleaved_row_major(long rows, long cols, const double* p) {
+    DenseMatrix x(rows, cols);
+    for (long i = 0; i < rows; ++i)
+      for (long j = 0; j < cols; ++j) x(i, j) = Cplx(p[2 * (i * cols + j)], p[2 * (i * cols + j) + 1]);
+    return x;
+  }
 };
-using RVector = std::vector<double>;
+
+// Row-major complex tensor of small rank (tensor.hpp:26-120; contractions run
+// on the device through the mirror's operations, not here).
+class Tensor {
+ public:
+  Tensor() = default;
+  explicit Tensor(std::vector<long> shape) : shape_(std::move(shape)), data_(size_of(shape_), Cplx(0, 0)) {}
+  static size_t size_of(const std::vector<long>& shape) {
+    long n = 1;
+    for (long s : shape) {
+      if (s < 1) throw InvalidMatrix("tensor dimension must be >= 1");
+      n *= s;
+    }
+    return static_cast<size_t>(n);
+  }
+  const std::vector<long>& shape() const { return shape_; }
+  long dim(int axis) const { return shape_[static_cast<size_t>(axis)]; }
+  int rank() const { return static_cast<int>(shape_.size()); }
+  long size() const { return static_cast<long>(data_.size()); }
+  Cplx* data() { return data_.data(); }
+  const Cplx* data() const { return data_.data(); }
+  Cplx& operator()(long i, long j, long k) { return data_[static_cast<size_t>((i * shape_[1] + j) * shape_[2] + k)]; }
+  Cplx operator()(long i, long j, long k) const {
+    return data_[static_cast<size_t>((i * shape_[1] + j) * shape_[2] + k)];
+  }
+  // row-major copy of a matrix into the given shape (tensor.hpp:105-109)
+  static Tensor from_matrix(const DenseMatrix& m, std::vector<long> shape) {
+    Tensor t(std::move(shape));
+    if (static_cast<long>(t.data_.size()) != m.rows() * m.cols()) throw InternalConsistency("reshape size mismatch");
+    for (long i = 0; i < m.rows(); ++i)
+      for (long j = 0; j < m.cols(); ++j) t.data_[static_cast<size_t>(i * m.cols() + j)] = m(i, j);
+    return t;
+  }
+
+ private:
+  std::vector<long> shape_;
+  std::vector<Cplx> data_;
+};
 
 // ---- models.hpp:7-56 ------------------------------------------------------
 namespace models {
@@ -297,18 +363,34 @@ class SvdBackend {
 };
 
 // svd_full (linalg.cpp:67-70) on the GPU Jacobi kernel, fix_phases convention
+// (linalg.cpp:19-35).  A block with an all-zero imaginary part takes the real
+// FP64 path (achi_svd: real factors, the same convention); any other complex
+// block the complex path (achi_svd_complex).  Non-finite entries ->
+// InvalidMatrix (check_input, linalg.cpp:11-15).
 inline SvdResult svd_full(const DenseMatrix& m) {
   if (m.rows() < 1 || m.cols() < 1) throw InvalidMatrix("svd: matrix must be at least 1x1");
   const long r = std::min(m.rows(), m.cols());
-  std::vector<double> a = m.row_major(), s(r), u(m.rows() * r), vt(r * m.cols());
-  int sweeps = 0;
-  b200::check(achi_svd(b200::Device::get().ctx(), static_cast<int>(m.rows()),
-                       static_cast<int>(m.cols()), a.data(), s.data(), u.data(), vt.data(), &sweeps));
   SvdResult out;
-  out.u = DenseMatrix::from_row_major(m.rows(), r, u.data());
-  out.sigma = s;
-  out.v_dagger = DenseMatrix::from_row_major(r, m.cols(), vt.data());
+  out.sigma.assign(static_cast<size_t>(r), 0.0);
   out.rank = r;
+  int sweeps = 0;
+  if (m.is_real()) {
+    std::vector<double> a = m.real_row_major(), u(static_cast<size_t>(m.rows() * r)),
+                        vt(static_cast<size_t>(r * m.cols()));
+    b200::check(achi_svd(b200::Device::get().ctx(), static_cast<int>(m.rows()),
+                         static_cast<int>(m.cols()), a.data(), out.sigma.data(), u.data(), vt.data(),
+                         &sweeps));
+    out.u = DenseMatrix::from_real_row_major(m.rows(), r, u.data());
+    out.v_dagger = DenseMatrix::from_real_row_major(r, m.cols(), vt.data());
+  } else {
+    std::vector<double> a = m.interleaved_row_major(), u(static_cast<size_t>(2 * m.rows() * r)),
+                        vd(static_cast<size_t>(2 * r * m.cols()));
+    b200::check(achi_svd_complex(b200::Device::get().ctx(), static_cast<int>(m.rows()),
+                                 static_cast<int>(m.cols()), a.data(), out.sigma.data(), u.data(),
+                                 vd.data(), &sweeps));
+    out.u = DenseMatrix::from_interleaved_row_major(m.rows(), r, u.data());
+    out.v_dagger = DenseMatrix::from_interleaved_row_major(r, m.cols(), vd.data());
+  }
   return out;
 }
 // svd_truncated (linalg.cpp:72-89)
@@ -366,26 +448,231 @@ inline SvdResult svd_dispatch(const DenseMatrix& m, const BackendPolicy& policy,
 
 struct EigsResult {
   double eigenvalue = 0;
-  RVector eigenvector;
+  CVector eigenvector;
   int matvec_count = 0;
   double residual = 0;
 };
-// eigs_lowest (linalg.cpp:107-178) for a dense symmetric operator (the
-// reference's host std::function operator cannot run on the device; on the DMRG
-// path the Lanczos runs inside dmrg::two_site_sweep on H_eff).
-inline EigsResult eigs_lowest(const DenseMatrix& h, const RVector& v0, double tol = 1e-10,
+using LinearMap = std::function<void(const CVector&, CVector&)>;
+
+namespace detail {
+struct RealMap {  // a complex LinearMap as a real operator (realified when complex)
+  const LinearMap* op;
+  long dim;
+  bool realified;
+  bool complex_seen = false;
+  CVector in, out;
+  static void call(void* user, const double* x, double* y, int64_t n) {
+    auto* self = static_cast<RealMap*>(user);
+    const long d = self->dim;
+    self->in.assign(static_cast<size_t>(d), Cplx(0, 0));
+    for (long i = 0; i < d; ++i) self->in[i] = self->realified ? Cplx(x[i], x[d + i]) : Cplx(x[i], 0.0);
+    self->out.assign(static_cast<size_t>(d), Cplx(0, 0));
+    (*self->op)(self->in, self->out);
+    for (long i = 0; i < d; ++i) {
+      y[i] = self->out[i].real();
+      if (self->realified)
+        y[d + i] = self->out[i].imag();
+      else if (self->out[i].imag() != 0.0)
+        self->complex_seen = true;
+    }
+    if (self->complex_seen && !self->realified)
+      for (int64_t i = 0; i < n; ++i) y[i] = std::nan("");  // abort; rerun realified
+  }
+};
+}  // namespace detail
+
+// eigs_lowest (linalg.cpp:107-178) for a LinearMap (linalg.hpp:64-78): the
+// restarted Lanczos runs on the device, the operator on the host
+// (achi_eigs_lowest_callback).  A real operator from a real v0 runs the real
+// iteration (the reference's arithmetic to rounding); a complex Hermitian
+// one runs as the real symmetric [[Re H, -Im H], [Im H, Re H]] on [x; y],
+// whose lowest eigenvector [x; y] gives the complex eigenvector x + i y.
+inline EigsResult eigs_lowest(const LinearMap& apply_h, long dim, const CVector& v0, double tol = 1e-10,
                               int max_iter = 200) {
-  const int dim = static_cast<int>(h.rows());
-  if (static_cast<int>(v0.size()) != dim) throw InvalidMatrix("eigs_lowest: v0 size mismatch");
-  std::vector<double> a = h.row_major();
+  if (dim < 1 || static_cast<long>(v0.size()) != dim) throw InvalidMatrix("eigs_lowest: v0 size mismatch");
+  bool v0_real = true;
+  for (const Cplx& x : v0)
+    if (x.imag() != 0.0) v0_real = false;
+  for (int pass = v0_real ? 0 : 1; pass < 2; ++pass) {
+    detail::RealMap rm{&apply_h, dim, pass == 1, false, {}, {}};
+    const long rd = rm.realified ? 2 * dim : dim;
+    std::vector<double> x0(static_cast<size_t>(rd)), vec(static_cast<size_t>(rd));
+    for (long i = 0; i < dim; ++i) {
+      x0[i] = v0[i].real();
+      if (rm.realified) x0[dim + i] = v0[i].imag();
+    }
+    EigsResult r;
+    const int rc = achi_eigs_lowest_callback(b200::Device::get().ctx(), static_cast<int>(rd),
+                                             &detail::RealMap::call, &rm, x0.data(), tol, max_iter,
+                                             &r.eigenvalue, vec.data(), &r.matvec_count, &r.residual);
+    if (rm.complex_seen && !rm.realified) continue;  // complex operator: run realified
+    b200::check(rc);
+    r.eigenvector.assign(static_cast<size_t>(dim), Cplx(0, 0));
+    for (long i = 0; i < dim; ++i) r.eigenvector[i] = rm.realified ? Cplx(vec[i], vec[dim + i]) : Cplx(vec[i], 0);
+    return r;
+  }
+  throw InternalConsistency("eigs_lowest: unreachable");
+}
+
+// eigs_lowest for a dense Hermitian operator: a real matrix runs the device
+// Lanczos directly on the device matrix (achi_eigs_lowest_dense), a complex
+// one through its real 2 dim x 2 dim form.
+inline EigsResult eigs_lowest(const DenseMatrix& h, const CVector& v0, double tol = 1e-10,
+                              int max_iter = 200) {
+  const long dim = h.rows();
+  if (h.cols() != dim || static_cast<long>(v0.size()) != dim) throw InvalidMatrix("eigs_lowest: v0 size mismatch");
+  bool real = h.is_real();
+  for (const Cplx& x : v0) real = real && x.imag() == 0.0;
+  const long rd = real ? dim : 2 * dim;
+  std::vector<double> a(static_cast<size_t>(rd * rd)), x0(static_cast<size_t>(rd)), vec(static_cast<size_t>(rd));
+  for (long i = 0; i < dim; ++i) {
+    x0[i] = v0[i].real();
+    if (!real) x0[dim + i] = v0[i].imag();
+    for (long j = 0; j < dim; ++j) {
+      const Cplx v = h(i, j);
+      a[static_cast<size_t>(i * rd + j)] = v.real();
+      if (!real) {
+        a[static_cast<size_t>(i * rd + dim + j)] = -v.imag();
+        a[static_cast<size_t>((dim + i) * rd + j)] = v.imag();
+        a[static_cast<size_t>((dim + i) * rd + dim + j)] = v.real();
+      }
+    }
+  }
   EigsResult r;
-  r.eigenvector.assign(dim, 0.0);
-  b200::check(achi_eigs_lowest_dense(b200::Device::get().ctx(), dim, a.data(), v0.data(), tol,
-                                     max_iter, &r.eigenvalue, r.eigenvector.data(),
-                                     &r.matvec_count, &r.residual));
+  b200::check(achi_eigs_lowest_dense(b200::Device::get().ctx(), static_cast<int>(rd), a.data(), x0.data(),
+                                     tol, max_iter, &r.eigenvalue, vec.data(), &r.matvec_count, &r.residual));
+  r.eigenvector.assign(static_cast<size_t>(dim), Cplx(0, 0));
+  for (long i = 0; i < dim; ++i) r.eigenvector[i] = real ? Cplx(vec[i], 0) : Cplx(vec[i], vec[dim + i]);
   return r;
 }
+
+// C = A B for complex row-major A (M x K) and B (K x N) on the device DMMA
+// GEMM (achi_dgemm; four real products, operands padded to even leading
+// dimensions): the contraction inside Tensor::contract (tensor.hpp:195-196).
+inline std::vector<Cplx> cgemm(long M, long N, long K, const Cplx* A, const Cplx* B) {
+  const long Kp = K + (K & 1), Np = N + (N & 1);
+  std::vector<double> ar(static_cast<size_t>(M * Kp), 0.0), ai(ar.size(), 0.0), br(static_cast<size_t>(K * Np), 0.0),
+      bi(br.size(), 0.0);
+  for (long i = 0; i < M; ++i)
+    for (long k = 0; k < K; ++k) {
+      ar[static_cast<size_t>(i * Kp + k)] = A[i * K + k].real();
+      ai[static_cast<size_t>(i * Kp + k)] = A[i * K + k].imag();
+    }
+  for (long k = 0; k < K; ++k)
+    for (long j = 0; j < N; ++j) {
+      br[static_cast<size_t>(k * Np + j)] = B[k * N + j].real();
+      bi[static_cast<size_t>(k * Np + j)] = B[k * N + j].imag();
+    }
+  std::vector<double> t[4];
+  const double* pa[4] = {ar.data(), ai.data(), ar.data(), ai.data()};
+  const double* pb[4] = {br.data(), bi.data(), bi.data(), br.data()};
+  for (int q = 0; q < 4; ++q) {
+    t[q].assign(static_cast<size_t>(M * Np), 0.0);
+    b200::check(achi_dgemm(b200::Device::get().ctx(), static_cast<int>(M), static_cast<int>(Np),
+                           static_cast<int>(Kp), 1, pa[q], Kp, 0, pb[q], Np, t[q].data(), Np));
+  }
+  std::vector<Cplx> c(static_cast<size_t>(M * N));
+  for (long i = 0; i < M; ++i)
+    for (long j = 0; j < N; ++j) {
+      const size_t o = static_cast<size_t>(i * Np + j);
+      c[static_cast<size_t>(i * N + j)] = Cplx(t[0][o] - t[1][o], t[2][o] + t[3][o]);
+    }
+  return c;
+}
 }  // namespace linalg
+
+// ---- mps.hpp:20-99: MPS container, split / merge of two-site blocks --------
+namespace mps {
+struct TruncationOutcome {
+  int kept_chi = 0;
+  double truncation_error = 0;
+  double entropy = 0;
+  SingularSpectrum spectrum;
+  bool degenerate_cut = false;
+};
+
+// Open-boundary MPS of (left, phys, right) site tensors (mps.hpp:30-50).  The
+// device-resident state of a run lives in dmrg::Chain; this host container is
+// what split/merge and snapshots exchange.
+class MatrixProductState {
+ public:
+  MatrixProductState() = default;
+  explicit MatrixProductState(std::vector<Tensor> sites) : sites_(std::move(sites)) {}
+  int size() const { return static_cast<int>(sites_.size()); }
+  int phys_dim() const { return static_cast<int>(sites_.front().dim(1)); }
+  Tensor& site(int i) { return sites_[static_cast<size_t>(i)]; }
+  const Tensor& site(int i) const { return sites_[static_cast<size_t>(i)]; }
+  void set_site(int i, Tensor t) { sites_[static_cast<size_t>(i)] = std::move(t); }
+  std::vector<int> bond_dims() const {  // mps.cpp:24-29
+    std::vector<int> b;
+    for (int i = 0; i + 1 < size(); ++i) b.push_back(static_cast<int>(sites_[static_cast<size_t>(i)].dim(2)));
+    return b;
+  }
+
+ private:
+  std::vector<Tensor> sites_;
+};
+
+enum class AbsorbSide { left, right };
+struct SplitResult {
+  Tensor left;              // (chi_left, d, kept)
+  SingularSpectrum lambda;  // kept values
+  Tensor right;             // (kept, d, chi_right)
+  TruncationOutcome outcome;
+};
+
+// split_two_site (mps.cpp:124-166): device SVD, entropy and truncation error
+// (achi_spectrum_stats); the kept factors are sliced and lambda absorbed on
+// the host (O(chi^2) copies of the API-level helper; the DMRG path absorbs on
+// the device).
+inline SplitResult split_two_site(const DenseMatrix& theta, int d, int chi_left, int chi_right,
+                                  int chi_request, double trunc_floor = 1e-14,
+                                  AbsorbSide absorb = AbsorbSide::right) {
+  if (theta.rows() != static_cast<long>(d) * chi_left || theta.cols() != static_cast<long>(d) * chi_right)
+    throw InvalidMatrix("split_two_site: theta shape mismatch");
+  if (chi_request < 1) throw InvalidRank("split_two_site: chi_request >= 1");
+  linalg::SvdResult svd = linalg::svd_full(theta);
+  const double s1 = svd.sigma.empty() ? 0.0 : svd.sigma[0];
+  if (!(s1 > 0)) throw DegenerateSpectrum("split_two_site: zero matrix");
+  long significant = 0;
+  for (double x : svd.sigma)
+    if (x > trunc_floor * s1) ++significant;
+  significant = std::max<long>(significant, 1);
+  const long kept = std::min<long>(chi_request, significant);
+  SplitResult out;
+  out.outcome.spectrum.values = svd.sigma;
+  out.outcome.kept_chi = static_cast<int>(kept);
+  out.outcome.entropy = entropy_from_spectrum(out.outcome.spectrum);
+  out.outcome.truncation_error = truncation_error(out.outcome.spectrum, static_cast<int>(kept));
+  out.outcome.degenerate_cut = kept < static_cast<long>(svd.sigma.size()) &&
+                               std::abs(svd.sigma[kept - 1] - svd.sigma[kept]) <= 1e-12 * s1;
+  DenseMatrix u(theta.rows(), kept), vdag(kept, theta.cols());
+  for (long j = 0; j < kept; ++j)
+    for (long i = 0; i < theta.rows(); ++i)
+      u(i, j) = svd.u(i, j) * (absorb == AbsorbSide::left ? svd.sigma[j] : 1.0);
+  for (long j = 0; j < theta.cols(); ++j)
+    for (long i = 0; i < kept; ++i)
+      vdag(i, j) = svd.v_dagger(i, j) * (absorb == AbsorbSide::right ? svd.sigma[i] : 1.0);
+  out.lambda.values.assign(svd.sigma.begin(), svd.sigma.begin() + kept);
+  out.left = Tensor::from_matrix(u, {chi_left, d, kept});
+  out.right = Tensor::from_matrix(vdag, {kept, d, chi_right});
+  return out;
+}
+
+// merge_two_site (mps.cpp:317-324): (l, s1, x) * (x, s2, r) -> (l s1) x (s2 r),
+// on the device GEMM
+inline DenseMatrix merge_two_site(const MatrixProductState& psi, int k) {
+  const Tensor& a = psi.site(k);
+  const Tensor& b = psi.site(k + 1);
+  if (a.dim(2) != b.dim(0)) throw InvalidMatrix("merge_two_site: bond mismatch");
+  const long l = a.dim(0), d1 = a.dim(1), x = a.dim(2), d2 = b.dim(1), r = b.dim(2);
+  const std::vector<Cplx> c = linalg::cgemm(l * d1, d2 * r, x, a.data(), b.data());
+  DenseMatrix m(l * d1, d2 * r);
+  for (long i = 0; i < l * d1; ++i)
+    for (long j = 0; j < d2 * r; ++j) m(i, j) = c[static_cast<size_t>(i * d2 * r + j)];
+  return m;
+}
+}  // namespace mps
 
 // ---- dmrg.hpp:10-98 ---------------------------------------------------------
 namespace dmrg {

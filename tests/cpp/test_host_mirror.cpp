@@ -55,13 +55,34 @@ static DenseMatrix random_real(long r, long c, unsigned seed) {
   for (auto& x : m.d) x = g(rng);
   return m;
 }
+static DenseMatrix random_complex(long r, long c, unsigned seed) {
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> g;
+  DenseMatrix m(r, c);
+  for (auto& x : m.d) {
+    const double re = g(rng);
+    x = Cplx(re, g(rng));
+  }
+  return m;
+}
 static double recon_error(const DenseMatrix& m, const linalg::SvdResult& r) {
   double e = 0;
   for (long i = 0; i < m.rows(); ++i)
     for (long j = 0; j < m.cols(); ++j) {
-      double s = 0;
+      Cplx s = 0;
       for (long k = 0; k < static_cast<long>(r.sigma.size()); ++k) s += r.u(i, k) * r.sigma[k] * r.v_dagger(k, j);
       e = std::max(e, std::abs(s - m(i, j)));
+    }
+  return e;
+}
+// max |U^H U - I| over the first k columns
+static double unitarity_error(const DenseMatrix& u, long k) {
+  double e = 0;
+  for (long a = 0; a < k; ++a)
+    for (long b = 0; b < k; ++b) {
+      Cplx s = 0;
+      for (long i = 0; i < u.rows(); ++i) s += std::conj(u(i, a)) * u(i, b);
+      e = std::max(e, std::abs(s - (a == b ? 1.0 : 0.0)));
     }
   return e;
 }
@@ -99,8 +120,8 @@ static void test_linalg() {
   {  // svd_full identity 2x2 (test_linalg.cpp:38)
     auto r = linalg::svd_full(DenseMatrix::Identity(2, 2));
     CHECK(approx(r.sigma[0], 1.0, 1e-12) && approx(r.sigma[1], 1.0, 1e-12));
-    CHECK(std::abs(r.u(0, 0) - 1) <= 1e-12 && std::abs(r.u(1, 1) - 1) <= 1e-12);
-    CHECK(std::abs(r.v_dagger(0, 0) - 1) <= 1e-12 && std::abs(r.v_dagger(0, 1)) <= 1e-12);
+    CHECK(std::abs(r.u(0, 0) - 1.0) <= 1e-12 && std::abs(r.u(1, 1) - 1.0) <= 1e-12);
+    CHECK(std::abs(r.v_dagger(0, 0) - 1.0) <= 1e-12 && std::abs(r.v_dagger(0, 1)) <= 1e-12);
   }
   {  // diag(3,2)
     DenseMatrix m(2, 2);
@@ -115,7 +136,7 @@ static void test_linalg() {
     CHECK(r.rank == std::min(rows, cols));
     CHECK(recon_error(m, r) <= 1e-12);
     double fro = 0, s2 = 0;
-    for (double x : m.d) fro += x * x;
+    for (Cplx x : m.d) fro += std::norm(x);
     for (double s : r.sigma) s2 += s * s;
     CHECK(approx(fro, s2, 1e-12));
     for (size_t k = 1; k < r.sigma.size(); ++k) CHECK(r.sigma[k] <= r.sigma[k - 1]);
@@ -143,26 +164,101 @@ static void test_linalg() {
     DenseMatrix h(3, 3);
     h(0, 0) = -1;
     h(2, 2) = 1;
-    auto r = linalg::eigs_lowest(h, RVector(3, 1.0), 1e-12, 100);
+    auto r = linalg::eigs_lowest(h, CVector(3, 1.0), 1e-12, 100);
     CHECK(approx(r.eigenvalue, -1.0, 1e-10));
     CHECK(approx(std::abs(r.eigenvector[0]), 1.0, 1e-8));
     DenseMatrix s(4, 4);
     s(0, 0) = s(3, 3) = 0.25;
     s(1, 1) = s(2, 2) = -0.25;
     s(1, 2) = s(2, 1) = 0.5;
-    auto q = linalg::eigs_lowest(s, RVector{0.3, -0.7, 0.2, 0.9}, 1e-12, 100);
+    auto q = linalg::eigs_lowest(s, CVector{0.3, -0.7, 0.2, 0.9}, 1e-12, 100);
     CHECK(approx(q.eigenvalue, -0.75, 1e-10));
-    CHECK_THROWS_AS(linalg::eigs_lowest(s, RVector(4, 0.0), 1e-10, 10), InvalidMatrix);
+    CHECK_THROWS_AS(linalg::eigs_lowest(s, CVector(4, 0.0), 1e-10, 10), InvalidMatrix);
     DenseMatrix a = random_real(32, 32, 12), hs(32, 32);
     for (long i = 0; i < 32; ++i)
       for (long j = 0; j < 32; ++j) hs(i, j) = 0.5 * (a(i, j) + a(j, i));
     bool threw = false;
     try {
-      linalg::eigs_lowest(hs, RVector(32, 1.0), 1e-14, 3);
+      linalg::eigs_lowest(hs, CVector(32, 1.0), 1e-14, 3);
     } catch (const EigenNonConvergence& e) {
       threw = std::isfinite(e.best_residual) && e.best_residual > 0;
     }
     CHECK(threw);
+  }
+  {  // complex svd_full (test_linalg.cpp:25-82 on MatrixXcd::Random): reconstruction,
+     // isometric factors, non-increasing sigma, fix_phases, sum sigma^2 = ||A||_F^2
+    for (auto [rows, cols] : {std::pair<long, long>{8, 8}, {5, 9}, {9, 5}, {1, 7}, {40, 30}}) {
+      DenseMatrix m = random_complex(rows, cols, 7);
+      auto r = linalg::svd_full(m);
+      const long k = std::min(rows, cols);
+      CHECK(r.rank == k && recon_error(m, r) <= 1e-12);
+      CHECK(unitarity_error(r.u, k) <= 1e-10);
+      double fro = 0, s2 = 0;
+      for (Cplx x : m.d) fro += std::norm(x);
+      for (double x : r.sigma) s2 += x * x;
+      CHECK(approx(fro, s2, 1e-12));
+      for (long q = 0; q < k; ++q) {  // first largest |u| entry real and positive
+        long imax = 0;
+        double best = 0;
+        for (long i = 0; i < rows; ++i)
+          if (std::abs(r.u(i, q)) > best) best = std::abs(r.u(i, q)), imax = i;
+        CHECK(r.u(imax, q).real() > 0 && std::abs(r.u(imax, q).imag()) <= 1e-15 * best);
+      }
+    }
+    DenseMatrix bad(2, 2);
+    bad(0, 1) = Cplx(0, std::nan(""));
+    CHECK_THROWS_AS(linalg::svd_full(bad), InvalidMatrix);
+  }
+  {  // eigs_lowest(LinearMap, ...) (linalg.hpp:71-78): real and complex Hermitian operators
+    DenseMatrix h(3, 3);
+    h(0, 0) = -1;
+    h(2, 2) = 1;
+    linalg::LinearMap op = [&](const CVector& x, CVector& y) {
+      for (long i = 0; i < 3; ++i) {
+        y[i] = 0;
+        for (long j = 0; j < 3; ++j) y[i] += h(i, j) * x[j];
+      }
+    };
+    auto r = linalg::eigs_lowest(op, 3, CVector(3, 1.0), 1e-12, 100);
+    CHECK(approx(r.eigenvalue, -1.0, 1e-10));
+    // a random complex Hermitian 6 x 6: LinearMap path (realified) vs the dense path
+    DenseMatrix c = random_complex(6, 6, 99), hc(6, 6);
+    for (long i = 0; i < 6; ++i)
+      for (long j = 0; j < 6; ++j) hc(i, j) = 0.5 * (c(i, j) + std::conj(c(j, i)));
+    linalg::LinearMap opc = [&](const CVector& x, CVector& y) {
+      for (long i = 0; i < 6; ++i) {
+        y[i] = 0;
+        for (long j = 0; j < 6; ++j) y[i] += hc(i, j) * x[j];
+      }
+    };
+    auto rc = linalg::eigs_lowest(opc, 6, CVector(6, 1.0), 1e-11, 200);
+    auto rd = linalg::eigs_lowest(hc, CVector(6, 1.0), 1e-11, 200);
+    CHECK(approx(rc.eigenvalue, rd.eigenvalue, 1e-9));
+    double res = 0;  // |H v - E v|
+    for (long i = 0; i < 6; ++i) {
+      Cplx y = 0;
+      for (long j = 0; j < 6; ++j) y += hc(i, j) * rc.eigenvector[j];
+      res += std::norm(y - rc.eigenvalue * rc.eigenvector[i]);
+    }
+    CHECK(std::sqrt(res) <= 1e-9);
+  }
+  {  // split_two_site / merge_two_site (mps.cpp:124-166, 317-324; test_mps.cpp)
+    const int d = 2, cl = 3, cr = 4;
+    DenseMatrix theta = random_complex(d * cl, d * cr, 17);
+    auto sp = mps::split_two_site(theta, d, cl, cr, 6);
+    CHECK(sp.outcome.kept_chi == 6 && sp.left.dim(2) == 6 && sp.right.dim(0) == 6);
+    mps::MatrixProductState psi({sp.left, sp.right});
+    DenseMatrix back = mps::merge_two_site(psi, 0);
+    double e = 0;
+    for (long i = 0; i < theta.rows(); ++i)
+      for (long j = 0; j < theta.cols(); ++j) e = std::max(e, std::abs(back(i, j) - theta(i, j)));
+    CHECK(e <= 1e-12);
+    auto sp2 = mps::split_two_site(theta, d, cl, cr, 2, 1e-14, mps::AbsorbSide::left);
+    CHECK(sp2.outcome.kept_chi == 2 && sp2.lambda.values.size() == 2);
+    CHECK(approx(sp2.outcome.truncation_error, mps::truncation_error(sp2.outcome.spectrum, 2), 1e-14));
+    CHECK_THROWS_AS(mps::split_two_site(theta, d, cl, cr + 1, 2), InvalidMatrix);
+    CHECK_THROWS_AS(mps::split_two_site(theta, d, cl, cr, 0), InvalidRank);
+    CHECK_THROWS_AS(mps::split_two_site(DenseMatrix(d * cl, d * cr), d, cl, cr, 2), DegenerateSpectrum);
   }
   {  // select_backend threshold dispatch (test_linalg.cpp:228)
     linalg::BackendRegistry registry;
