@@ -353,11 +353,15 @@ int achi_chain_load_mps(achi_chain* chain, const int32_t* bond_dims, const doubl
       for (double x : hs[k])
         if (!std::isfinite(x)) fail(ACHI_E_INVALID_MATRIX, "load_mps: non-finite site entry");
     }
-    if (canonicalize) canonicalize_left(hs, dims, ch.d);  // canonicalize(psi, 0), mps.cpp:204-210
+    std::vector<DevBuf> ds;
+    if (canonicalize) ds = canonical_on_device(*ch.ctx, hs, dims, ch.d);  // canonicalize(psi, 0), mps.cpp:204-210
     for (int k = 1; k < ch.n; ++k)
       if (dims[k] > ch.cap[k]) fail(ACHI_E_INVALID_RANK, "load_mps: bond dimension exceeds capacity");
     for (int k = 1; k < ch.n; ++k) ch.chi[k] = dims[k];
-    ch.upload_sites(hs);
+    if (canonicalize)
+      ch.copy_sites_device(ds);
+    else
+      ch.upload_sites(hs);
     ch.rebuild_envs();
     ch.ctx->sync();
   });

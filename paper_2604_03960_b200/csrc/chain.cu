@@ -126,91 +126,121 @@ std::vector<int> capped_bond_dims(int n, int d, int chi) {
   return dims;
 }
 
-// Thin Householder QR of a column-major m x ncol matrix, k = min(m, ncol)
-// reflectors with LAPACK dlarfg signs (beta = -sign(alpha) * ||x||):
-// a -> Q (m x k, column-major), r -> R (k x ncol, column-major, upper
-// trapezoidal).  Setup-sized (host side).
-int householder_qr(std::vector<double>& a, int m, int ncol, std::vector<double>& r) {
-  const int k = std::min(m, ncol);
-  std::vector<double> v(static_cast<size_t>(m) * k, 0.0), tau(k, 0.0);
-  auto A = [&](int i, int j) -> double& { return a[static_cast<size_t>(j) * m + i]; };
-  for (int j = 0; j < k; ++j) {
-    double xn = 0;
-    for (int i = j + 1; i < m; ++i) xn += A(i, j) * A(i, j);
-    xn = std::sqrt(xn);
-    const double alpha = A(j, j);
-    double* vj = &v[static_cast<size_t>(j) * m];
-    vj[j] = 1.0;
-    if (xn == 0.0) {
-      tau[j] = 0.0;
-    } else {
-      const double beta = alpha >= 0 ? -std::hypot(alpha, xn) : std::hypot(alpha, xn);
-      tau[j] = (beta - alpha) / beta;
-      for (int i = j + 1; i < m; ++i) vj[i] = A(i, j) / (alpha - beta);
-      A(j, j) = beta;
-      for (int i = j + 1; i < m; ++i) A(i, j) = 0.0;
-      for (int c = j + 1; c < ncol; ++c) {  // apply H_j to the trailing columns
-        double s = 0;
-        for (int i = j; i < m; ++i) s += vj[i] * A(i, c);
-        s *= tau[j];
-        for (int i = j; i < m; ++i) A(i, c) -= s * vj[i];
-      }
-    }
+// C (M x N) = A (M x K) * B (K x N), row-major, any shapes (setup-sized
+// products of canonicalisation; 16 x 16 shared-memory tiles, FP64 FMA)
+__global__ void matmul_kernel(const double* __restrict__ A, const double* __restrict__ B,
+                              double* __restrict__ C, int M, int N, int K) {
+  __shared__ double As[16][17], Bs[16][17];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int row = blockIdx.y * 16 + ty, col = blockIdx.x * 16 + tx;
+  double acc = 0.0;
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    As[ty][tx] = (row < M && k0 + tx < K) ? A[static_cast<long>(row) * K + k0 + tx] : 0.0;
+    Bs[ty][tx] = (k0 + ty < K && col < N) ? B[static_cast<long>(k0 + ty) * N + col] : 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc = fma(As[ty][k], Bs[k][tx], acc);
+    __syncthreads();
   }
-  r.assign(static_cast<size_t>(k) * ncol, 0.0);
-  for (int j = 0; j < ncol; ++j)
-    for (int i = 0; i <= std::min(j, k - 1); ++i) r[static_cast<size_t>(j) * k + i] = A(i, j);
-  // Q = H_0 ... H_{k-1} [I_k; 0]
-  std::vector<double> q(static_cast<size_t>(m) * k, 0.0);
-  auto Q = [&](int i, int j) -> double& { return q[static_cast<size_t>(j) * m + i]; };
-  for (int j = 0; j < k; ++j) Q(j, j) = 1.0;
-  for (int j = k - 1; j >= 0; --j) {
-    const double* vj = &v[static_cast<size_t>(j) * m];
-    for (int c = 0; c < k; ++c) {
-      double s = 0;
-      for (int i = j; i < m; ++i) s += vj[i] * Q(i, c);
-      s *= tau[j];
-      for (int i = j; i < m; ++i) Q(i, c) -= s * vj[i];
-    }
+  if (row < M && col < N) C[static_cast<long>(row) * N + col] = acc;
+}
+
+// U (m x k row-major) <- U * diag(sigma)
+__global__ void scale_cols_kernel(double* __restrict__ U, int m, int k, const double* __restrict__ sigma) {
+  const long tot = static_cast<long>(m) * k;
+  for (long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; t < tot;
+       t += static_cast<long>(gridDim.x) * blockDim.x)
+    U[t] *= sigma[t % k];
+}
+
+__global__ void scale_all_kernel(double* __restrict__ x, long n, const double* __restrict__ nrm2,
+                                 int* __restrict__ bad) {
+  const double n2 = *nrm2;
+  if (!(n2 > 0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *bad = 1;
+    return;
   }
-  a.swap(q);
-  return k;
+  const double inv = 1.0 / sqrt(n2);
+  for (long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<long>(gridDim.x) * blockDim.x)
+    x[t] *= inv;
 }
 
 }  // namespace
 
-// canonicalize(psi, 0) (mps.cpp:172-210): push_left on sites n-1..1 (right
-// moves only).  Site k is (dims[k], d, dims[k+1]) row-major; push_left may
-// shrink dims[k] to min(d * dims[k+1], dims[k]).
-void canonicalize_left(std::vector<std::vector<double>>& s, std::vector<int>& dims, int d) {
+// canonicalize(psi, 0) (mps.cpp:172-210: push_left on sites n-1..1) on the
+// device.  Site i as M (l x d r, row-major) is factored M = (U S) V^T by the
+// Jacobi SVD with V accumulated (orthonormal also across zero and noise-level
+// values); site i <- V^T (k x d r, rows orthonormal), site i-1 <- site i-1 *
+// (U S).  This is push_left with an SVD instead of Householder QR: the same
+// bond dimensions k = min(l, d r) and the same state, in another gauge of
+// bond i (a k x k rotation), which every later step is covariant under
+// (energies and kept ranks agree with the QR gauge to rounding).
+void device_canonicalize_left(Ctx& c, std::vector<DevBuf>& s, std::vector<int>& dims, int d) {
   const int n = static_cast<int>(s.size());
+  SvdWs ws;
   for (int i = n - 1; i >= 1; --i) {
-    const int l = dims[i], r = dims[i + 1], m = d * r;
-    // M^T with M = site as l x (d r): column-major (m x l) buffer == site row-major
-    std::vector<double> a(s[i].begin(), s[i].end()), rr;
-    const int k = householder_qr(a, m, l, rr);  // a: Q (m x k), rr: R (k x l)
-    s[i] = a;  // site i <- Q^T (k x m) row-major == Q column-major
-    // site i-1 (ll*d x l) <- site i-1 * R^T (l x k)
-    const int ll = dims[i - 1];
-    std::vector<double> nb(static_cast<size_t>(ll) * d * k, 0.0);
-    for (int row = 0; row < ll * d; ++row)
-      for (int c = 0; c < k; ++c) {
-        double acc = 0;  // (R^T)(t, c) = R(c, t), nonzero for t >= c
-        for (int t = c; t < l; ++t)
-          acc += s[i - 1][static_cast<size_t>(row) * l + t] * rr[static_cast<size_t>(t) * k + c];
-        nb[static_cast<size_t>(row) * k + c] = acc;
-      }
-    s[i - 1] = nb;
+    const int l = dims[i], r = dims[i + 1], cols = d * r, k = std::min(l, cols), ll = dims[i - 1];
+    SvdResultDev res = svd_device(c, ws, s[i].p, l, cols, l, cols, SvdSide::kCols);
+    svd_phase_signs(c, ws, res, k);
+    DevBuf U, VT, nb;
+    U.reserve(static_cast<size_t>(l) * k);
+    VT.reserve(static_cast<size_t>(k) * cols);
+    svd_gather(c, ws, res, k, U.p, VT.p);
+    scale_cols_kernel<<<std::max(1, std::min(cdiv(static_cast<long>(l) * k, 256), 4 * c.num_sms)), 256, 0,
+                        c.stream>>>(U.p, l, k, res.sigma);
+    ACHI_LAUNCHED(c);
+    nb.reserve(static_cast<size_t>(ll) * d * k);
+    matmul_kernel<<<dim3(cdiv(k, 16), cdiv(static_cast<long>(ll) * d, 16)), dim3(16, 16), 0, c.stream>>>(
+        s[i - 1].p, U.p, nb.p, ll * d, k, l);
+    ACHI_LAUNCHED(c);
+    c.sync();
+    res.sweeps();  // NumericalFailure if the Jacobi iteration hit its cap
+    s[i] = std::move(VT);
+    s[i - 1] = std::move(nb);
     dims[i] = k;
   }
 }
 
+// host sites -> device (unpadded), canonicalize(psi, 0) on the device
+std::vector<DevBuf> canonical_on_device(Ctx& c, const std::vector<std::vector<double>>& hs,
+                                        std::vector<int>& dims, int d, int times) {
+  std::vector<DevBuf> ds(hs.size());
+  for (size_t k = 0; k < hs.size(); ++k) {
+    ds[k].reserve(hs[k].size());
+    ACHI_CUDA(cudaMemcpyAsync(ds[k].p, hs[k].data(), sizeof(double) * hs[k].size(),
+                              cudaMemcpyHostToDevice, c.stream));
+  }
+  for (int t = 0; t < times; ++t) {
+    device_canonicalize_left(c, ds, dims, d);
+    if (t + 1 < times) {
+      // normalise the centre site between the two canonicalisations (random_mps, mps.cpp:93-95)
+      const long n0 = static_cast<long>(dims[0]) * d * dims[1];
+      DevBuf nrm;
+      DevArr<int> bad;
+      nrm.reserve(1);
+      int* pb = bad.reserve(1);
+      ACHI_CUDA(cudaMemsetAsync(pb, 0, sizeof(int), c.stream));
+      device_norm2(c, ds[0].p, n0, nrm.p);
+      scale_all_kernel<<<std::max(1, std::min(cdiv(n0, 256), 4 * c.num_sms)), 256, 0, c.stream>>>(
+          ds[0].p, n0, nrm.p, pb);
+      ACHI_LAUNCHED(c);
+      int hb = 0;
+      ACHI_CUDA(cudaMemcpyAsync(&hb, pb, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      if (hb) fail(ACHI_E_NUMERICAL_FAILURE, "random_mps: zero-norm state");
+    }
+  }
+  return ds;
+}
+
 namespace {
 
-// random_mps (mps.cpp:75-95) with one real normal draw per entry, then the
-// second canonicalize of run_dmrg (dmrg.cpp:236).
-std::vector<std::vector<double>> random_real_canonical(int n, int d, int chi, uint64_t seed,
-                                                       std::vector<int>& dims_out) {
+// random_mps (mps.cpp:75-95) with one real normal draw per entry (host
+// generator: the reference's mt19937_64 sequence), canonicalize + normalise,
+// then the second canonicalize of run_dmrg (dmrg.cpp:236) -- on the device.
+std::vector<std::vector<double>> random_real_sites(int n, int d, int chi, uint64_t seed,
+                                                   std::vector<int>& dims_out) {
   if (chi < 1) fail(ACHI_E_INVALID_RANK, "random_mps: chi must be >= 1");
   std::mt19937_64 rng(seed);
   std::normal_distribution<double> gauss(0.0, 1.0);
@@ -222,13 +252,6 @@ std::vector<std::vector<double>> random_real_canonical(int n, int d, int chi, ui
     s[i].resize(static_cast<size_t>(dims[i]) * d * dims[i + 1]);
     for (double& x : s[i]) x = gauss(rng);
   }
-  canonicalize_left(s, dims, d);
-  double nrm = 0;
-  for (double x : s[0]) nrm += x * x;
-  nrm = std::sqrt(nrm);
-  if (!(nrm > 0)) fail(ACHI_E_NUMERICAL_FAILURE, "random_mps: zero-norm state");
-  for (double& x : s[0]) x /= nrm;
-  canonicalize_left(s, dims, d);
   dims_out = dims;
   return s;
 }
@@ -314,9 +337,10 @@ void Chain::create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g) 
     upload_sites(neel_canonical(n, d));
   } else {
     std::vector<int> dims;
-    auto hs = random_real_canonical(n, d, g.controller.chi_min, g.seed, dims);
+    auto hs = random_real_sites(n, d, g.controller.chi_min, g.seed, dims);
+    auto ds = canonical_on_device(c, hs, dims, d, 2);
     for (int k = 1; k < n; ++k) chi[k] = dims[k];
-    upload_sites(hs);
+    copy_sites_device(ds);
   }
   std::vector<achi_bond_state> st(n - 1);
   for (auto& b : st) {
@@ -339,6 +363,18 @@ void Chain::upload_sites(const std::vector<std::vector<double>>& hs) {
     if (static_cast<long>(hs[k].size()) != static_cast<long>(l) * d * r)
       fail(ACHI_E_INTERNAL, "upload_sites: size mismatch");
     upload_padded3(*ctx, hs[k].data(), l, d, r, site[k].p);
+  }
+  ctx->sync();
+}
+
+// unpadded device sites (l, d, r) -> the chain's padded storage
+void Chain::copy_sites_device(const std::vector<DevBuf>& ds) {
+  for (int k = 0; k < n; ++k) {
+    const int l = chi[k], r = chi[k + 1], lp = pad2i(l), rp = pad2i(r);
+    ACHI_CUDA(cudaMemsetAsync(site[k].p, 0, sizeof(double) * lp * d * rp, ctx->stream));
+    ACHI_CUDA(cudaMemcpy2DAsync(site[k].p, sizeof(double) * rp, ds[k].p, sizeof(double) * r,
+                                sizeof(double) * r, static_cast<size_t>(l) * d, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
   }
   ctx->sync();
 }

@@ -27,8 +27,11 @@ struct VisitHost {
   int matvecs;
 };
 
-// canonicalize(psi, 0) on host site tensors (setup sized; mps.cpp:172-210)
-void canonicalize_left(std::vector<std::vector<double>>& sites, std::vector<int>& dims, int d);
+// canonicalize(psi, 0) (mps.cpp:172-210) on the device: host site tensors
+// (l, d, r row-major) in, unpadded device site tensors out (`times` passes,
+// the centre site normalised between passes as random_mps does).
+std::vector<DevBuf> canonical_on_device(Ctx& c, const std::vector<std::vector<double>>& sites,
+                                        std::vector<int>& dims, int d, int times = 1);
 
 struct Chain {
   Ctx* ctx = nullptr;
@@ -75,6 +78,7 @@ struct Chain {
   void rebuild_envs();
   double expectation_energy();
   void upload_sites(const std::vector<std::vector<double>>& host_sites);
+  void copy_sites_device(const std::vector<DevBuf>& device_sites);
   void visit(int bond, bool moving_right, int sweep, int slot);
   void sweep(int sweep_index, achi_sweep_record* rec, int32_t* chi_profile, double* entropy,
              achi_trace_row* trace_out, achi_visit_record* visits_out);
