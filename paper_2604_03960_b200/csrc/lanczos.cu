@@ -807,6 +807,474 @@ __global__ void __launch_bounds__(ORTH_THREADS) lanczos_step_small_kernel(FusedS
   hs::phase_c(f.h, f.h.out, blk, nblk);
 }
 
+// ---- persistent eigensolve for small blocks (chi <= 128) -----------------
+// The whole restarted Lanczos of one eigs_lowest call as ONE cooperative
+// launch: W worker CTAs run every phase of every step -- the fused H_eff
+// matvec (heff_phases.cuh phases A and B; phase C is folded into the first
+// orthogonalisation pass), the CGS2 orthogonalisation, the Ritz vector, the
+// explicit residual check and the restart -- separated by a barrier among the
+// workers; one more CTA (the "tridiagonal CTA") solves the tridiagonal
+// eigenproblem of each step concurrently and posts the reference's step
+// decision (linalg.cpp:141-148).  The workers run the next step
+// speculatively and read the decision of step j at the end of step j+1 (a
+// step later), so the tridiagonal solve is off their critical path; a step
+// computed after the loop should have stopped is discarded (its matvec is not
+// counted).  Deterministic stops (end of block, max_iter) are known without
+// the decision.  This replaces per-step kernel launches, the graph's
+// conditional loop and the fork/join to the tridiagonal stream with barriers.
+constexpr int PZ_THREADS = hs::HS_THREADS;  // 256, = ORTH_THREADS
+
+struct PzArgs {
+  hs::HsArgs h;          // L, R, mix, dims; theta/out unused (set per matvec)
+  double* Q;             // basis, LANCZOS_BLOCK + 1 vectors at stride
+  long stride;
+  double* w;             // matvec output / orthogonalised vector
+  double* ritz;
+  double* tmp;
+  const double* v0;
+  double* out;
+  long n;                // padded two-site length
+  double* pa;            // [64][W] partials
+  double* pb;            // [65][W]
+  double* pc;            // [W]
+  double* alpha;         // [64]
+  double* beta;          // [64]
+  double* sbuf;          // [2][64] tridiagonal eigenvectors by job parity
+  double* tres;          // [2][4] theta, res_bound, bnorm, alpha by job parity
+  int* dec;              // [2] stop decision by job parity
+  int* job;              // [2][2] (j, matvecs before the cycle) by job parity
+  unsigned* posted;      // jobs posted (seq)
+  unsigned* done;        // jobs finished by the tridiagonal CTA
+  unsigned* bar;         // [2] worker barrier: arrivals, generation
+  LanczosCtl* ctl;
+  LanczosStatus* st;
+  double tol;
+  int block, max_iter;
+  int W;                 // worker CTAs; CTA W is the tridiagonal CTA
+  unsigned long long* prof;  // optional clock64 phase totals of worker 0 (ACHI_LANCZOS_PROF)
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// barrier among the W worker CTAs: one monotonic arrival counter (zeroed per
+// launch); arrival is a release reduction, the wait an acquire poll for
+// W * (barriers passed so far)
+__device__ __forceinline__ void pz_sync(const PzArgs& a, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned target = (gen + 1u) * static_cast<unsigned>(a.W);
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.bar), "r"(1u) : "memory");
+    while (ld_acquire(a.bar) < target) {
+    }
+  }
+  ++gen;
+  __syncthreads();
+}
+
+// every worker: sum over workers of part[v][0..W) for v < nv (fixed order)
+__device__ void pz_reduce(const double* part, int nv, int W, double* coef) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int v = warp; v < nv; v += PZ_THREADS / 32) {
+    double t = 0.0;
+    for (int b = lane; b < W; b += 32) t += __ldcg(part + static_cast<long>(v) * W + b);
+    t = warp_sum(t);
+    if (lane == 0) coef[v] = t;
+  }
+  __syncthreads();
+}
+
+// block partial of sum_x f(x) over [b0, b1) -> part[rank] (thread 0 writes)
+__device__ __forceinline__ void pz_put(double v, double* part, int rank, double* red) {
+  v = block_sum(v, red);
+  if (threadIdx.x == 0) part[rank] = v;
+}
+
+// partial dots of w against q_0..q_{nv-1} over [b0, b1) -> part[v][rank];
+// also self-dot w.w -> part[nv][rank] when self
+__device__ void pz_dots(const PzArgs& a, int nv, long b0, long b1, int rank, double* part, bool self,
+                        double (*sh)[65]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt = nv + (self ? 1 : 0);
+  for (int v0 = 0; v0 < nt; v0 += DOT_GROUP) {
+    double acc[DOT_GROUP];
+#pragma unroll
+    for (int g = 0; g < DOT_GROUP; ++g) acc[g] = 0.0;
+    for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) {
+      const double wx = a.w[x];
+#pragma unroll
+      for (int g = 0; g < DOT_GROUP; ++g) {
+        const int v = v0 + g;
+        if (v < nv)
+          acc[g] += a.Q[v * a.stride + x] * wx;
+        else if (v == nv && self)
+          acc[g] += wx * wx;
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < DOT_GROUP; ++g) {
+      const double r = warp_sum(acc[g]);
+      if (lane == 0 && v0 + g < nt) sh[warp][v0 + g] = r;
+    }
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < nt; v += PZ_THREADS) {
+    double t = 0.0;
+#pragma unroll
+    for (int w8 = 0; w8 < PZ_THREADS / 32; ++w8) t += sh[w8][v];
+    part[static_cast<long>(v) * a.W + rank] = t;
+  }
+  __syncthreads();
+}
+
+// matvec w = H theta over the workers: phases A and B of heff_phases.cuh with
+// a barrier after each; the caller folds phase C (sum over e) into its next
+// elementwise pass via pz_w().
+__device__ void pz_matvec(const PzArgs& a, hs::HsArgs& h, const hs::MixSmem& mw, const double* theta,
+                          double* As, double* Bs, int rank, unsigned& gen) {
+  hs::phase_a<hs::HS_KMAX>(h, mw, theta, As, Bs, rank, a.W);
+  pz_sync(a, gen);
+  hs::phase_b<hs::HS_KMAX>(h, As, Bs, rank, a.W);
+  pz_sync(a, gen);
+}
+__device__ __forceinline__ double pz_w(const hs::HsArgs& h, long tot, long x) {
+  double v = 0.0;
+  for (int e = 0; e < h.D3; ++e) v += h.part[e * tot + x];
+  return v;
+}
+
+// the tridiagonal CTA: one job per step (j, matvecs before the cycle); the
+// lowest pair of T_{j+1} (hinted by the previous step of the same cycle), the
+// residual bound and the stop decision, posted by job parity.
+__device__ void pz_tridiag_cta(const PzArgs& a) {
+  __shared__ double sa[LANCZOS_BLOCK], sb[LANCZOS_BLOCK], sbb[LANCZOS_BLOCK];
+  __shared__ double th_s, sc_s;
+  __shared__ int jj_s, mv_s;
+  __shared__ TwistScratch tw;
+  unsigned seq = 0;
+  double theta_prev = 0.0, r_prev = 0.0;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      while (ld_acquire(a.posted) <= seq) __nanosleep(32);
+      const int p = (seq + 1) & 1;
+      jj_s = *reinterpret_cast<volatile int*>(&a.job[2 * p]);
+      mv_s = *reinterpret_cast<volatile int*>(&a.job[2 * p + 1]);
+    }
+    __syncthreads();
+    ++seq;
+    const int j = jj_s, mv0 = mv_s;
+    if (j < 0) return;  // the workers are done
+    const int p = seq & 1;
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+      const double bi = __ldcg(a.beta + i);
+      sa[i] = __ldcg(a.alpha + i);
+      sb[i] = bi;
+      sbb[i] = bi * bi;
+    }
+    __syncthreads();
+    const int k = j + 1;
+    double* s = a.sbuf + 64 * p;
+    if (threadIdx.x < 32) {
+      double theta = sa[0], scale = fabs(sa[0]);
+      if (k > 1) theta = tridiag_lowest_value(sa, sb, sbb, k, true, theta_prev, r_prev, &scale);
+      if (threadIdx.x == 0) {
+        th_s = theta;
+        sc_s = scale;
+      }
+    }
+    __syncthreads();
+    const double theta = th_s, scale = sc_s;
+    if (k > 1)
+      tridiag_vector_twisted(sa, sb, sbb, k, theta, scale, tw, s);
+    else if (threadIdx.x == 0)
+      s[0] = 1.0;
+    __syncthreads();
+    const double bn = sb[j];
+    const double res_bound = bn * fabs(s[j]);
+    theta_prev = theta;
+    r_prev = res_bound;
+    if (threadIdx.x == 0) {
+      const double tscale = fmax(1.0, fabs(theta));
+      const bool breakdown = bn <= 1e-14 * tscale;
+      const bool stop = res_bound <= a.tol * tscale || breakdown || j + 1 == a.block ||
+                        mv0 + j + 1 >= a.max_iter;
+      double* r = a.tres + 4 * p;
+      r[0] = theta;
+      r[1] = res_bound;
+      r[2] = bn;
+      r[3] = sa[j];
+      a.dec[p] = stop ? 1 : 0;
+      __threadfence();
+      st_release(a.done, seq);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(PZ_THREADS) lanczos_persistent_kernel(PzArgs a) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ hs::MixSmem mw;
+  __shared__ double sh[PZ_THREADS / 32][65];
+  __shared__ double coef[66];
+  __shared__ double red[32];
+  __shared__ double scal[8];
+  const int rank = blockIdx.x;
+  if (rank == a.W) {
+    pz_tridiag_cta(a);
+    return;
+  }
+  double* As = reinterpret_cast<double*>(dyn);
+  double* Bs = As + hs::HS_TM * hs::hs_ld<hs::HS_KMAX>();
+  hs::load_mix(a.h.mix, mw);
+  hs::HsArgs h = a.h;
+  const long n = a.n, tot = n;
+  const long chunk = (n + a.W - 1) / a.W;
+  const long b0 = static_cast<long>(rank) * chunk, b1 = min(n, b0 + chunk);
+  unsigned gen = 0, seq = 0;
+  auto post = [&](int j, int mv0) {  // worker 0 posts step j to the tridiagonal CTA
+    if (rank == 0 && threadIdx.x == 0) {
+      const int p = (seq + 1) & 1;
+      a.job[2 * p] = j;
+      a.job[2 * p + 1] = mv0;
+      __threadfence();
+      st_release(a.posted, seq + 1);
+    }
+    ++seq;
+  };
+  auto wait_done = [&](unsigned s) {
+    if (threadIdx.x == 0)
+      while (ld_acquire(a.done) < s) __nanosleep(32);
+    __syncthreads();
+  };
+  auto finish = [&](int flags, int matvecs, int steps, int cycles, double best, double ev, double res,
+                    const double* tr) {
+    if (rank == 0 && threadIdx.x == 0) {
+      LanczosCtl& c = *a.ctl;
+      c.flags = flags;
+      c.matvecs = matvecs;
+      c.steps = steps;
+      c.cycles = cycles;
+      c.best = best;
+      c.tol = a.tol;
+      c.block = a.block;
+      c.max_iter = a.max_iter;
+      a.st->ev = ev;
+      a.st->res = res;
+      if (tr) {
+        a.st->theta = __ldcg(tr);
+        a.st->res_bound = __ldcg(tr + 1);
+        a.st->bnorm = __ldcg(tr + 2);
+        a.st->alpha = __ldcg(tr + 3);
+      }
+    }
+    post(-1, 0);  // release the tridiagonal CTA
+  };
+  // ---- prologue: q_0 = v0 / ||v0|| (linalg.cpp:109-115) ----
+  {
+    double v = 0.0;
+    for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) v += a.v0[x] * a.v0[x];
+    pz_put(v, a.pc, rank, red);
+    pz_sync(a, gen);
+    pz_reduce(a.pc, 1, a.W, coef);
+    const double n2 = coef[0];
+    if (!(n2 > 0)) {
+      finish(LZ_BAD_V0, 0, 0, 0, INFINITY, 0.0, 0.0, nullptr);
+      return;
+    }
+    const double inv = 1.0 / sqrt(n2);
+    for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) a.Q[x] = a.v0[x] * inv;
+    pz_sync(a, gen);
+  }
+  int matvecs = 0, steps = 0, cycles = 0;
+  double best = INFINITY;
+  for (;;) {  // restart cycles (linalg.cpp:126-170)
+    ++cycles;
+    const int mv0 = matvecs;
+    int j = 0, k = 0;
+    unsigned seq_last = 0;  // job of the final step
+    for (;; ++j) {
+      // ---- step j: w = H q_j, orthogonalise, q_{j+1} ----
+      const bool pf = a.prof && rank == 0 && threadIdx.x == 0;
+      unsigned long long t0 = pf ? clock64() : 0, t1 = 0;
+      auto mark = [&](int slot) {
+        if (pf) {
+          t1 = clock64();
+          a.prof[slot] += t1 - t0;
+          t0 = t1;
+        }
+      };
+      hs::phase_a<hs::HS_KMAX>(h, mw, a.Q + j * a.stride, As, Bs, rank, a.W);
+      mark(0);
+      pz_sync(a, gen);
+      mark(1);
+      hs::phase_b<hs::HS_KMAX>(h, As, Bs, rank, a.W);
+      mark(2);
+      pz_sync(a, gen);
+      mark(3);
+      const int nv = j + 1;
+      for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) a.w[x] = pz_w(h, tot, x);
+      // (each thread reads back only the w[x] it wrote)
+      pz_dots(a, nv, b0, b1, rank, a.pa, false, sh);
+      mark(4);
+      pz_sync(a, gen);
+      mark(5);
+      pz_reduce(a.pa, nv, a.W, coef);
+      const double alpha_j = coef[nv - 1];
+      double nrm1 = 0.0;
+      for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) {
+        const double v = project_out(a.Q, a.stride, nv, coef, a.w[x], x);
+        a.w[x] = v;
+        nrm1 += v * v;
+      }
+      nrm1 = block_sum(nrm1, red);
+      if (threadIdx.x == 0) a.pb[static_cast<long>(nv) * a.W + rank] = nrm1;
+      __syncthreads();
+      pz_dots(a, nv, b0, b1, rank, a.pb, false, sh);
+      mark(6);
+      pz_sync(a, gen);
+      mark(7);
+      pz_reduce(a.pb, nv + 1, a.W, coef);
+      double h2sq = 0.0;
+      for (int i = 0; i < nv; ++i) h2sq = fma(coef[i], coef[i], h2sq);
+      const double wn2 = coef[nv];
+      const bool pyth = h2sq <= 0.25 * wn2;
+      double nrm = 0.0;
+      for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) {
+        const double v = project_out(a.Q, a.stride, nv, coef, a.w[x], x);
+        a.w[x] = v;
+        nrm += v * v;
+      }
+      double bn;
+      if (!pyth) {
+        pz_put(nrm, a.pc, rank, red);
+        pz_sync(a, gen);
+        pz_reduce(a.pc, 1, a.W, scal);
+        bn = sqrt(scal[0]);
+      } else {
+        bn = sqrt(fmax(wn2 - h2sq, 0.0));
+      }
+      if (j + 1 <= LANCZOS_BLOCK && bn > 0) {
+        const double inv = 1.0 / bn;
+        double* qn = a.Q + (j + 1) * a.stride;
+        for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) qn[x] = a.w[x] * inv;
+      }
+      if (rank == 0 && threadIdx.x == 0) {
+        a.alpha[j] = alpha_j;
+        a.beta[j] = bn;
+      }
+      __syncthreads();
+      mark(8);
+      post(j, mv0);
+      const unsigned seq_j = seq;
+      pz_sync(a, gen);  // q_{j+1} complete
+      mark(9);
+      ++steps;
+      // the decision of step j-1 (posted one step ago)
+      if (j >= 1) {
+        wait_done(seq_j - 1);
+        mark(10);
+        if (pf) a.prof[11] += 1;
+        if (__ldcg(a.dec + ((seq_j - 1) & 1))) {  // stopped at j-1: this step is discarded
+          k = j;
+          seq_last = seq_j - 1;
+          --steps;
+          break;
+        }
+      }
+      if (j + 1 == a.block || mv0 + j + 1 >= a.max_iter) {  // stops at j regardless
+        wait_done(seq_j);
+        k = j + 1;
+        seq_last = seq_j;
+        break;
+      }
+    }
+    matvecs = mv0 + k;
+    // ---- Ritz vector r = normalize(Q s), s from step k-1 (linalg.cpp:154-155) ----
+    const double* s = a.sbuf + 64 * (seq_last & 1);
+    const double* tr = a.tres + 4 * (seq_last & 1);
+    for (int i = threadIdx.x; i < k; i += PZ_THREADS) coef[i] = __ldcg(s + i);
+    __syncthreads();
+    {
+      double v = 0.0;
+      for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) {
+        double r = 0.0;
+        for (int i = 0; i < k; ++i) r += coef[i] * a.Q[i * a.stride + x];
+        a.ritz[x] = r;
+        v += r * r;
+      }
+      pz_put(v, a.pc, rank, red);
+      pz_sync(a, gen);
+      pz_reduce(a.pc, 1, a.W, scal);
+      const double inv = 1.0 / sqrt(scal[0]);
+      for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) a.ritz[x] *= inv;
+      pz_sync(a, gen);
+    }
+    // ---- explicit residual (linalg.cpp:156-162): w = H r, ev = r.w, ||w - ev r|| ----
+    pz_matvec(a, h, mw, a.ritz, As, Bs, rank, gen);
+    ++matvecs;
+    {
+      double v = 0.0;
+      for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) {
+        const double wx = pz_w(h, tot, x);
+        a.w[x] = wx;
+        v += a.ritz[x] * wx;
+      }
+      pz_put(v, a.pc, rank, red);
+      pz_sync(a, gen);
+      pz_reduce(a.pc, 1, a.W, scal);
+    }
+    const double ev = scal[0];
+    {
+      double v = 0.0;
+      for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) {
+        const double t = a.w[x] - ev * a.ritz[x];
+        a.tmp[x] = t;
+        v += t * t;
+      }
+      pz_put(v, a.pa, rank, red);
+      pz_sync(a, gen);
+      pz_reduce(a.pa, 1, a.W, scal + 1);
+    }
+    const double res = sqrt(scal[1]);
+    best = fmin(best, res);
+    if (res <= a.tol * fmax(1.0, fabs(ev))) {
+      if (a.out != a.ritz)
+        for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) a.out[x] = a.ritz[x];
+      finish(LZ_CONVERGED, matvecs, steps, cycles, best, ev, res, tr);
+      return;
+    }
+    if (matvecs >= a.max_iter) {
+      finish(LZ_NONCONVERGED, matvecs, steps, cycles, best, ev, res, tr);
+      return;
+    }
+    // ---- restart (linalg.cpp:163-169) ----
+    const bool breakdown = __ldcg(tr + 2) <= 1e-14 * fmax(1.0, fabs(__ldcg(tr)));
+    if (breakdown) {
+      const double f = res > 0 ? 1e-8 / res : 0.0;
+      double v = 0.0;
+      for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) {
+        const double q = a.ritz[x] + f * a.tmp[x];
+        a.Q[x] = q;
+        v += q * q;
+      }
+      pz_put(v, a.pb, rank, red);
+      pz_sync(a, gen);
+      pz_reduce(a.pb, 1, a.W, scal + 2);
+      const double inv = 1.0 / sqrt(scal[2]);
+      for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) a.Q[x] *= inv;
+    } else {
+      for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) a.Q[x] = a.ritz[x];
+    }
+    pz_sync(a, gen);
+  }
+}
+
 struct Kernels {
   Ctx& ctx;
   LanczosWs& ws;
@@ -958,9 +1426,9 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
   static PinnedArr<unsigned long long> prof_h;
   static thread_local long prof_calls = 0;
   if (prof_on && !prof_buf.p) {
-    prof_buf.reserve(8);
+    prof_buf.reserve(16);
     prof_h.reserve(8);
-    ACHI_CUDA(cudaMemsetAsync(prof_buf.p, 0, 8 * sizeof(unsigned long long), ctx.stream));
+    ACHI_CUDA(cudaMemsetAsync(prof_buf.p, 0, 16 * sizeof(unsigned long long), ctx.stream));
   }
   if (prof_on && ++prof_calls % 200 == 0) {
     ACHI_CUDA(cudaMemcpyAsync(prof_h.p, prof_buf.p, 8 * sizeof(unsigned long long),
@@ -1095,6 +1563,59 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
     R.ctl.matvecs = matvecs;
     R.ctl.best = best;
     R.ctl.flags = LZ_NONCONVERGED;
+    return;
+  }
+
+  // ---- small blocks: the whole eigensolve as one persistent cooperative kernel ----
+  static const bool persist_on = [] {
+    const char* e = std::getenv("ACHI_LANCZOS_PERSIST");
+    return !(e && e[0] == '0');
+  }();
+  hs::HsArgs pz_h{};
+  long pz_items = 0;
+  if (persist_on && small_op && heff_small_fusable(ctx, *small_op, ws.qcur.p, ws.w.p, &pz_h, &pz_items)) {
+    const size_t smem = hs::smem_bytes<hs::HS_KMAX>();
+    const int maxres = per_device_once("lanczos_persistent_kernel", ctx.device, [&] {
+      ACHI_CUDA(cudaFuncSetAttribute(lanczos_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+      int per_sm = 0;
+      ACHI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lanczos_persistent_kernel, PZ_THREADS,
+                                                              smem));
+      return std::max(1, per_sm) * ctx.num_sms;
+    });
+    const int W = static_cast<int>(std::max<long>(1, std::min<long>(
+        std::max<long>(pz_items, cdiv(n, 4L * PZ_THREADS)), ctx.cap_grid(maxres) - 1)));
+    double* pzd = ws.pzd.reserve(static_cast<size_t>(130) * W + 256);
+    int* pzi = ws.pzi.reserve(16);
+    ACHI_CUDA(cudaMemsetAsync(pzi, 0, 16 * sizeof(int), ctx.stream));
+    PzArgs pa{pz_h, ws.q(0), ws.stride, ws.w.p, ws.ritz.p, ws.tmp.p, v0, out, n,
+              pzd, pzd + 64L * W, pzd + 129L * W, ws.alpha(), ws.beta(),
+              pzd + 130L * W, pzd + 130L * W + 128, pzi, pzi + 2,
+              reinterpret_cast<unsigned*>(pzi + 6), reinterpret_cast<unsigned*>(pzi + 7),
+              reinterpret_cast<unsigned*>(pzi + 8), ws.ctl.p, K.dev_status(), tol, block, max_iter, W,
+              prof_on ? prof_buf.p : nullptr};
+    if (prof_on && prof_calls % 200 == 0) {
+      static PinnedArr<unsigned long long> ph;
+      ph.reserve(16);
+      ACHI_CUDA(cudaMemcpyAsync(ph.p, prof_buf.p, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                ctx.stream));
+      ctx.sync();
+      const double st = ph.p[11] ? static_cast<double>(ph.p[11]) : 1.0;
+      std::fprintf(stderr,
+                   "[lanczos-persist] W=%d steps=%llu cycles/step: A %.0f bar %.0f B %.0f bar %.0f C+dots %.0f "
+                   "bar %.0f proj+dots %.0f bar %.0f proj+q %.0f bar %.0f wait %.0f\n",
+                   W, ph.p[11], ph.p[0] / st, ph.p[1] / st, ph.p[2] / st, ph.p[3] / st, ph.p[4] / st,
+                   ph.p[5] / st, ph.p[6] / st, ph.p[7] / st, ph.p[8] / st, ph.p[9] / st, ph.p[10] / st);
+    }
+    void* kargs[] = {&pa};
+    ACHI_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lanczos_persistent_kernel), dim3(W + 1),
+                                          dim3(PZ_THREADS), kargs, smem, ctx.stream));
+    ACHI_LAUNCHED(ctx);
+    ws.pend_graph = false;
+    LanczosResult* R = ws.res_h.p;
+    ACHI_CUDA(cudaMemcpyAsync(&R->ctl, ws.ctl.p, sizeof(LanczosCtl), cudaMemcpyDeviceToHost, ctx.stream));
+    ACHI_CUDA(cudaMemcpyAsync(&R->st, K.dev_status(), sizeof(LanczosStatus), cudaMemcpyDeviceToHost,
+                              ctx.stream));
     return;
   }
 

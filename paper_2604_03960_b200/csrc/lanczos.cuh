@@ -62,6 +62,8 @@ struct LanczosWs {
   DevBuf scal;    // alpha[64] beta[64] h1[64] h2[64] s[64] misc[64]
   DevArr<LanczosCtl> ctl;
   DevArr<unsigned> bar;  // sub-grid barrier counter of the fused small-chi step
+  DevBuf pzd;            // persistent eigensolve: partials, eigenvector / result slots
+  DevArr<int> pzi;       // persistent eigensolve: jobs, decisions, counters, barrier
   PinnedArr<LanczosCtl> ctl_h;
   PinnedArr<LanczosResult> res_h;  // result of the last eigs_lowest_async
   int64_t pend_body = 0, pend_cycle = 0, pend_once = 0;  // launch accounting of that call
