@@ -1583,8 +1583,14 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
                                                               smem));
       return std::max(1, per_sm) * ctx.num_sms;
     });
+    // workers: at least one per matvec work item, and few enough vector elements per
+    // thread that the orthogonalisation passes keep their loads in flight
+    static const int pz_elems = [] {
+      const char* e = std::getenv("ACHI_PZ_ELEMS");
+      return e ? std::max(1, std::atoi(e)) : 1;
+    }();
     const int W = static_cast<int>(std::max<long>(1, std::min<long>(
-        std::max<long>(pz_items, cdiv(n, 4L * PZ_THREADS)), ctx.cap_grid(maxres) - 1)));
+        std::max<long>(pz_items, cdiv(n, static_cast<long>(pz_elems) * PZ_THREADS)), ctx.cap_grid(maxres) - 1)));
     double* pzd = ws.pzd.reserve(static_cast<size_t>(130) * W + 256);
     int* pzi = ws.pzi.reserve(16);
     ACHI_CUDA(cudaMemsetAsync(pzi, 0, 16 * sizeof(int), ctx.stream));
