@@ -308,11 +308,12 @@ def run_ours(args, dist):
                             "rotations of every block pair), summed over the sweeps of each SVD",
                 "peak_source": "measured DMMA peak (profiles/fp64_peak_r01.txt)"}
     roof_mv = {"bound": "tensor",
-               "kernel": "Lanczos eigensolve: H_eff matvec (heff_small_kernel for chi <= 128, "
-                         "else dmma_gemm_kernel x2 + mpo_mix_kernel) + lanczos_orth_kernel",
+               "kernel": "Lanczos eigensolve: lanczos_persistent_kernel (one launch per eigensolve "
+                         "for chi <= 128: fused H_eff phases + CGS2 + tridiagonal CTA), else the "
+                         "graph of dmma_gemm_kernel x2 + mpo_mix_kernel + lanczos_orth_kernel",
                "achieved": round(mv_tfs, 4), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                "frac": round(mv_tfs / FP64_PEAK_TFLOPS, 6),
-               "traffic": traffic.get("lanczos_orth_kernel"),
+               "traffic": traffic.get("lanczos_persistent_kernel"),
                "work_def": "matvecs x (2*D*d^2*chl*chr*(chl+chr)+4*D^2*d^3*chl*chr) flops over the "
                            "eigensolve's device time (orthogonalisation and tridiagonal included)",
                "peak_source": "measured DMMA peak (profiles/fp64_peak_r01.txt)"}

@@ -311,6 +311,29 @@ int achi_bond_select(achi_ctx* ctx, const achi_dmrg_config* cfg, int n_sigma,
 int achi_dgemm(achi_ctx* ctx, int M, int N, int K, int a_kmajor, const double* a, long lda,
                int b_kmajor, const double* b, long ldb, double* c, long ldc);
 
+/* Route this context's contractions (H_eff, environments, theta merge) of at
+ * least min_flops (2 M N K) through achi_dgemm_ozaki's engine with `slices`
+ * digits (0 = off: the native DMMA engine, the default).  While on, the
+ * context's Lanczos loops are stepped from the host. */
+int achi_ctx_set_ozaki(achi_ctx* ctx, int slices, double min_flops);
+
+/* achi_dgemm on device pointers (queued on the context stream, no sync). */
+int achi_dgemm_device(achi_ctx* ctx, int M, int N, int K, int a_kmajor, const double* d_a, long lda,
+                      int b_kmajor, const double* d_b, long ldb, double* d_c, long ldc);
+
+/* Emulated-FP64 GEMM on the int8 tensor cores (Ozaki scheme, tcgen05.mma
+ * kind::i8, the north_star's "optionally emulated-precision"
+ * contraction): C (M x N row-major, ldc) = A B with every FP64 operand entry
+ * cut into `slices` signed 7-bit digits against a power-of-two scale per row
+ * of A / column of B, all digit products with p + q <= slices + 1 exact in
+ * int32 TMEM accumulators.  slices = 8 carries 56 bits (FP64 level); fewer
+ * trade accuracy for speed.  Device pointers.  A: M x K row-major (lda), or
+ * K x M when a_trans; B: K x N row-major (ldb), or N x K when b_kmajor.
+ * K <= 16384.  Queued on the context stream.  Replaces the GEMM inside
+ * Tensor::contract (tensor.hpp:195-196) as an opt-in alternative to the DMMA engine. */
+int achi_dgemm_ozaki_device(achi_ctx* ctx, int M, int N, int K, const double* d_a, long lda, int a_trans,
+                            const double* d_b, long ldb, int b_kmajor, double* d_c, long ldc, int slices);
+
 /* Device-resident timing hook for K1: `reps` applications of the effective
  * Hamiltonian at chl = chr = chi (XXZ bulk MPO, D = 5) on pseudo-random
  * device data; returns the average device ms per matvec and the achieved

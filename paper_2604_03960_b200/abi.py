@@ -179,6 +179,12 @@ def load():
         "achi_device_times_ex": (C.c_int, [vp, C.c_int, C.c_int, dp, C.c_int]),
         "achi_ctx_set_lanczos_graph": (C.c_int, [vp, C.c_int]),
         "achi_svd_complex": (C.c_int, [vp, C.c_int, C.c_int, dp, dp, dp, dp, P(C.c_int)]),
+        "achi_ctx_set_ozaki": (C.c_int, [vp, C.c_int, d]),
+        "achi_dgemm_device": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_long,
+                                        C.c_int, C.c_void_p, C.c_long, C.c_void_p, C.c_long]),
+        "achi_dgemm_ozaki_device": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_long,
+                                              C.c_int, C.c_void_p, C.c_long, C.c_int, C.c_void_p,
+                                              C.c_long, C.c_int]),
         "achi_eigs_lowest_callback": (C.c_int, [vp, C.c_int, MATVEC_FN, C.c_void_p, dp, d, C.c_int,
                                                 dp, dp, P(C.c_int), dp]),
         "achi_svd_complex_device": (C.c_int, [vp, C.c_int, C.c_int, C.c_void_p, C.c_void_p,

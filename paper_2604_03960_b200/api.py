@@ -256,6 +256,23 @@ class Context:
         self._check(rc)
         return ev.value, vec, mv.value, res.value
 
+    def dgemm_ozaki_device(self, M, N, K, d_a, lda, d_b, ldb, d_c, ldc, slices=8, a_trans=False,
+                           b_kmajor=False):
+        """Emulated-FP64 GEMM on the int8 tensor cores (device pointers): C = A B."""
+        self._check(self.lib.achi_dgemm_ozaki_device(self.h, M, N, K, C.c_void_p(d_a), lda,
+                                                     int(a_trans), C.c_void_p(d_b), ldb, int(b_kmajor),
+                                                     C.c_void_p(d_c), ldc, int(slices)))
+
+    def set_ozaki(self, slices, min_flops=1e9):
+        """Emulated-FP64 contractions on the int8 tensor cores for GEMMs of at least
+        min_flops (0 slices: off, the native DMMA engine)."""
+        self._check(self.lib.achi_ctx_set_ozaki(self.h, int(slices), float(min_flops)))
+
+    def dgemm_device(self, M, N, K, d_a, lda, d_b, ldb, d_c, ldc, a_kmajor=True, b_kmajor=False):
+        """The DMMA GEMM engine on device pointers (queued, no sync): C = A B."""
+        self._check(self.lib.achi_dgemm_device(self.h, M, N, K, int(a_kmajor), C.c_void_p(d_a), lda,
+                                               int(b_kmajor), C.c_void_p(d_b), ldb, C.c_void_p(d_c), ldc))
+
     def dgemm(self, a, b, a_kmajor=True, b_kmajor=False):
         """C = A @ B on the TMA/DMMA engine.  a: (M,K) if a_kmajor else (K,M) stored;
         b: (N,K) if b_kmajor else (K,N) stored."""

@@ -4,6 +4,7 @@
 #include <memory>
 
 #include "chain.cuh"
+#include "ozaki.cuh"
 
 using namespace achi;
 
@@ -169,6 +170,14 @@ int achi_flush_l2(achi_ctx* ctx, size_t bytes) {
     const size_t n = bytes / sizeof(double);
     c.flush.reserve(n);
     ACHI_CUDA(cudaMemsetAsync(c.flush.p, 0, n * sizeof(double), c.stream));
+  });
+}
+
+int achi_ctx_set_ozaki(achi_ctx* ctx, int slices, double min_flops) {
+  return guard(ctx, [&] {
+    if (slices != 0 && (slices < 2 || slices > OZ_MAX_SLICES)) fail(ACHI_E_INVALID_CONFIG, "ozaki: slices 0 or 2..9");
+    ctx->c.ozaki_slices = slices;
+    ctx->c.ozaki_min_flops = min_flops;
   });
 }
 
@@ -608,6 +617,15 @@ int achi_dgemm(achi_ctx* ctx, int M, int N, int K, int a_kmajor, const double* a
   });
 }
 
+int achi_dgemm_device(achi_ctx* ctx, int M, int N, int K, int a_kmajor, const double* d_a, long lda,
+                      int b_kmajor, const double* d_b, long ldb, double* d_c, long ldc) {
+  return guard(ctx, [&] {
+    Ctx& cx = ctx->c;
+    gemm(cx, M, N, K, Operand{d_a, lda, a_kmajor ? Major::kK : Major::kMN},
+         Operand{d_b, ldb, b_kmajor ? Major::kK : Major::kMN}, d_c, ldc);
+  });
+}
+
 int achi_spectrum_stats(achi_ctx* ctx, int n_sigma, const double* sigma, int kept, double eps,
                         double* out4) {
   return guard(ctx, [&] {
@@ -686,6 +704,14 @@ int achi_eigs_lowest_dense(achi_ctx* ctx, int dim, const double* h, const double
     *eigenvalue = e.eigenvalue;
     *matvecs = e.matvecs;
     *residual = e.residual;
+  });
+}
+
+int achi_dgemm_ozaki_device(achi_ctx* ctx, int M, int N, int K, const double* d_a, long lda, int a_trans,
+                            const double* d_b, long ldb, int b_kmajor, double* d_c, long ldc, int slices) {
+  return guard(ctx, [&] {
+    if (M < 1 || N < 1 || K < 1) fail(ACHI_E_INVALID_MATRIX, "ozaki: empty operand");
+    dgemm_ozaki(ctx->c, M, N, K, d_a, lda, a_trans != 0, d_b, ldb, b_kmajor != 0, d_c, ldc, slices);
   });
 }
 

@@ -222,6 +222,12 @@ struct Ctx {
   // (0: every kernel visible to ncu and to the per-matvec event accounting),
   // or the process default (-1: ACHI_LANCZOS_GRAPH, on unless "0")
   int lanczos_graph = -1;
+  // emulated-FP64 contractions on the int8 tensor cores (ozaki.cu): digits per
+  // operand entry (0: off, the DMMA engine) for GEMMs of at least ozaki_min_flops
+  int ozaki_slices = 0;
+  double ozaki_min_flops = 1e9;
+  DevBuf oz_digits;
+  DevArr<int> oz_ex;
   int cap_grid(long want) const {
     return static_cast<int>(grid_cap > 0 ? std::min<long>(want, grid_cap) : want);
   }

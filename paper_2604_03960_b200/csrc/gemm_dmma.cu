@@ -1,6 +1,7 @@
 // Host side of the TMA-fed DMMA GEMM: tensor-map encoding, tile-config and
 // split-K selection, deterministic split-K reduction.
 #include "gemm_dmma.cuh"
+#include "ozaki.cuh"
 
 namespace achi {
 namespace gemm_detail {
@@ -110,6 +111,12 @@ void gemm(Ctx& ctx, int M, int N, int K, const Operand& A, const Operand& B, dou
   if (K <= 0) {
     for (int r = 0; r < M; ++r)
       ACHI_CUDA(cudaMemsetAsync(C + static_cast<long>(r) * ldc, 0, sizeof(double) * N, ctx.stream));
+    return;
+  }
+  if (ctx.ozaki_slices > 0 && 2.0 * M * N * K >= ctx.ozaki_min_flops && K <= (1 << 14)) {
+    // opt-in emulated FP64 on the int8 tensor cores (ozaki.cu)
+    dgemm_ozaki(ctx, M, N, K, A.ptr, A.ld, A.major == Major::kMN, B.ptr, B.ld, B.major == Major::kK, C, ldc,
+                ctx.ozaki_slices);
     return;
   }
   if (A.major == Major::kK && B.major == Major::kMN)

@@ -1382,7 +1382,9 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
     const char* e = std::getenv("ACHI_LANCZOS_GRAPH");
     return !(e && e[0] == '0');
   }();
-  const bool use_graph = ctx.lanczos_graph >= 0 ? ctx.lanczos_graph != 0 : graph_default;
+  // (the emulated-FP64 engine sizes its digit workspace per call: no graph capture)
+  const bool use_graph = ctx.ozaki_slices == 0 &&
+                         (ctx.lanczos_graph >= 0 ? ctx.lanczos_graph != 0 : graph_default);
   ws.pend_graph = use_graph;
   // ACHI_LANCZOS_FUSED=1 (opt-in): for chi <= 128 in graph mode the whole step is
   // one cooperative launch (lanczos_step_small_kernel) over max(orthogonalisation
