@@ -551,3 +551,22 @@ def test_expectation_energy_and_snapshot_reload(ctx, oracle, tmp_path):
     assert abs(other.energy() - e_state) <= 1e-10 * abs(e_state)
     r2 = other.sweep(3)
     assert abs(r2["energy"] - e_last) <= 1e-10 * abs(e_last)
+
+
+# ---------------- the contraction engine itself (achi_dgemm) ----------------
+
+@pytest.mark.parametrize("M,N,K", [(64, 64, 64), (128, 128, 32), (1280, 1024, 256), (1024, 256, 1280),
+                                   (512, 96, 480), (2, 2, 2), (130, 70, 18)])
+def test_dgemm_operand_majors(ctx, M, N, K):
+    """Every operand-major combination of the TMA/DMMA GEMM (gemm_dmma.cuh) that the
+    contractions use, including the split-K and 128x128-tile configurations."""
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    for ak in (True, False):
+        for bk in (False, True):
+            a = rng.standard_normal((M, K) if ak else (K, M))
+            b = rng.standard_normal((N, K) if bk else (K, N))
+            c = ctx.dgemm(a, b, ak, bk)
+            A = a if ak else a.T
+            B = b.T if bk else b
+            ref = A @ B
+            assert np.abs(c - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max()) * np.sqrt(K), (ak, bk)
