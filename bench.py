@@ -429,21 +429,49 @@ def heff_insweep(ctx, args):
     cfg = abi.fixed_config(CHI_MAX, max_sweeps=s_idx + 1, eps_conv=1e-300)
     ctx.set_lanczos_graph(0)
     ch = Chain(ctx, spec, cfg)
+    oz = None
     try:
         for s in range(s_idx):
             ch.sweep(s)
+        sites = ch.sites() if args.ozaki_slices > 0 else None
         ctx.device_times(enable=True, reset=True)
         ctx.timer_start()
         r = ch.sweep(s_idx)
         sweep_ms = ctx.timer_stop()
         ph = ctx.device_times(enable=False)
+        if sites is not None:
+            # the same sweep from the same state with every large contraction (H_eff,
+            # environments, theta merge) on the emulated-FP64 int8 engine (ozaki.cu)
+            ch.close()
+            ch2 = Chain(ctx, spec, cfg)
+            ch2.load_state(sites)
+            del sites
+            ctx.set_ozaki(args.ozaki_slices)
+            try:
+                ctx.device_times(enable=True, reset=True)
+                ctx.timer_start()
+                r2 = ch2.sweep(s_idx)
+                ms2 = ctx.timer_stop()
+                ph2 = ctx.device_times(enable=False)
+            finally:
+                ctx.set_ozaki(0)
+                ch2.close()
+            h2 = ph2["heff"]
+            tf2 = h2["work"] / max(h2["ms"], 1e-9) / 1e9
+            oz = {"digits": args.ozaki_slices, "achieved": round(tf2, 3), "unit": "TFLOP/s (FP64-equivalent)",
+                  "frac_of_dmma_peak": round(tf2 / FP64_PEAK_TFLOPS, 4), "heff_ms": round(h2["ms"], 2),
+                  "sweep_ms": round(ms2, 1),
+                  "energy_rel_diff_vs_native": abs(r2["energy"] - r["energy"]) / abs(r["energy"]),
+                  "chi_profile_equal": bool((r2["chi_profile"] == r["chi_profile"]).all()),
+                  "note": "the same sweep from the same state, H_eff/environment/merge GEMMs of >= 1 GFLOP "
+                          "on tcgen05.mma kind::i8 (Ozaki digits), everything else unchanged"}
     finally:
         ch.close()
         ctx.set_lanczos_graph(-1)
     h = ph["heff"]
     tf = h["work"] / max(h["ms"], 1e-9) / 1e9
     chi = r["chi_profile"]
-    return {"bound": "tensor",
+    out = {"bound": "tensor",
             "kernel": "H_eff matvec in a real sweep (dmma_gemm_kernel x2 + mpo_mix_kernel; "
                       "heff_small_kernel at the chain ends)",
             "achieved": round(tf, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
@@ -455,6 +483,9 @@ def heff_insweep(ctx, args):
             "work_def": "sum over the sweep's matvecs of 2*D*d^2*chl*chr*(chl+chr)+4*D^2*d^3*chl*chr "
                         "flops / sum of their CUDA-event times",
             "peak_source": "measured DMMA peak (profiles/fp64_peak_r01.txt)"}
+    if oz is not None:
+        out["emulated_fp64"] = oz
+    return out
 
 
 def svd_part(ctx, args):
@@ -627,6 +658,8 @@ def main():
     ap.add_argument("--skip-complex-svd", action="store_true")
     ap.add_argument("--skip-heff-insweep", action="store_true")
     ap.add_argument("--heff-sweep", type=int, default=5)
+    ap.add_argument("--ozaki-slices", type=int, default=7,
+                    help="digits of the emulated-FP64 leg of the in-sweep H_eff measurement (0: skip)")
     ap.add_argument("--skip-real", action="store_true")
     ap.add_argument("--real-budget-s", type=float, default=100.0)
     ap.add_argument("--c4-chains", type=int, default=64)

@@ -246,6 +246,149 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128u));
 }
 
+// ---- staged variant: every digit tile of a K chunk is loaded once ----
+// For each 64-byte K chunk all s digit tiles of A (128 rows) and of B (64 rows)
+// are staged (SWIZZLE_64B), then every digit pair with p + q <= s + 1 is issued
+// into the TMEM accumulator of its weight (s accumulators x 64 columns <= 512):
+// each digit tile is read from L2 once per chunk instead of once per pair (the
+// pair loop of ozaki_gemm_kernel re-streams it ~s/2 times).  Two stages.
+constexpr int SKB = 64;  // K bytes per stage row (64B swizzle)
+constexpr int S_STAGES = 2;
+__host__ __device__ constexpr int staged_stage_bytes(int s) { return s * (TM + TN) * SKB; }
+__host__ __device__ constexpr int staged_smem(int s) { return S_STAGES * staged_stage_bytes(s) + 1024 + 256; }
+
+__device__ __forceinline__ uint64_t smem_desc64(const void* tile, int k_bytes) {
+  const uint32_t addr = smem_u32(tile) + static_cast<uint32_t>(k_bytes);
+  return static_cast<uint64_t>((addr & 0x3FFFFu) >> 4) | (1ull << 16) | (static_cast<uint64_t>(512u >> 4) << 32) |
+         (1ull << 46) | (4ull << 61);
+}
+
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+    ozaki_staged_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                        const int* __restrict__ ea, const int* __restrict__ eb, double* __restrict__ C,
+                        long ldc, int M, int N, int K, int s) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int SB = staged_stage_bytes(s);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S_STAGES * SB);
+  uint64_t* empty = full + S_STAGES;
+  uint64_t* tfull = empty + S_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  const int nk = (K + SKB - 1) / SKB;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {  // TMEM: one 64-column int32 accumulator per digit weight
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer: all digits of A and B for chunk kc
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kc = 0; kc < nk; ++kc) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        unsigned char* st = smem + stage * SB;
+        mbar_expect_tx(&full[stage], SB);
+        for (int p = 0; p < s; ++p) {
+          tma_load_3d(st + p * TM * SKB, &mapA, &full[stage], kc * SKB, m0, p);
+          tma_load_3d(st + s * TM * SKB + p * TN * SKB, &mapB, &full[stage], kc * SKB, n0, p);
+        }
+        if (++stage == S_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer: pairs (p, q), p + q <= s + 1, into accumulator w - 2
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kc = 0; kc < nk; ++kc) {
+        mbar_wait(&full[stage], phase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const unsigned char* st = smem + stage * SB;
+        for (int w = 2; w <= s + 1; ++w) {
+          const uint32_t d = tmem + static_cast<uint32_t>((w - 2) * TN);
+          for (int p = max(1, w - s); p <= min(s, w - 1); ++p) {
+            const int q = w - p;
+            const unsigned char* ta = st + (p - 1) * TM * SKB;
+            const unsigned char* tb = st + s * TM * SKB + (q - 1) * TN * SKB;
+#pragma unroll
+            for (int kk = 0; kk < SKB / UMMA_K; ++kk) {
+              const bool first = kc == 0 && p == max(1, w - s) && kk == 0;
+              mma_i8(d, smem_desc64(ta, kk * UMMA_K), smem_desc64(tb, kk * UMMA_K), first ? 0u : 1u);
+            }
+          }
+        }
+        umma_commit(&empty[stage]);
+        if (++stage == S_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      umma_commit(tfull);
+    }
+  } else {
+    const int lg = warp & 3;
+    const int row = m0 + 32 * lg + lane;
+    double c[TN];
+#pragma unroll
+    for (int j = 0; j < TN; ++j) c[j] = 0.0;
+    mbar_wait(tfull, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    for (int w = s + 1; w >= 2; --w) {  // smallest weight first
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * lg) << 16) + static_cast<uint32_t>((w - 2) * TN);
+      uint32_t v[TN];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,"
+          "%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63},"
+          " [%64];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+            "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+            "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+            "=r"(v[29]), "=r"(v[30]), "=r"(v[31]), "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]),
+            "=r"(v[36]), "=r"(v[37]), "=r"(v[38]), "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]),
+            "=r"(v[43]), "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]),
+            "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]),
+            "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const double f = ldexp(1.0, -7 * w);
+#pragma unroll
+      for (int j = 0; j < TN; ++j) c[j] = fma(static_cast<double>(static_cast<int32_t>(v[j])), f, c[j]);
+    }
+    if (row < M) {
+      const int er = ea[row];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int col = n0 + j;
+        if (col < N) C[static_cast<long>(row) * ldc + col] = ldexp(c[j], er + eb[col]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+}
+
 // Digits of the rows of X (R x K): row r = X[r][k] (ld, !trans) or X[k][r] (trans).
 // ex[r]: 2^ex[r] > max_k |x|; D[p][r][k] (int8, row stride Kp) for p < s.
 __global__ void rowexp_kernel(const double* __restrict__ X, long ld, int R, int K, int trans,
@@ -310,14 +453,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // int8 digit planes [s][rows][Kp] as a 3-D tensor (K bytes, rows, plane), box TKB x box_rows x 1
-CUtensorMap digit_map(const int8_t* base, int rows, int Kp, int s, int box_rows) {
+CUtensorMap digit_map(const int8_t* base, int rows, int Kp, int s, int box_rows, int box_k = TKB,
+                      CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(s)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(Kp) * rows};
-  cuuint32_t box[3] = {static_cast<cuuint32_t>(TKB), static_cast<cuuint32_t>(box_rows), 1u};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(box_k), static_cast<cuuint32_t>(box_rows), 1u};
   cuuint32_t estr[3] = {1u, 1u, 1u};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box,
-                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(ACHI_E_CUDA, "cuTensorMapEncodeTiled (digits) failed: " + std::to_string(r));
   return m;
@@ -347,6 +491,23 @@ void dgemm_ozaki(Ctx& ctx, int M, int N, int K, const double* A, long lda, bool 
   digits_kernel<<<dim3(cdiv(Kp, 32), cdiv(N, 32)), dim3(32, 8), 0, ctx.stream>>>(B, ldb, N, K, Kp,
                                                                                    b_kmajor ? 0 : 1, slices, eb, DB);
   ACHI_LAUNCHED(ctx);
+  static const int staged_env = [] {  // ACHI_OZAKI_STAGED=0: the pair-streaming kernel
+    const char* e = std::getenv("ACHI_OZAKI_STAGED");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (staged_env && slices <= 8) {
+    per_device_once("ozaki_staged_kernel", ctx.device, [] {
+      ACHI_CUDA(cudaFuncSetAttribute(ozaki_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     staged_smem(8)));
+      return 1;
+    });
+    const CUtensorMap ma = digit_map(DA, M, Kp, slices, TM, SKB, CU_TENSOR_MAP_SWIZZLE_64B);
+    const CUtensorMap mb = digit_map(DB, N, Kp, slices, TN, SKB, CU_TENSOR_MAP_SWIZZLE_64B);
+    ozaki_staged_kernel<<<dim3(cdiv(N, TN), cdiv(M, TM)), OZ_THREADS, staged_smem(slices), ctx.stream>>>(
+        ma, mb, ea, eb, C, ldc, M, N, Kp, slices);
+    ACHI_LAUNCHED(ctx);
+    return;
+  }
   per_device_once("ozaki_gemm_kernel", ctx.device, [] {
     ACHI_CUDA(cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM));
     return 1;
