@@ -104,7 +104,18 @@ constexpr int HS_JRB = 16;  // jr per phase-A tile (d = 2)
 // The GEMM tile is staged in shared memory and mixed there (no X buffer).
 template <int KM>
 __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const double* theta,
-                                        double* As, double* Bs, int blk, int nblk) {
+                                        double* As, double* Bs, int blk, int nblk,
+                                        unsigned long long* prof = nullptr) {
+  // prof (optional, thread 0 of the caller's CTA): cycles in [0] loads, [1] MMA, [2] mixing
+  const bool pf = prof && threadIdx.x == 0;
+  unsigned long long pt = pf ? clock64() : 0;
+  auto pmark = [&](int i) {
+    if (pf) {
+      const unsigned long long n = clock64();
+      prof[i] += n - pt;
+      pt = n;
+    }
+  };
   constexpr int HS_LD = hs_ld<KM>(), RG = HS_THREADS / KM;  // row groups of the K-major loads
   const int t = threadIdx.x;
   const int chl = a.chl, chr = a.chr, dd = a.d * a.d, D1 = a.D1, D3 = a.D3;
@@ -152,9 +163,11 @@ __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const
       }
     }
     __syncthreads();
+    pmark(0);
     double acc[2][4];
     tile_mma<KM>(As, Bs, chl, acc);
     __syncthreads();
+    pmark(1);
     // stage the 32 x 64 tile (rows (bl, a), cols (s, q)) into As, then mix
     tile_store(acc, As, HS_LD, 0, 0, HS_TM, HS_TN);
     __syncthreads();
@@ -173,6 +186,7 @@ __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const
       }
       a.X[((static_cast<long>(bl) * dd + sp) * D3 + e) * chr + jr] = v;  // Y[(bl s') (e jr)]
     }
+    pmark(2);
   }
 }
 

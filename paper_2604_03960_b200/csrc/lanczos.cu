@@ -1109,7 +1109,7 @@ __global__ void __launch_bounds__(PZ_THREADS) lanczos_persistent_kernel(PzArgs a
           t0 = t1;
         }
       };
-      hs::phase_a<hs::HS_KMAX>(h, mw, a.Q + j * a.stride, As, Bs, rank, a.W);
+      hs::phase_a<hs::HS_KMAX>(h, mw, a.Q + j * a.stride, As, Bs, rank, a.W, pf ? a.prof + 12 : nullptr);
       mark(0);
       pz_sync(a, gen);
       mark(1);
@@ -1611,9 +1611,10 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
       const double st = ph.p[11] ? static_cast<double>(ph.p[11]) : 1.0;
       std::fprintf(stderr,
                    "[lanczos-persist] W=%d steps=%llu cycles/step: A %.0f bar %.0f B %.0f bar %.0f C+dots %.0f "
-                   "bar %.0f proj+dots %.0f bar %.0f proj+q %.0f bar %.0f wait %.0f\n",
+                   "bar %.0f proj+dots %.0f bar %.0f proj+q %.0f bar %.0f wait %.0f | A: loads %.0f mma %.0f mix %.0f\n",
                    W, ph.p[11], ph.p[0] / st, ph.p[1] / st, ph.p[2] / st, ph.p[3] / st, ph.p[4] / st,
-                   ph.p[5] / st, ph.p[6] / st, ph.p[7] / st, ph.p[8] / st, ph.p[9] / st, ph.p[10] / st);
+                   ph.p[5] / st, ph.p[6] / st, ph.p[7] / st, ph.p[8] / st, ph.p[9] / st, ph.p[10] / st,
+                   ph.p[12] / st, ph.p[13] / st, ph.p[14] / st);
     }
     void* kargs[] = {&pa};
     ACHI_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lanczos_persistent_kernel), dim3(W + 1),
