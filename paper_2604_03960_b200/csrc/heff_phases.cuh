@@ -80,10 +80,14 @@ __device__ __forceinline__ void tile_store(const double (&acc)[2][4], double* C,
 }
 
 
-// Mixing coefficients of the bond (CSR) staged once per CTA.
+// Mixing coefficients of the bond (CSR) staged once per CTA, plus a dense
+// copy (HS_MIXD x HS_MIXD, zero-filled) for the register-blocked mixing of
+// phase A when nout, nin <= HS_MIXD (every XXZ bulk bond: D = 5, d = 2 -> 20 x 20).
+constexpr int HS_MIXD = 20;
 struct MixSmem {
   double wv[HS_MAXNNZ];
   int wc[HS_MAXNNZ], wr[HS_MAXW + 1];
+  double wd[HS_MIXD * HS_MIXD];  // wd[j * HS_MIXD + i]
 };
 __device__ __forceinline__ void load_mix(const DevMix& m, MixSmem& w) {
   for (int i = threadIdx.x; i < m.nnz; i += blockDim.x) {
@@ -91,6 +95,11 @@ __device__ __forceinline__ void load_mix(const DevMix& m, MixSmem& w) {
     w.wc[i] = m.col[i];
   }
   for (int i = threadIdx.x; i <= m.nout; i += blockDim.x) w.wr[i] = m.rowptr[i];
+  for (int i = threadIdx.x; i < HS_MIXD * HS_MIXD; i += blockDim.x) w.wd[i] = 0.0;
+  __syncthreads();
+  if (m.nout <= HS_MIXD && m.nin <= HS_MIXD)
+    for (int j = threadIdx.x; j < m.nout; j += blockDim.x)
+      for (int p = m.rowptr[j]; p < m.rowptr[j + 1]; ++p) w.wd[j * HS_MIXD + m.col[p]] = m.val[p];
 }
 
 // Tile shape of phase A: rows = a block of `blb` left indices bl with all D1
@@ -171,6 +180,35 @@ __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const
     // stage the 32 x 64 tile (rows (bl, a), cols (s, q)) into As, then mix
     tile_store(acc, As, HS_LD, 0, 0, HS_TM, HS_TN);
     __syncthreads();
+    if (dd * D3 <= HS_MIXD && D1 * dd <= HS_MIXD) {
+      // register-blocked mixing: thread (bll, q, half) loads the D1 dd inputs of its
+      // column once and forms half of the dd D3 outputs as dense dot products with
+      // the broadcast W12 rows (no per-term index chains)
+      const int nin = D1 * dd, njo = dd * D3, pairs = blb * HS_JRB;
+      for (int u = t; u < 2 * pairs; u += HS_THREADS) {
+        const int pr = u % pairs, half = u / pairs;
+        const int bll = pr / HS_JRB, q = pr % HS_JRB;
+        const int bl = bl0 + bll, jr = jr0 + q;
+        if (bl >= chl || jr >= chr) continue;
+        double x[HS_MIXD];
+#pragma unroll
+        for (int i = 0; i < HS_MIXD; ++i) {
+          const int aa = i / dd, ss = i - aa * dd;
+          x[i] = i < nin ? As[(bll * D1 + aa) * HS_LD + ss * HS_JRB + q] : 0.0;
+        }
+        const int j0 = half ? (njo + 1) / 2 : 0, j1 = half ? njo : (njo + 1) / 2;
+        double* yrow = a.X + (static_cast<long>(bl) * njo) * chr + jr;  // Y[(bl s') (e jr)], j = s' D3 + e
+        for (int j = j0; j < j1; ++j) {
+          const double* wj = w.wd + j * HS_MIXD;
+          double v = 0.0;
+#pragma unroll
+          for (int i = 0; i < HS_MIXD; ++i) v = fma(wj[i], x[i], v);
+          yrow[static_cast<long>(j) * chr] = v;
+        }
+      }
+      pmark(2);
+      continue;
+    }
     const int nout = blb * dd * D3 * HS_JRB;  // outputs (bl, s', e, q)
     for (int o = t; o < nout; o += HS_THREADS) {
       const int q = o % HS_JRB, rest = o / HS_JRB;
