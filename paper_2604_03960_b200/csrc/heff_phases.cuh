@@ -112,9 +112,13 @@ constexpr int HS_JRB = 16;  // jr per phase-A tile (d = 2)
 // A: Y[((bl,s'),e), jr] = sum_{(a,s)} W12[(s',e),(a,s)] sum_jl L[(bl,a),jl] theta[jl,(s,jr)]
 // The GEMM tile is staged in shared memory and mixed there (no X buffer).
 template <int KM>
+// Lc (optional, persistent callers): a shared-memory cache of the L tile of the
+// CTA's first item, filled when lfill (the first matvec of an eigensolve) and
+// read instead of global memory afterwards (L is constant within an eigensolve)
 __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const double* theta,
                                         double* As, double* Bs, int blk, int nblk,
-                                        unsigned long long* prof = nullptr) {
+                                        unsigned long long* prof = nullptr, double* Lc = nullptr,
+                                        bool lfill = false) {
   // prof (optional, thread 0 of the caller's CTA): cycles in [0] loads, [1] MMA, [2] mixing
   const bool pf = prof && threadIdx.x == 0;
   unsigned long long pt = pf ? clock64() : 0;
@@ -134,8 +138,10 @@ __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const
   for (int item = blk; item < tm * tn; item += nblk) {
     const int bl0 = (item / tn) * blb, jr0 = (item % tn) * HS_JRB;
     __syncthreads();
-    {
-      // As[m][k] = L[bl0*D1 + m][k] (m < blb*D1): thread -> (k = t % KM, rows t / KM + RG u);
+    const bool cached = Lc && item == blk;
+    double* At = cached ? Lc : As;  // A operand of this item's GEMM
+    if (!cached || lfill) {
+      // At[m][k] = L[bl0*D1 + m][k] (m < blb*D1): thread -> (k = t % KM, rows t / KM + RG u);
       // every load of a thread is issued before its stores
       const int k = t % KM, r0 = t / KM;
       double v[HS_TM / RG];
@@ -148,7 +154,7 @@ __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const
       }
       if (k < K4)
 #pragma unroll
-        for (int u = 0; u < HS_TM / RG; ++u) As[(r0 + RG * u) * HS_LD + k] = v[u];
+        for (int u = 0; u < HS_TM / RG; ++u) At[(r0 + RG * u) * HS_LD + k] = v[u];
     }
     {
       // Bs[n][k] = theta[k][s*chr + jr0 + q], n = s*16 + q: thread -> (n = t % 64, k = t / 64 + 4u),
@@ -174,7 +180,7 @@ __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const
     __syncthreads();
     pmark(0);
     double acc[2][4];
-    tile_mma<KM>(As, Bs, chl, acc);
+    tile_mma<KM>(At, Bs, chl, acc);
     __syncthreads();
     pmark(1);
     // stage the 32 x 64 tile (rows (bl, a), cols (s, q)) into As, then mix
@@ -229,8 +235,10 @@ __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const
 }
 
 // B: P_e[(bl,s'), br] = sum_jr Y[(bl,s'),(e,jr)] R[br,(e,jr)]  (one item per e: split-K)
+// Rc (optional): shared-memory cache of the R tile of the CTA's first item, as Lc
 template <int KM>
-__device__ __forceinline__ void phase_b(const HsArgs& a, double* As, double* Bs, int blk, int nblk) {
+__device__ __forceinline__ void phase_b(const HsArgs& a, double* As, double* Bs, int blk, int nblk,
+                                        double* Rc = nullptr, bool rfill = false) {
   constexpr int HS_LD = hs_ld<KM>(), RG = HS_THREADS / KM;
   const int t = threadIdx.x;
   const int chl = a.chl, chr = a.chr, dd = a.d * a.d, D3 = a.D3;
@@ -255,8 +263,10 @@ __device__ __forceinline__ void phase_b(const HsArgs& a, double* As, double* Bs,
 #pragma unroll
         for (int u = 0; u < HS_TM / RG; ++u) As[(r0 + RG * u) * HS_LD + jr] = v[u];
     }
-    {
-      // Bs[n][jr] = R[n0+n][e][jr]: thread -> (jr = t % KM, n = t / KM + RG u), chunks of 32
+    const bool cached = Rc && item == blk;
+    double* Bt = cached ? Rc : Bs;  // B operand of this item's GEMM
+    if (!cached || rfill) {
+      // Bt[n][jr] = R[n0+n][e][jr]: thread -> (jr = t % KM, n = t / KM + RG u), chunks of 32
       const int jr = t % KM, q0 = t / KM;
 #pragma unroll
       for (int h = 0; h < HS_TN / RG / 32; ++h) {
@@ -268,12 +278,12 @@ __device__ __forceinline__ void phase_b(const HsArgs& a, double* As, double* Bs,
         }
         if (jr < K4)
 #pragma unroll
-          for (int u = 0; u < 32; ++u) Bs[(q0 + RG * (32 * h + u)) * HS_LD + jr] = v[u];
+          for (int u = 0; u < 32; ++u) Bt[(q0 + RG * (32 * h + u)) * HS_LD + jr] = v[u];
       }
     }
     __syncthreads();
     double acc[2][4];
-    tile_mma<KM>(As, Bs, chr, acc);
+    tile_mma<KM>(As, Bt, chr, acc);
     tile_store(acc, a.part + static_cast<long>(e) * M2 * N2, N2, m0, n0, M2, N2);
   }
 }

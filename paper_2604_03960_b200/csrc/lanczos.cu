@@ -937,10 +937,10 @@ __device__ void pz_dots(const PzArgs& a, int nv, long b0, long b1, int rank, dou
 // a barrier after each; the caller folds phase C (sum over e) into its next
 // elementwise pass via pz_w().
 __device__ void pz_matvec(const PzArgs& a, hs::HsArgs& h, const hs::MixSmem& mw, const double* theta,
-                          double* As, double* Bs, int rank, unsigned& gen) {
-  hs::phase_a<hs::HS_KMAX>(h, mw, theta, As, Bs, rank, a.W);
+                          double* As, double* Bs, int rank, unsigned& gen, double* Lc, double* Rc) {
+  hs::phase_a<hs::HS_KMAX>(h, mw, theta, As, Bs, rank, a.W, nullptr, Lc, false);
   pz_sync(a, gen);
-  hs::phase_b<hs::HS_KMAX>(h, As, Bs, rank, a.W);
+  hs::phase_b<hs::HS_KMAX>(h, As, Bs, rank, a.W, Rc, false);
   pz_sync(a, gen);
 }
 __device__ __forceinline__ double pz_w(const hs::HsArgs& h, long tot, long x) {
@@ -1031,6 +1031,10 @@ __global__ void __launch_bounds__(PZ_THREADS) lanczos_persistent_kernel(PzArgs a
   }
   double* As = reinterpret_cast<double*>(dyn);
   double* Bs = As + hs::HS_TM * hs::hs_ld<hs::HS_KMAX>();
+  // L and R tiles of this worker's first items, kept for the whole eigensolve
+  double* Lc = Bs + hs::HS_TN * hs::hs_ld<hs::HS_KMAX>();
+  double* Rc = Lc + hs::HS_TM * hs::hs_ld<hs::HS_KMAX>();
+  bool cfill = true;
   hs::load_mix(a.h.mix, mw);
   hs::HsArgs h = a.h;
   const long n = a.n, tot = n;
@@ -1109,11 +1113,13 @@ __global__ void __launch_bounds__(PZ_THREADS) lanczos_persistent_kernel(PzArgs a
           t0 = t1;
         }
       };
-      hs::phase_a<hs::HS_KMAX>(h, mw, a.Q + j * a.stride, As, Bs, rank, a.W, pf ? a.prof + 12 : nullptr);
+      hs::phase_a<hs::HS_KMAX>(h, mw, a.Q + j * a.stride, As, Bs, rank, a.W, pf ? a.prof + 12 : nullptr, Lc,
+                               cfill);
       mark(0);
       pz_sync(a, gen);
       mark(1);
-      hs::phase_b<hs::HS_KMAX>(h, As, Bs, rank, a.W);
+      hs::phase_b<hs::HS_KMAX>(h, As, Bs, rank, a.W, Rc, cfill);
+      cfill = false;
       mark(2);
       pz_sync(a, gen);
       mark(3);
@@ -1216,7 +1222,7 @@ __global__ void __launch_bounds__(PZ_THREADS) lanczos_persistent_kernel(PzArgs a
       pz_sync(a, gen);
     }
     // ---- explicit residual (linalg.cpp:156-162): w = H r, ev = r.w, ||w - ev r|| ----
-    pz_matvec(a, h, mw, a.ritz, As, Bs, rank, gen);
+    pz_matvec(a, h, mw, a.ritz, As, Bs, rank, gen, Lc, Rc);
     ++matvecs;
     {
       double v = 0.0;
@@ -1576,7 +1582,7 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
   hs::HsArgs pz_h{};
   long pz_items = 0;
   if (persist_on && small_op && heff_small_fusable(ctx, *small_op, ws.qcur.p, ws.w.p, &pz_h, &pz_items)) {
-    const size_t smem = hs::smem_bytes<hs::HS_KMAX>();
+    const size_t smem = 2 * hs::smem_bytes<hs::HS_KMAX>();  // As, Bs + the L / R tile caches
     const int maxres = per_device_once("lanczos_persistent_kernel", ctx.device, [&] {
       ACHI_CUDA(cudaFuncSetAttribute(lanczos_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
