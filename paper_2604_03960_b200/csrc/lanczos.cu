@@ -933,6 +933,63 @@ __device__ void pz_dots(const PzArgs& a, int nv, long b0, long b1, int rank, dou
   __syncthreads();
 }
 
+// One pass over the worker's chunk for nv <= PZ_FUSE basis vectors, every Q
+// value loaded once and held in registers: the vector is either formed from
+// the matvec partials (first = true: w = sum_e P_e, phase C) or projected
+// (w <- w - Q coef, ||w'||^2 -> part[nv][rank]); then the partial dots
+// Q^T w -> part[v][rank].  Same per-element operation order as pz_w /
+// project_out + pz_dots.
+constexpr int PZ_FUSE = 16;
+__device__ __forceinline__ double pz_w(const hs::HsArgs& h, long tot, long x) {
+  double v = 0.0;
+  for (int e = 0; e < h.D3; ++e) v += h.part[e * tot + x];
+  return v;
+}
+__device__ void pz_fused_pass(const PzArgs& a, const hs::HsArgs& h, long tot, int nv, bool first,
+                              const double* coef, long b0, long b1, int rank, double* part,
+                              double (*sh)[65], double* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double acc[PZ_FUSE];
+#pragma unroll
+  for (int i = 0; i < PZ_FUSE; ++i) acc[i] = 0.0;
+  double nrm = 0.0;
+  for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) {
+    double q[PZ_FUSE];
+#pragma unroll
+    for (int i = 0; i < PZ_FUSE; ++i) q[i] = i < nv ? a.Q[i * a.stride + x] : 0.0;
+    double v;
+    if (first) {
+      v = pz_w(h, tot, x);
+    } else {
+      v = a.w[x];
+#pragma unroll
+      for (int i = 0; i < PZ_FUSE; ++i)
+        if (i < nv) v -= coef[i] * q[i];
+      nrm += v * v;
+    }
+    a.w[x] = v;
+#pragma unroll
+    for (int i = 0; i < PZ_FUSE; ++i) acc[i] += q[i] * v;
+  }
+#pragma unroll
+  for (int i = 0; i < PZ_FUSE; ++i) {
+    const double r = warp_sum(acc[i]);
+    if (lane == 0 && i < nv) sh[warp][i] = r;
+  }
+  if (!first) {
+    nrm = block_sum(nrm, red);  // (block_sum synchronises the CTA)
+    if (threadIdx.x == 0) part[static_cast<long>(nv) * a.W + rank] = nrm;
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < nv; v += PZ_THREADS) {
+    double t = 0.0;
+#pragma unroll
+    for (int w8 = 0; w8 < PZ_THREADS / 32; ++w8) t += sh[w8][v];
+    part[static_cast<long>(v) * a.W + rank] = t;
+  }
+  __syncthreads();
+}
+
 // matvec w = H theta over the workers: phases A and B of heff_phases.cuh with
 // a barrier after each; the caller folds phase C (sum over e) into its next
 // elementwise pass via pz_w().
@@ -942,11 +999,6 @@ __device__ void pz_matvec(const PzArgs& a, hs::HsArgs& h, const hs::MixSmem& mw,
   pz_sync(a, gen);
   hs::phase_b<hs::HS_KMAX>(h, As, Bs, rank, a.W, Rc, false);
   pz_sync(a, gen);
-}
-__device__ __forceinline__ double pz_w(const hs::HsArgs& h, long tot, long x) {
-  double v = 0.0;
-  for (int e = 0; e < h.D3; ++e) v += h.part[e * tot + x];
-  return v;
 }
 
 // the tridiagonal CTA: one job per step (j, matvecs before the cycle); the
@@ -1124,24 +1176,32 @@ __global__ void __launch_bounds__(PZ_THREADS) lanczos_persistent_kernel(PzArgs a
       pz_sync(a, gen);
       mark(3);
       const int nv = j + 1;
-      for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) a.w[x] = pz_w(h, tot, x);
-      // (each thread reads back only the w[x] it wrote)
-      pz_dots(a, nv, b0, b1, rank, a.pa, false, sh);
+      if (nv <= PZ_FUSE) {
+        pz_fused_pass(a, h, tot, nv, true, coef, b0, b1, rank, a.pa, sh, red);
+      } else {
+        for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) a.w[x] = pz_w(h, tot, x);
+        // (each thread reads back only the w[x] it wrote)
+        pz_dots(a, nv, b0, b1, rank, a.pa, false, sh);
+      }
       mark(4);
       pz_sync(a, gen);
       mark(5);
       pz_reduce(a.pa, nv, a.W, coef);
       const double alpha_j = coef[nv - 1];
-      double nrm1 = 0.0;
-      for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) {
-        const double v = project_out(a.Q, a.stride, nv, coef, a.w[x], x);
-        a.w[x] = v;
-        nrm1 += v * v;
+      if (nv <= PZ_FUSE) {
+        pz_fused_pass(a, h, tot, nv, false, coef, b0, b1, rank, a.pb, sh, red);
+      } else {
+        double nrm1 = 0.0;
+        for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) {
+          const double v = project_out(a.Q, a.stride, nv, coef, a.w[x], x);
+          a.w[x] = v;
+          nrm1 += v * v;
+        }
+        nrm1 = block_sum(nrm1, red);
+        if (threadIdx.x == 0) a.pb[static_cast<long>(nv) * a.W + rank] = nrm1;
+        __syncthreads();
+        pz_dots(a, nv, b0, b1, rank, a.pb, false, sh);
       }
-      nrm1 = block_sum(nrm1, red);
-      if (threadIdx.x == 0) a.pb[static_cast<long>(nv) * a.W + rank] = nrm1;
-      __syncthreads();
-      pz_dots(a, nv, b0, b1, rank, a.pb, false, sh);
       mark(6);
       pz_sync(a, gen);
       mark(7);
