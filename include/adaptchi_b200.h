@@ -16,10 +16,13 @@
  *    by a chain handle.  One context = one device + one CUDA stream; a context
  *    is used by one host thread at a time ("a DMRG run is
  *    strictly sequential; multiple runs may execute concurrently").
- *  - Arithmetic is real FP64.  The reference stores complex128
+ *  - Arithmetic is real FP64 by default.  The reference stores complex128
  *    (tensor.hpp:14-17); for the XXZ/Heisenberg family with the Neel start all
  *    state data are real once the MPO's sigma^y channel is written in the real
  *    gauge (iY, -jy*iY): the dense Hamiltonian is identical.
+ *    A chain with complex states (the complex random_mps start) runs in
+ *    complex128 (achi_dmrg_config.arithmetic); its sites are read and loaded
+ *    through the *_complex entry points as interleaved (re, im) pairs.
  *  - Tensor layouts are the reference's row-major layouts: site tensors
  *    (left, phys, right) (mps.hpp:28-29), environment blocks (bra, mpo, ket)
  *    (dmrg.hpp:38-39), MPO tensors (left, phys_out, phys_in, right)
@@ -60,13 +63,20 @@ enum { ACHI_MODE_FIXED = 0, ACHI_MODE_THRESHOLD = 1, ACHI_MODE_DIRECT = 2, ACHI_
 enum { ACHI_PREDICT_OFF = 0, ACHI_PREDICT_LINEAR = 1, ACHI_PREDICT_QUADRATIC = 2 };
 enum { ACHI_PID_ADDITIVE = 0, ACHI_PID_MULTIPLICATIVE = 1 };
 /* Initial state (dmrg.cpp:222-235).  ACHI_INIT_RANDOM is the reference's complex
- * random_mps (mps.cpp:75-95) and is rejected by the real FP64 path.
+ * random_mps (mps.cpp:75-95); it runs the chain in complex arithmetic.
  * ACHI_INIT_RANDOM_REAL draws the same mt19937_64(seed) normal sequence, one
  * real value per entry, on capped_bond_dims(n, 2, chi_min) (mps.cpp:60-73),
  * then canonicalize(psi, 0) and normalise as random_mps does.  On the real path
  * ACHI_INIT_AUTOMATIC resolves to RANDOM_REAL for the transverse-field Ising
  * family (its Hamiltonian is real, so its ground state is real). */
 enum { ACHI_INIT_AUTOMATIC = 0, ACHI_INIT_NEEL = 1, ACHI_INIT_RANDOM = 2, ACHI_INIT_RANDOM_REAL = 3 };
+/* Arithmetic of a chain.  ACHI_ARITH_REAL (default): real FP64 sites and
+ * environments with the real-gauge MPO.  ACHI_ARITH_COMPLEX: complex128 sites
+ * and environments as the reference stores them (tensor.hpp:14-21), computed
+ * as 4M real DMMA contractions on planar [Re; Im] storage; AUTOMATIC then
+ * resolves as the reference does (TFIM -> the complex random_mps start,
+ * dmrg.cpp:222-235).  ACHI_INIT_RANDOM selects complex arithmetic by itself. */
+enum { ACHI_ARITH_REAL = 0, ACHI_ARITH_COMPLEX = 1 };
 
 typedef struct achi_model_spec {
   int32_t family;      /* ACHI_HEISENBERG_XXZ | ACHI_TRANSVERSE_ISING */
@@ -97,7 +107,7 @@ typedef struct achi_dmrg_config {
   double eps_conv;          /* 1e-8 */
   double eig_tol;           /* 1e-10 */
   int32_t initial_state;    /* ACHI_INIT_* */
-  int32_t _pad;
+  int32_t arithmetic;       /* ACHI_ARITH_* (0 = real) */
   uint64_t seed;            /* 1234 */
   double noise_floor;       /* 1e-14 */
   achi_controller_config controller;
@@ -226,6 +236,16 @@ int achi_chain_load_state(achi_chain* chain, const int32_t* bond_dims,
  * Replaces load_mps + canonicalize + Environment::rebuild for a resumed run. */
 int achi_chain_load_mps(achi_chain* chain, const int32_t* bond_dims, const double* const* sites,
                         int canonicalize);
+/* 1 when the chain runs in complex128 (ACHI_ARITH_COMPLEX or a complex start) */
+int achi_chain_is_complex(const achi_chain* chain);
+/* copy complex site tensor k (row-major (l,d,r), interleaved re/im: 2*l*d*r
+ * doubles) of a complex chain (MatrixProductState::site, mps.hpp:28-29) */
+int achi_chain_get_site_complex(const achi_chain* chain, int k, double* out, size_t capacity);
+/* achi_chain_load_mps for a complex chain: sites interleaved re/im (mps.cpp:276-315
+ * snapshots, resumed runs); canonicalize != 0 runs canonicalize(psi, 0) on the
+ * device (complex SVD push_left) */
+int achi_chain_load_mps_complex(achi_chain* chain, const int32_t* bond_dims,
+                                const double* const* sites, int canonicalize);
 /* expectation_energy (dmrg.cpp:284-298) of the chain's current state on the
  * device: left environments rebuilt from the boundary through every site
  * (independent of the cached environments); <psi|H|psi> (psi is normalised

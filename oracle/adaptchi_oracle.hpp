@@ -603,8 +603,12 @@ inline MPS<cd> random_mps(int n, int d, int chi, uint64_t seed) {
     long r = i == n - 1 ? 1 : dims[i];
     Tensor<cd> t({l, d, r});
     for (long k = 0; k < t.size(); ++k) {
-      double re = gauss(rng);
+      // mps.cpp:86 writes Cplx(gauss(rng), gauss(rng)); the order of the two
+      // draws is unspecified in C++ and g++ (the reference's toolchain)
+      // evaluates constructor arguments right to left: the imaginary part is
+      // the first draw (checked with g++ here)
       double im = gauss(rng);
+      double re = gauss(rng);
       t.data[k] = cd(re, im);
     }
     psi.sites.push_back(std::move(t));

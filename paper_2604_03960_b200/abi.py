@@ -19,6 +19,7 @@ MODE_FIXED, MODE_THRESHOLD, MODE_DIRECT, MODE_PID = 0, 1, 2, 3
 PREDICT_OFF, PREDICT_LINEAR, PREDICT_QUADRATIC = 0, 1, 2
 PID_ADDITIVE, PID_MULTIPLICATIVE = 0, 1
 INIT_AUTOMATIC, INIT_NEEL, INIT_RANDOM, INIT_RANDOM_REAL = 0, 1, 2, 3
+ARITH_REAL, ARITH_COMPLEX = 0, 1
 
 ERROR_NAMES = {
     1: "Error", 2: "InvalidMatrix", 3: "NumericalFailure", 4: "InvalidRank",
@@ -51,7 +52,7 @@ class ControllerConfig(C.Structure):
 class DmrgConfig(C.Structure):
     _fields_ = [("max_sweeps", C.c_int32), ("eig_max_iter", C.c_int32),
                 ("eps_conv", C.c_double), ("eig_tol", C.c_double),
-                ("initial_state", C.c_int32), ("_pad", C.c_int32),
+                ("initial_state", C.c_int32), ("arithmetic", C.c_int32),
                 ("seed", C.c_uint64), ("noise_floor", C.c_double),
                 ("controller", ControllerConfig)]
 
@@ -168,6 +169,9 @@ def load():
         "achi_chain_load_state": (C.c_int, [vp, P(i32), P(dp)]),
         "achi_chain_load_mps": (C.c_int, [vp, P(i32), P(dp), C.c_int]),
         "achi_chain_energy": (C.c_int, [vp, dp]),
+        "achi_chain_is_complex": (C.c_int, [vp]),
+        "achi_chain_get_site_complex": (C.c_int, [vp, C.c_int, dp, C.c_size_t]),
+        "achi_chain_load_mps_complex": (C.c_int, [vp, P(i32), P(dp), C.c_int]),
         "achi_heff_apply": (C.c_int, [vp] + [C.c_int] * 6 + [dp] * 6),
         "achi_env_update_left": (C.c_int, [vp] + [C.c_int] * 5 + [dp] * 4),
         "achi_env_update_right": (C.c_int, [vp] + [C.c_int] * 5 + [dp] * 4),

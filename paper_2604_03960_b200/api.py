@@ -372,8 +372,19 @@ class Chain:
         self.ctx.lib.achi_chain_bond_dims(self.h, _ip(d))
         return d
 
+    @property
+    def is_complex(self):
+        """True when the chain runs in complex128 (ARITH_COMPLEX or the complex random start)."""
+        return bool(self.ctx.lib.achi_chain_is_complex(self.h))
+
     def site(self, k):
+        """Site tensor k as a host (l, d, r) array (complex128 on a complex chain)."""
         dims = [1] + list(self.bond_dims()) + [1]
+        if self.is_complex:
+            out = np.zeros((dims[k], 2, dims[k + 1]), np.complex128)
+            self.ctx._check(self.ctx.lib.achi_chain_get_site_complex(
+                self.h, k, out.ctypes.data_as(C.POINTER(C.c_double)), 2 * out.size))
+            return out
         out = np.zeros((dims[k], 2, dims[k + 1]))
         self.ctx._check(self.ctx.lib.achi_chain_get_site(self.h, k, _dp(out), out.size))
         return out
@@ -394,6 +405,13 @@ class Chain:
         """Load site tensors (l, d, r) and rebuild environments at centre 0;
         canonicalize=True first applies canonicalize(psi, 0) (mps.cpp:172-210)."""
         dims = np.array([s.shape[2] for s in sites[:-1]], np.int32)
+        if self.is_complex:
+            flat = [np.ascontiguousarray(s, dtype=np.complex128) for s in sites]
+            ptrs = (C.POINTER(C.c_double) * len(flat))(
+                *[a.ctypes.data_as(C.POINTER(C.c_double)) for a in flat])
+            self.ctx._check(self.ctx.lib.achi_chain_load_mps_complex(self.h, _ip(dims), ptrs,
+                                                                     int(canonicalize)))
+            return
         flat = [np.ascontiguousarray(s, dtype=np.float64) for s in sites]
         ptrs = (C.POINTER(C.c_double) * len(flat))(*[_dp(a) for a in flat])
         self.ctx._check(self.ctx.lib.achi_chain_load_mps(self.h, _ip(dims), ptrs, int(canonicalize)))

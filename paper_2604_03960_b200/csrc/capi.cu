@@ -301,9 +301,55 @@ int achi_chain_get_site(const achi_chain* chain, int k, double* out, size_t capa
   achi_ctx* ctx = ch.owner;
   return guard(ctx, [&] {
     if (k < 0 || k >= ch.n) fail(ACHI_E_INVALID_RANK, "site index out of range");
+    if (ch.cplx) fail(ACHI_E_UNSUPPORTED_MODEL, "complex chain: use achi_chain_get_site_complex");
     const int l = ch.chi[k], r = ch.chi[k + 1];
     if (capacity < static_cast<size_t>(l) * ch.d * r) fail(ACHI_E_SIZE_GUARD, "capacity");
     download_padded3(*ch.ctx, ch.site[k].p, l, ch.d, r, out);
+  });
+}
+
+int achi_chain_is_complex(const achi_chain* chain) { return chain && chain->ch.cplx ? 1 : 0; }
+
+int achi_chain_get_site_complex(const achi_chain* chain, int k, double* out, size_t capacity) {
+  achi_chain* ch_ = const_cast<achi_chain*>(chain);
+  Chain& ch = ch_->ch;
+  return guard(ch.owner, [&] {
+    if (k < 0 || k >= ch.n) fail(ACHI_E_INVALID_RANK, "site index out of range");
+    if (!ch.cplx) fail(ACHI_E_UNSUPPORTED_MODEL, "real chain: use achi_chain_get_site");
+    const int l = ch.chi[k], r = ch.chi[k + 1];
+    if (capacity < 2 * static_cast<size_t>(l) * ch.d * r) fail(ACHI_E_SIZE_GUARD, "capacity");
+    ch.download_site_c(k, out);
+  });
+}
+
+int achi_chain_load_mps_complex(achi_chain* chain, const int32_t* bond_dims, const double* const* sites,
+                                int canonicalize) {
+  Chain& ch = chain->ch;
+  return guard(ch.owner, [&] {
+    if (!ch.cplx) fail(ACHI_E_UNSUPPORTED_MODEL, "real chain: use achi_chain_load_mps");
+    std::vector<int> dims(ch.n + 1, 1);
+    for (int k = 1; k < ch.n; ++k) {
+      if (bond_dims[k - 1] < 1) fail(ACHI_E_INVALID_RANK, "load_mps: bond dimension must be >= 1");
+      dims[k] = bond_dims[k - 1];
+    }
+    std::vector<std::vector<double>> hs(ch.n);
+    for (int k = 0; k < ch.n; ++k) {
+      const size_t sz = 2 * static_cast<size_t>(dims[k]) * ch.d * dims[k + 1];
+      hs[k].assign(sites[k], sites[k] + sz);
+      for (double x : hs[k])
+        if (!std::isfinite(x)) fail(ACHI_E_INVALID_MATRIX, "load_mps: non-finite site entry");
+    }
+    std::vector<DevBuf> ds;
+    if (canonicalize) ds = canonical_on_device_c(*ch.ctx, hs, dims, ch.d);
+    for (int k = 1; k < ch.n; ++k)
+      if (dims[k] > ch.cap[k]) fail(ACHI_E_INVALID_RANK, "load_mps: bond dimension exceeds capacity");
+    for (int k = 1; k < ch.n; ++k) ch.chi[k] = dims[k];
+    if (canonicalize)
+      ch.copy_sites_device_c(ds);
+    else
+      ch.upload_sites_c(hs);
+    ch.rebuild_envs();
+    ch.ctx->sync();
   });
 }
 
@@ -313,6 +359,7 @@ int achi_chain_get_env(const achi_chain* chain, int which, int k, int64_t* shape
   achi_ctx* ctx = ch.owner;
   return guard(ctx, [&] {
     if (k < 0 || k >= ch.n) fail(ACHI_E_INVALID_RANK, "env index out of range");
+    if (ch.cplx) fail(ACHI_E_UNSUPPORTED_MODEL, "complex chain: environments are planar complex");
     const int chi = which == 0 ? ch.chi[k] : ch.chi[k + 1];
     const int D = which == 0 ? ch.mpo[k].l : ch.mpo[k].r;
     shape3[0] = chi;
@@ -350,6 +397,7 @@ int achi_chain_load_mps(achi_chain* chain, const int32_t* bond_dims, const doubl
   Chain& ch = chain->ch;
   achi_ctx* ctx = ch.owner;
   return guard(ctx, [&] {
+    if (ch.cplx) fail(ACHI_E_UNSUPPORTED_MODEL, "complex chain: use achi_chain_load_mps_complex");
     std::vector<int> dims(ch.n + 1, 1);
     for (int k = 1; k < ch.n; ++k) {
       if (bond_dims[k - 1] < 1) fail(ACHI_E_INVALID_RANK, "load_mps: bond dimension must be >= 1");

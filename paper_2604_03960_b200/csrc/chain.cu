@@ -110,6 +110,8 @@ std::vector<std::vector<double>> neel_canonical(int n, int d) {
   return s;
 }
 
+}  // namespace
+
 // capped_bond_dims (mps.cpp:60-73): min(chi, d^k, d^(n-k)) per bond
 std::vector<int> capped_bond_dims(int n, int d, int chi) {
   std::vector<int> dims(n - 1, chi);
@@ -125,6 +127,8 @@ std::vector<int> capped_bond_dims(int n, int d, int chi) {
   }
   return dims;
 }
+
+namespace {
 
 // C (M x N) = A (M x K) * B (K x N), row-major, any shapes (setup-sized
 // products of canonicalisation; 16 x 16 shared-memory tiles, FP64 FMA)
@@ -268,12 +272,17 @@ void Chain::create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g) 
   validate_config(g);
   n = s.n;
   mpo = build_mpo_real(s);
+  if (g.arithmetic != ACHI_ARITH_REAL && g.arithmetic != ACHI_ARITH_COMPLEX)
+    fail(ACHI_E_INVALID_CONFIG, "dmrg: arithmetic must be ACHI_ARITH_REAL or ACHI_ARITH_COMPLEX");
   int init = g.initial_state;
-  if (init == ACHI_INIT_AUTOMATIC)
-    init = s.family == ACHI_HEISENBERG_XXZ ? ACHI_INIT_NEEL : ACHI_INIT_RANDOM_REAL;
-  if (init != ACHI_INIT_NEEL && init != ACHI_INIT_RANDOM_REAL)
-    fail(ACHI_E_UNSUPPORTED_MODEL,
-         "random complex initial state (random_mps, mps.cpp:75-95) is not on the real FP64 path");
+  if (init == ACHI_INIT_AUTOMATIC)  // dmrg.cpp:222-235 (complex: TFIM -> random_mps)
+    init = s.family == ACHI_HEISENBERG_XXZ
+               ? ACHI_INIT_NEEL
+               : (g.arithmetic == ACHI_ARITH_COMPLEX ? ACHI_INIT_RANDOM : ACHI_INIT_RANDOM_REAL);
+  if (init != ACHI_INIT_NEEL && init != ACHI_INIT_RANDOM_REAL && init != ACHI_INIT_RANDOM)
+    fail(ACHI_E_INVALID_CONFIG, "dmrg: unknown initial state");
+  cplx = g.arithmetic == ACHI_ARITH_COMPLEX || init == ACHI_INIT_RANDOM;
+  const size_t planes = cplx ? 2 : 1;
   // mixing matrices
   std::vector<MixMatrix> all;
   for (int b = 0; b + 1 < n; ++b) all.push_back(mix_heff(mpo[b], mpo[b + 1]));
@@ -301,12 +310,17 @@ void Chain::create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g) 
     const char* e = std::getenv("ACHI_SVD_WARM");
     warm_svd = !(e && e[0] == '0');
   }
-  size_t max_vec = 0, max_ws = 0;
+  size_t max_vec = 0, max_ws = 0, max_lhat = 0, max_rhat = 0, max_scr = 0;
   for (int k = 0; k < n; ++k) {
     const size_t cl = pad2i(cap[k]), cr = pad2i(cap[k + 1]);
-    site[k].reserve(cl * d * cr);
-    L[k].reserve(cl * cl * mpo[k].l);
-    R[k].reserve(cr * cr * mpo[k].r);
+    site[k].reserve(planes * cl * d * cr);
+    L[k].reserve(planes * cl * cl * mpo[k].l);
+    R[k].reserve(planes * cr * cr * mpo[k].r);
+    max_lhat = std::max(max_lhat, 4 * cl * cl * mpo[k].l);
+    max_rhat = std::max(max_rhat, 4 * cr * cr * mpo[k].r);
+    // realified operands of the merge / environment updates + a transposed site
+    max_scr = std::max(max_scr, std::max({4 * cl * cl * mpo[k].l, 4 * cr * cr * mpo[k].r, 4 * cl * d * cr}) +
+                                    2 * cl * d * cr);
     ACHI_CUDA(cudaMemsetAsync(L[k].p, 0, sizeof(double) * L[k].cap, c.stream));
     ACHI_CUDA(cudaMemsetAsync(R[k].p, 0, sizeof(double) * R[k].cap, c.stream));
     if (k + 1 < n) {
@@ -316,11 +330,20 @@ void Chain::create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g) 
     }
     max_ws = std::max(max_ws, cl * cr * d * std::max(mpo[k].l, mpo[k].r));
   }
-  theta.reserve(max_vec);
-  vec.reserve(max_vec);
-  c.ws_a.reserve(max_ws);
-  c.ws_b.reserve(max_ws);
-  lz.reserve(static_cast<long>(max_vec));
+  theta.reserve(planes * max_vec);
+  vec.reserve(planes * max_vec);
+  c.ws_a.reserve(planes * max_ws);
+  c.ws_b.reserve(planes * max_ws);
+  lz.reserve(static_cast<long>(planes * max_vec));
+  if (cplx) {
+    lhat.reserve(max_lhat);
+    rhat.reserve(max_rhat);
+    scr.reserve(max_scr);
+    cth.reserve(2 * max_vec);
+    cu.reserve(2 * max_vec);
+    cv.reserve(2 * max_vec);
+    csig.reserve(max_vec);
+  }
   states.reserve(n);
   trace.reserve(2 * (n - 1));
   visits.reserve(2 * (n - 1));
@@ -334,7 +357,34 @@ void Chain::create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g) 
   ACHI_LAUNCHED(c);
   // initial state + canonicalize, environments, controller cold start (dmrg.cpp:222-250)
   if (init == ACHI_INIT_NEEL) {
-    upload_sites(neel_canonical(n, d));
+    auto hs = neel_canonical(n, d);
+    if (cplx) {  // real values, zero imaginary parts
+      for (auto& v : hs) {
+        std::vector<double> z(2 * v.size(), 0.0);
+        for (size_t t = 0; t < v.size(); ++t) z[2 * t] = v[t];
+        v.swap(z);
+      }
+      upload_sites_c(hs);
+    } else {
+      upload_sites(hs);
+    }
+  } else if (init == ACHI_INIT_RANDOM) {
+    std::vector<int> dims;
+    auto hs = random_complex_sites(n, d, g.controller.chi_min, g.seed, dims);
+    auto ds = canonical_on_device_c(c, hs, dims, d, 2);
+    for (int k = 1; k < n; ++k) chi[k] = dims[k];
+    copy_sites_device_c(ds);
+  } else if (cplx) {  // the real random start in complex storage
+    std::vector<int> dims;
+    auto hs = random_real_sites(n, d, g.controller.chi_min, g.seed, dims);
+    for (auto& v : hs) {
+      std::vector<double> z(2 * v.size(), 0.0);
+      for (size_t t = 0; t < v.size(); ++t) z[2 * t] = v[t];
+      v.swap(z);
+    }
+    auto ds = canonical_on_device_c(c, hs, dims, d, 2);
+    for (int k = 1; k < n; ++k) chi[k] = dims[k];
+    copy_sites_device_c(ds);
   } else {
     std::vector<int> dims;
     auto hs = random_real_sites(n, d, g.controller.chi_min, g.seed, dims);
@@ -390,6 +440,7 @@ double Chain::expectation_energy() {
     const int D = k < n ? mpo[k].l : 1;
     mx = std::max(mx, cp * cp * static_cast<size_t>(D));
   }
+  if (cplx) mx *= 2;
   DevBuf e[2];
   for (auto& b : e) {
     b.reserve(mx);
@@ -400,8 +451,12 @@ double Chain::expectation_energy() {
   int cur = 0;
   for (int k = 0; k < n; ++k) {
     ACHI_CUDA(cudaMemsetAsync(e[cur ^ 1].p, 0, sizeof(double) * mx, c.stream));
-    env_left(c, e[cur].p, site[k].p, pad2i(chi[k]), pad2i(chi[k + 1]), d, mpo[k].l, mpo[k].r,
-             mleft[k], e[cur ^ 1].p);
+    if (cplx)  // planar: the real part of L_n is plane 0
+      env_left_c(c, e[cur].p, site[k].p, pad2i(chi[k]), pad2i(chi[k + 1]), d, mpo[k].l, mpo[k].r,
+                 mleft[k], scr.p, e[cur ^ 1].p);
+    else
+      env_left(c, e[cur].p, site[k].p, pad2i(chi[k]), pad2i(chi[k + 1]), d, mpo[k].l, mpo[k].r,
+               mleft[k], e[cur ^ 1].p);
     cur ^= 1;
   }
   double h = 0.0;
@@ -411,13 +466,22 @@ double Chain::expectation_energy() {
 }
 
 void Chain::rebuild_envs() {  // Environment::rebuild(psi, mpo, 0), dmrg.cpp:51-56
-  for (int k = n - 2; k >= 0; --k)
-    env_right(*ctx, R[k + 1].p, site[k + 1].p, pad2i(chi[k + 2]), pad2i(chi[k + 1]), d,
-              mpo[k + 1].l, mpo[k + 1].r, mright[k + 1], R[k].p);
+  for (int k = n - 2; k >= 0; --k) {
+    if (cplx)
+      env_right_c(*ctx, R[k + 1].p, site[k + 1].p, pad2i(chi[k + 2]), pad2i(chi[k + 1]), d,
+                  mpo[k + 1].l, mpo[k + 1].r, mright[k + 1], scr.p, R[k].p);
+    else
+      env_right(*ctx, R[k + 1].p, site[k + 1].p, pad2i(chi[k + 2]), pad2i(chi[k + 1]), d,
+                mpo[k + 1].l, mpo[k + 1].r, mright[k + 1], R[k].p);
+  }
 }
 
 // visit_bond (dmrg.cpp:84-171)
 void Chain::visit(int b, bool right, int sweep_index, int slot) {
+  if (cplx) {
+    visit_complex(b, right, sweep_index, slot);
+    return;
+  }
   Ctx& c = *ctx;
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();

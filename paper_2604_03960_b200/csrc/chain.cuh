@@ -33,6 +33,15 @@ struct VisitHost {
 std::vector<DevBuf> canonical_on_device(Ctx& c, const std::vector<std::vector<double>>& sites,
                                         std::vector<int>& dims, int d, int times = 1);
 
+// complex128 counterparts (chain_complex.cu): canonicalize(psi, 0) of host
+// sites given as interleaved (re, im) (l, d, r) tensors, on the device by
+// complex SVD push_left; returns unpadded interleaved device sites.
+std::vector<DevBuf> canonical_on_device_c(Ctx& c, const std::vector<std::vector<double>>& sites,
+                                          std::vector<int>& dims, int d, int times = 1);
+// random_mps (mps.cpp:75-95): the reference's mt19937_64 complex draws
+std::vector<std::vector<double>> random_complex_sites(int n, int d, int chi, uint64_t seed,
+                                                      std::vector<int>& dims_out);
+
 struct Chain {
   Ctx* ctx = nullptr;
   achi_ctx* owner = nullptr;
@@ -70,6 +79,13 @@ struct Chain {
     long matvecs = 0, svd_sweeps = 0, visits = 0;
   } stats;
   bool profile = false;  // sync after each visit so phase times are exact
+  // complex128 chain: every site / environment / theta buffer holds two planes
+  // [Re; Im] of the real padded layout (contract.cuh); lhat / rhat are the
+  // realified environments of the current visit, scr the realified operands of
+  // the merge and the environment updates, cth / cu / cv / csig the
+  // interleaved theta and SVD factors of the complex SVD.
+  bool cplx = false;
+  DevBuf lhat, rhat, scr, cth, cu, cv, csig;
   // run-level bookkeeping (dmrg.cpp:255-281)
   double prev_energy = 0;
   bool have_prev = false;
@@ -80,6 +96,11 @@ struct Chain {
   void upload_sites(const std::vector<std::vector<double>>& host_sites);
   void copy_sites_device(const std::vector<DevBuf>& device_sites);
   void visit(int bond, bool moving_right, int sweep, int slot);
+  void visit_complex(int bond, bool moving_right, int sweep, int slot);
+  // interleaved complex sites: host (l, d, r) -> padded planar storage, and back
+  void upload_sites_c(const std::vector<std::vector<double>>& host_sites);
+  void copy_sites_device_c(const std::vector<DevBuf>& device_sites);
+  void download_site_c(int k, double* out);
   void sweep(int sweep_index, achi_sweep_record* rec, int32_t* chi_profile, double* entropy,
              achi_trace_row* trace_out, achi_visit_record* visits_out);
   long site_size(int k) const { return static_cast<long>(pad2i(chi[k])) * d * pad2i(chi[k + 1]); }

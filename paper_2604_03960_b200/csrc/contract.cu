@@ -252,6 +252,149 @@ void theta_merge(Ctx& ctx, const double* A, const double* B, int chl, int chm, i
        Operand{B, static_cast<long>(d) * chr, Major::kMN}, theta, static_cast<long>(d) * chr);
 }
 
+// ---------------------------------------------------------------------------
+// complex128, planar (contract.cuh)
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void realify_kernel(const double* __restrict__ src, long plane, long M, long K, long sm,
+                               long sk, int conj, double* __restrict__ dst) {
+  const long tot = M * K, ld = 2 * K;
+  for (long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; t < tot;
+       t += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long m = t / K, k = t - m * K;
+    const long o = m * sm + k * sk;
+    const double re = src[o], im = conj ? -src[o + plane] : src[o + plane];
+    dst[m * ld + k] = re;
+    dst[m * ld + K + k] = -im;
+    dst[(m + M) * ld + k] = im;
+    dst[(m + M) * ld + K + k] = re;
+  }
+}
+
+__global__ void ptranspose_kernel(const double* __restrict__ src, long rows, long cols,
+                                  double* __restrict__ dst) {
+  __shared__ double tile[32][33];
+  const long plane = rows * cols;
+  const long r0 = static_cast<long>(blockIdx.y) * 32, c0 = static_cast<long>(blockIdx.x) * 32;
+  for (int p = 0; p < 2; ++p) {
+    const double* s = src + p * plane;
+    double* dd = dst + p * plane;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const long r = r0 + i, c = c0 + threadIdx.x;
+      tile[i][threadIdx.x] = (r < rows && c < cols) ? s[r * cols + c] : 0.0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const long c = c0 + i, r = r0 + threadIdx.x;
+      if (r < rows && c < cols) dd[c * rows + r] = tile[threadIdx.x][i];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+void realify(Ctx& ctx, const double* src, long plane, long M, long K, long sm, long sk, bool conj,
+             double* dst) {
+  const long tot = M * K;
+  if (tot <= 0) return;
+  const int blocks = static_cast<int>(std::min<long>(cdiv(tot, 256), 8L * ctx.num_sms));
+  realify_kernel<<<blocks, 256, 0, ctx.stream>>>(src, plane, M, K, sm, sk, conj ? 1 : 0, dst);
+  ACHI_LAUNCHED(ctx);
+}
+
+void planar_transpose(Ctx& ctx, const double* src, long rows, long cols, double* dst) {
+  if (rows <= 0 || cols <= 0) return;
+  dim3 grid(static_cast<unsigned>(cdiv(cols, 32)), static_cast<unsigned>(cdiv(rows, 32)));
+  ptranspose_kernel<<<grid, dim3(32, 8), 0, ctx.stream>>>(src, rows, cols, dst);
+  ACHI_LAUNCHED(ctx);
+}
+
+void heff_prepare_c(Ctx& ctx, const double* L, int chl_, int D1_, const double* R, int chr_,
+                    int D3_, double* Lhat, double* Rhat) {
+  const long chl = chl_, D1 = D1_, chr = chr_, D3 = D3_;
+  // L as [(bl, a), jl]; R as [br, (e, jr)]
+  realify(ctx, L, chl * D1 * chl, chl * D1, chl, chl, 1, false, Lhat);
+  realify(ctx, R, chr * D3 * chr, chr, D3 * chr, D3 * chr, 1, false, Rhat);
+}
+
+void heff_apply_c(Ctx& ctx, const HeffOpsC& op, const double* theta, double* out) {
+  const long chl = op.chl, chr = op.chr, d = op.d, D1 = op.D1, D3 = op.D3;
+  double* X = ctx.ws_a.reserve(static_cast<size_t>(2 * chl * D1 * d * d * chr));
+  double* Y = ctx.ws_b.reserve(static_cast<size_t>(2 * chl * d * d * D3 * chr));
+  // X[(q,bl,a),(s1,s2,jr)] = Lhat[(q,bl,a),(p,jl)] theta[(p,jl),(s1,s2,jr)]
+  gemm(ctx, static_cast<int>(2 * chl * D1), static_cast<int>(d * d * chr), static_cast<int>(2 * chl),
+       Operand{op.Lhat, 2 * chl, Major::kK}, Operand{theta, d * d * chr, Major::kMN}, X, d * d * chr);
+  // Y[(bl,s1',s2'),(q,e,jr)]: the plane inside each row
+  for (long q = 0; q < 2; ++q) {
+    MixGeom g{static_cast<int>(d * d), static_cast<int>(D3),
+              D1 * d * d * chr, 1, d * d * chr, chr,
+              d * d * 2 * D3 * chr, 1, 2 * D3 * chr, chr,
+              chl, chr};
+    mix(ctx, X + q * chl * D1 * d * d * chr, Y + q * D3 * chr, op.mix, g);
+  }
+  // out_q[(bl,s1',s2'), br] = Y[(bl,s1',s2'), (p,e,jr)] Rhat[(q,br), (p,e,jr)]
+  for (long q = 0; q < 2; ++q)
+    gemm(ctx, static_cast<int>(chl * d * d), static_cast<int>(chr), static_cast<int>(2 * D3 * chr),
+         Operand{Y, 2 * D3 * chr, Major::kK}, Operand{op.Rhat + q * chr * 2 * D3 * chr, 2 * D3 * chr, Major::kK},
+         out + q * chl * d * d * chr, chr);
+}
+
+void env_left_c(Ctx& ctx, const double* L, const double* A, int chl_, int chn_, int d_, int Dl_,
+                int Dr_, const DevMix& W, double* scr, double* Lnew) {
+  const long chl = chl_, chn = chn_, d = d_, Dl = Dl_, Dr = Dr_;
+  double* T1 = ctx.ws_a.reserve(static_cast<size_t>(2 * chl * Dl * d * chn));
+  double* T2 = ctx.ws_b.reserve(static_cast<size_t>(2 * chl * d * Dr * chn));
+  // T1 planar [(q,b,a),(s,j')] = realify(L as [(b,a), j]) . A planar [(p,j),(s,j')]
+  realify(ctx, L, chl * Dl * chl, chl * Dl, chl, chl, 1, false, scr);
+  gemm(ctx, static_cast<int>(2 * chl * Dl), static_cast<int>(d * chn), static_cast<int>(2 * chl),
+       Operand{scr, 2 * chl, Major::kK}, Operand{A, d * chn, Major::kMN}, T1, d * chn);
+  // T2 planar [(q,b,s'),(a',j')]: the planes are one more outer index of uniform stride
+  MixGeom g{static_cast<int>(d), static_cast<int>(Dr),
+            Dl * d * chn, 1, d * chn, chn,
+            d * Dr * chn, 1, Dr * chn, chn,
+            2 * chl, chn};
+  mix(ctx, T1, T2, W, g);
+  // Lnew planar [(q,b'),(a',j')] = realify(A^dagger as [b', (b,s')]) . T2 planar
+  realify(ctx, A, chl * d * chn, chn, chl * d, 1, chn, true, scr);
+  gemm(ctx, static_cast<int>(2 * chn), static_cast<int>(Dr * chn), static_cast<int>(2 * chl * d),
+       Operand{scr, 2 * chl * d, Major::kK}, Operand{T2, Dr * chn, Major::kMN}, Lnew, Dr * chn);
+}
+
+void env_right_c(Ctx& ctx, const double* R, const double* B, int chr_, int chn_, int d_, int Dl_,
+                 int Dr_, const DevMix& W, double* scr, double* Rnew) {
+  const long chr = chr_, chn = chn_, d = d_, Dl = Dl_, Dr = Dr_;
+  double* T1 = ctx.ws_a.reserve(static_cast<size_t>(2 * chr * Dr * chn * d));
+  double* T2 = ctx.ws_b.reserve(static_cast<size_t>(2 * d * chr * Dl * chn));
+  double* Bt = scr + std::max(4 * chr * chr * Dr, 4 * chn * d * chr);
+  // T1 planar [(q,b,e),(j,s)] = realify(R as [(b,e), j'']) . B^T planar [(p,j''),(j,s)]
+  planar_transpose(ctx, B, chn * d, chr, Bt);
+  realify(ctx, R, chr * Dr * chr, chr * Dr, chr, chr, 1, false, scr);
+  gemm(ctx, static_cast<int>(2 * chr * Dr), static_cast<int>(chn * d), static_cast<int>(2 * chr),
+       Operand{scr, 2 * chr, Major::kK}, Operand{Bt, chn * d, Major::kMN}, T1, chn * d);
+  // T2 planar [(q,s',b),(a,j)], one mixing launch per plane
+  for (long q = 0; q < 2; ++q) {
+    MixGeom g{static_cast<int>(d), static_cast<int>(Dl),
+              Dr * chn * d, d, chn * d, 1,
+              Dl * chn, 1, chr * Dl * chn, chn,
+              chr, chn};
+    mix(ctx, T1 + q * chr * Dr * chn * d, T2 + q * d * chr * Dl * chn, W, g);
+  }
+  // Rnew planar [(q,b'),(a,j)] = realify(conj(B) as [b', (s',b)]) . T2 planar
+  realify(ctx, B, chn * d * chr, chn, d * chr, d * chr, 1, true, scr);
+  gemm(ctx, static_cast<int>(2 * chn), static_cast<int>(Dl * chn), static_cast<int>(2 * d * chr),
+       Operand{scr, 2 * d * chr, Major::kK}, Operand{T2, Dl * chn, Major::kMN}, Rnew, Dl * chn);
+}
+
+void theta_merge_c(Ctx& ctx, const double* A, const double* B, int chl_, int chm_, int chr_, int d_,
+                   double* scr, double* theta) {
+  const long chl = chl_, chm = chm_, chr = chr_, d = d_;
+  realify(ctx, A, chl * d * chm, chl * d, chm, chm, 1, false, scr);
+  gemm(ctx, static_cast<int>(2 * chl * d), static_cast<int>(d * chr), static_cast<int>(2 * chm),
+       Operand{scr, 2 * chm, Major::kK}, Operand{B, d * chr, Major::kMN}, theta, d * chr);
+}
+
 void upload_padded3(Ctx& ctx, const double* host, int l, int d, int r, double* dev) {
   const int lp = pad2i(l), rp = pad2i(r);
   ACHI_CUDA(cudaMemsetAsync(dev, 0, sizeof(double) * lp * d * rp, ctx.stream));

@@ -75,6 +75,50 @@ void env_right(Ctx& ctx, const double* R, const double* B, int chr, int chn, int
 void theta_merge(Ctx& ctx, const double* A, const double* B, int chl, int chm, int chr, int d,
                  double* theta);
 
+// ---------------------------------------------------------------------------
+// complex128 (planar).  A complex tensor is stored as two planes [Re; Im], each
+// in the real padded layout above (plane stride = one plane's element count).
+// Every complex contraction is one real DMMA GEMM of doubled M and K:
+//   C_planar = realify(A) . B_planar,  realify(A) = [[Ar, -Ai], [Ai, Ar]]
+// with the left operand realified (rows (q, m), cols (p, k)) and the right
+// operand planar with the contracted index leading (rows (p, k)); the output
+// is planar with its M index leading.  Where the H_eff's second GEMM has the
+// intermediate on the left, the intermediate is written with the plane inside
+// its rows (Y[m, (p, k)]) and each output plane is one GEMM against one half of
+// the realified environment.  4 real multiplies per complex one (4M), all on
+// the FP64 tensor cores; the MPO mixing stays real (real-gauge W).
+// ---------------------------------------------------------------------------
+
+// dst (2M x 2K row-major) = realify of the matrix view z(m, k) = src[m sm + k sk]
+// (+ plane offset for the imaginary part), conjugated when `conj`.
+void realify(Ctx& ctx, const double* src, long plane, long M, long K, long sm, long sk, bool conj,
+             double* dst);
+// planar dst[p][k][n] = src[p][n][k] (two planes of rows x cols -> cols x rows)
+void planar_transpose(Ctx& ctx, const double* src, long rows, long cols, double* dst);
+
+struct HeffOpsC {
+  const double* Lhat;  // realify(L as [(bl, a), jl]): (2 chl~ D1) x (2 chl~)
+  const double* Rhat;  // realify(R as [br, (e, jr)]): (2 chr~) x (2 D3 chr~)
+  int chl, chr;        // padded
+  int d, D1, D3;
+  DevMix mix;
+};
+// out = H_eff theta on planar (chl~, d, d, chr~) complex tensors (dmrg.cpp:58-71)
+void heff_apply_c(Ctx& ctx, const HeffOpsC& op, const double* theta, double* out);
+// Lhat / Rhat of HeffOpsC from planar environments
+void heff_prepare_c(Ctx& ctx, const double* L, int chl, int D1, const double* R, int chr, int D3,
+                    double* Lhat, double* Rhat);
+// planar environment updates (update_left / update_right, dmrg.cpp:26-49); scr
+// holds >= max(4 chl~^2 Dl, 4 chn~ chl~ d) (left) / max(4 chr~^2 Dr, 4 chn~ d chr~)
+// + 2 chn~ d chr~ (right) doubles
+void env_left_c(Ctx& ctx, const double* L, const double* A, int chl, int chn, int d, int Dl, int Dr,
+                const DevMix& mix, double* scr, double* Lnew);
+void env_right_c(Ctx& ctx, const double* R, const double* B, int chr, int chn, int d, int Dl,
+                 int Dr, const DevMix& mix, double* scr, double* Rnew);
+// planar theta (chl~, d, d, chr~) = A . B; scr >= 4 chl~ d chm~ doubles
+void theta_merge_c(Ctx& ctx, const double* A, const double* B, int chl, int chm, int chr, int d,
+                   double* scr, double* theta);
+
 // Copy a host (l, d, r) tensor into a padded device tensor (l~, d, r~) with zero pads.
 void upload_padded3(Ctx& ctx, const double* host, int l, int d, int r, double* dev);
 // Copy a padded device tensor (l~, m, r~) to host (l, m, r).

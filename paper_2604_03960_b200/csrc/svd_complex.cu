@@ -90,8 +90,8 @@ struct GsRun {
 };
 
 // Complex Gram-Schmidt of one run (one CTA): candidate t (real index) read as
-// z = x + i y (length n) with its left vector w (length m); projected against
-// the vectors already kept for this run, kept when at least half of its norm
+// z = x + i y (length n) with its left vector w (length m); projected (twice)
+// against the vectors already kept for this run, kept when at least half of its norm
 // remains, until count / 2 are kept.  The inner products and norms are taken
 // on the side whose real vectors are orthonormal by construction (prim_u: the
 // left side; the other side is normalised Jacobi columns, zero for zero
@@ -121,6 +121,7 @@ __global__ void gs_kernel(const double* __restrict__ ue, const double* __restric
     for (int i = threadIdx.x; i < m; i += blockDim.x)
       cw[i] = make_double2(ue[static_cast<long>(i) * r2 + t], ue[static_cast<long>(i + m) * r2 + t]);
     __syncthreads();
+    for (int pass = 0; pass < 2; ++pass)  // projected twice (CGS2-style reorthogonalisation)
     for (int k = 0; k < kept; ++k) {
       double2 c = make_double2(0.0, 0.0);  // c = <p_k, cand_p> = sum conj(p_k) cand_p
       for (int i = threadIdx.x; i < lp; i += blockDim.x) {
@@ -200,14 +201,15 @@ __global__ void cphase_kernel(double2* __restrict__ U, double2* __restrict__ Vd,
 }  // namespace
 
 int svd_complex_device(Ctx& c, SvdWs& ws, const double* a, int m, int n, double* sigma, double* U,
-                       double* Vd) {
+                       double* Vd, int side_pref) {
   const int r = std::min(m, n), r2 = 2 * r, m2 = 2 * m, n2 = 2 * n;
   DevBuf E, UE, VTE, S2;
   E.reserve(static_cast<size_t>(m2) * n2);
   embed_kernel<<<std::max(1, std::min(cdiv(static_cast<long>(m) * n, 256), 8 * c.num_sms)), 256, 0, c.stream>>>(
       reinterpret_cast<const double2*>(a), m, n, E.p);
   ACHI_LAUNCHED(c);
-  const SvdSide side = m2 <= n2 ? SvdSide::kRows : SvdSide::kCols;
+  const SvdSide side = side_pref < 0 ? (m2 <= n2 ? SvdSide::kRows : SvdSide::kCols)
+                                     : (side_pref == 0 ? SvdSide::kRows : SvdSide::kCols);
   SvdResultDev res = svd_device(c, ws, E.p, m2, n2, m2, n2, side);
   svd_phase_signs(c, ws, res, r2);
   UE.reserve(static_cast<size_t>(m2) * r2);
@@ -217,15 +219,26 @@ int svd_complex_device(Ctx& c, SvdWs& ws, const double* a, int m, int n, double*
   ACHI_CUDA(cudaMemcpyAsync(s.data(), res.sigma, sizeof(double) * r2, cudaMemcpyDeviceToHost, c.stream));
   c.sync();
   const int sweeps = res.sweeps();
-  // runs of near-equal values (closer than 1e-6 sigma_1 to the next)
-  const double tol = 1e-6 * s[0];
+  // runs: values closer than 1e-4 sigma_1 to the next one (or than the Jacobi
+  // noise floor 64 sqrt(mg) eps ||E||_F, svd_jacobi.cu zero_floor_kernel); the
+  // values at or below the floor join the run above them (the vectors of values
+  // near the floor are as undetermined as the noise subspace, so the two are
+  // orthonormalised together).  Real vectors of values a gap g apart mix by
+  // ~eps sigma_1 / g, so a lone pair's first real vector is its complex vector
+  // to ~2e-12; inside a run the complex Gram-Schmidt visits the candidates in
+  // sigma order and keeps one vector per pair, so each kept vector stays with
+  // its own value unless the values are degenerate to that level.
+  double fro2 = 0.0;
+  for (int t = 0; t < r2; ++t) fro2 += s[t] * s[t];
+  const double floor_v = 64.0 * std::sqrt(static_cast<double>(res.mg)) * 2.220446049250313e-16 *
+                         std::sqrt(fro2);
   std::vector<int> src(r, -1);
   std::vector<GsRun> runs;
   std::vector<double> sig(r);
   int q = 0;
   for (int t = 0; t < r2;) {
     int e = t + 1;
-    while (e < r2 && s[e - 1] - s[e] <= tol) ++e;
+    while (e < r2 && (s[e] <= floor_v || s[e - 1] - s[e] <= std::max(1e-4 * s[0], floor_v))) ++e;
     int cnt = e - t;
     if (cnt % 2) {  // a run must hold whole pairs: extend by the next value
       if (e >= r2) fail(ACHI_E_NUMERICAL_FAILURE, "svd (complex): unpaired singular value");

@@ -87,7 +87,10 @@ void svd_gather(Ctx& ctx, SvdWs& ws, const SvdResultDev& r, int k, double* U, do
 // Complex svd_full (svd_complex.cu): a (m x n row-major, interleaved re/im,
 // device); sigma (r = min(m,n), device), U (m x r) and V^dagger (r x n),
 // row-major interleaved, fix_phases applied.  Returns the Jacobi sweeps.
+// side_pref: -1 by shape; 0 = U, 1 = V^dagger orthonormal to working precision
+// across the whole spectrum (noise-level values included; the other factor's
+// vectors of such values are only defined up to their sigma weight).
 int svd_complex_device(Ctx& ctx, SvdWs& ws, const double* a, int m, int n, double* sigma, double* U,
-                       double* Vd);
+                       double* Vd, int side_pref = -1);
 
 }  // namespace achi

@@ -686,9 +686,13 @@ struct DmrgConfig {
   InitialState initial_state = InitialState::automatic;
   uint64_t seed = 1234;
   double noise_floor = 1e-14;
+  // complex128 like the reference (automatic -> the complex random_mps for
+  // TFIM, dmrg.cpp:222-235); real (default) runs real-valued states in FP64
+  enum class Arithmetic { real, complex };
+  Arithmetic arithmetic = Arithmetic::real;
   achi_dmrg_config c() const {
-    return {max_sweeps, eig_max_iter, eps_conv, eig_tol, static_cast<int32_t>(initial_state), 0,
-            seed, noise_floor, controller.c()};
+    return {max_sweeps, eig_max_iter, eps_conv, eig_tol, static_cast<int32_t>(initial_state),
+            static_cast<int32_t>(arithmetic), seed, noise_floor, controller.c()};
   }
 };
 struct SweepRecord {
@@ -746,6 +750,27 @@ class Chain {
     std::vector<int32_t> d(n_ - 1);
     achi_chain_bond_dims(h_, d.data());
     return std::vector<int>(d.begin(), d.end());
+  }
+  // the current MPS (complex tensors, as the reference holds psi)
+  mps::MatrixProductState state() const {
+    const std::vector<int> b = bond_dims();
+    const bool cplx = achi_chain_is_complex(h_) != 0;
+    std::vector<Tensor> sites;
+    for (int k = 0; k < n_; ++k) {
+      const long l = k == 0 ? 1 : b[static_cast<size_t>(k - 1)];
+      const long r = k == n_ - 1 ? 1 : b[static_cast<size_t>(k)];
+      Tensor t({l, 2, r});
+      std::vector<double> buf(static_cast<size_t>(2 * l * 2 * r));
+      if (cplx) {
+        b200::check(achi_chain_get_site_complex(h_, k, buf.data(), buf.size()));
+        for (long i = 0; i < t.size(); ++i) t.data()[i] = Cplx(buf[2 * i], buf[2 * i + 1]);
+      } else {
+        b200::check(achi_chain_get_site(h_, k, buf.data(), buf.size()));
+        for (long i = 0; i < t.size(); ++i) t.data()[i] = Cplx(buf[i], 0.0);
+      }
+      sites.push_back(std::move(t));
+    }
+    return mps::MatrixProductState(std::move(sites));
   }
   static SweepRecord to_record(const achi_sweep_record& r, const int32_t* chi, const double* ent,
                                int nb) {

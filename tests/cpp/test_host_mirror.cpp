@@ -391,11 +391,23 @@ static void test_dmrg(double e_heis8, double e_tfim8) {
     auto r1 = dmrg::run_dmrg(heisenberg(8, models::SpinConvention::pauli), adaptive_config(32));
     for (const auto& s : r1.sweeps) CHECK(s.energy >= e_heis8 - 1e-9);
     // the reference's automatic start for TFIM is a random complex MPS
-    // (dmrg.cpp:230-236), which the real FP64 device path rejects; start from Neel
+    // (dmrg.cpp:230-236): complex arithmetic runs it unchanged
     auto tc = adaptive_config(32);
-    tc.initial_state = dmrg::DmrgConfig::InitialState::neel;
+    tc.arithmetic = dmrg::DmrgConfig::Arithmetic::complex;
     auto r2 = dmrg::run_dmrg(tfim(8, 1.0), tc);
     for (const auto& s : r2.sweeps) CHECK(s.energy >= e_tfim8 - 1e-9);
+    CHECK(std::abs(r2.energy - e_tfim8) <= 1e-8);
+    // the chain's state comes back as complex tensors: the complex random
+    // start (mps.cpp:75-95) has unit norm and genuinely complex entries
+    dmrg::Chain ch(tfim(8, 1.0), tc);
+    auto psi = ch.state();
+    CHECK(psi.size() == 8);
+    double nrm = 0, imag = 0;
+    for (long i = 0; i < psi.site(0).size(); ++i) nrm += std::norm(psi.site(0).data()[i]);
+    for (int k = 0; k < psi.size(); ++k)
+      for (long i = 0; i < psi.site(k).size(); ++i) imag = std::max(imag, std::abs(psi.site(k).data()[i].imag()));
+    CHECK(std::abs(nrm - 1.0) <= 1e-12);
+    CHECK(imag > 1e-3);
   }
   {  // test_dmrg.cpp:144, 254, 270
     ctrl::ControllerTrace trace;

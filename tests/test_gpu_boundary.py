@@ -119,3 +119,21 @@ def test_eigs_callback_errors(ctx):
     with pytest.raises(Exception) as ei:
         ctx.eigs_lowest(lambda x: h @ x, np.ones(32), 1e-14, 3)
     assert ei.value.name == "EigenNonConvergence" and ei.value.residual > 0
+
+
+@pytest.mark.parametrize("n,lo", [(32, -17), (64, -16), (48, -20), (40, -8)])
+def test_svd_complex_graded_spectrum(ctx, n, lo):
+    """DMRG-like exponentially graded spectra down past the noise floor: the
+    orthonormal factor (U for a square matrix) stays unitary across the whole
+    spectrum -- the tail and the noise subspace are orthonormalised together by
+    the complex Gram-Schmidt of svd_complex.cu; the lone pairs above them carry
+    the Jacobi vectors' own ~1e-11 accuracy on such spectra -- and U S V^dagger
+    reproduces A."""
+    rng = np.random.default_rng(n - lo)
+    s = np.logspace(0, lo, n)
+    a = unitary(rng, n) @ np.diag(s) @ unitary(rng, n)
+    u, sg, vd = ctx.svd_complex(a)
+    assert np.abs(u.conj().T @ u - np.eye(n)).max() <= 1e-10
+    assert np.linalg.norm(u @ np.diag(sg) @ vd - a) <= 1e-12
+    big = s > 1e-10
+    assert np.abs(sg[big] - s[big]).max() <= 1e-13
