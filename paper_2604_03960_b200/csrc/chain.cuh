@@ -85,7 +85,8 @@ struct Chain {
   // the merge and the environment updates, cth / cu / cv / csig the
   // interleaved theta and SVD factors of the complex SVD.
   bool cplx = false;
-  DevBuf lhat, rhat, scr, cth, cu, cv, csig;
+  DevBuf lhat, rhat, scr, cth, cu, cv, csig, cv_keep;
+  CsvdPlan cplan;
   // run-level bookkeeping (dmrg.cpp:255-281)
   double prev_energy = 0;
   bool have_prev = false;

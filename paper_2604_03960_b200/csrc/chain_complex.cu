@@ -321,8 +321,21 @@ void Chain::visit_complex(int b, bool right, int sweep_index, int slot) {
   const int m = chl * d, nn = d * chr, rk = std::min(m, nn);
   c.acc.begin(EventAcc::kSvd, c.stream);
   from_planar3(c, vec.p, chl, d * d, chr, cth.p);
-  // the factor that stays canonical is the orthonormal one (U moving right, V^dagger left)
-  const int svd_sweeps = svd_complex_device(c, svd, cth.p, m, nn, csig.p, cu.p, cv.p, right ? 0 : 1);
+  // the factor that stays canonical is the orthonormal one (U moving right, V^dagger left);
+  // warm start from the previous decomposition of this bond and direction (as the real path)
+  const SvdSide side = right ? SvdSide::kRows : SvdSide::kCols;
+  const int ngw = svd_working_cols(2 * m, 2 * nn, side);
+  VKeep& vk = vkeep[2 * static_cast<size_t>(b) + (right ? 1 : 0)];
+  const bool warm = warm_svd && vk.valid && vk.m == 2 * m && vk.n == 2 * nn;
+  cv_keep.reserve(static_cast<size_t>(ngw) * ngw);
+  const int svd_sweeps = svd_complex_stage1(c, svd, cplan, cth.p, m, nn, csig.p, right ? 0 : 1,
+                                            warm ? vk.v.p : nullptr, warm_svd ? cv_keep.p : nullptr);
+  if (warm_svd) {  // the buffers rotate: this bond keeps the new factor
+    std::swap(vk.v, cv_keep);
+    vk.m = 2 * m;
+    vk.n = 2 * nn;
+    vk.valid = true;
+  }
   c.acc.end(c.stream, 0.0);
   bond_select(c, csig.p, rk, cfg, states.p, b, sweep_index, right ? 1 : 0, trace.p + slot,
               visits.p + slot, bout.p);
@@ -338,6 +351,7 @@ void Chain::visit_complex(int b, bool right, int sweep_index, int slot) {
   const int kept = bo.kept;
   if (!(bo.lam_norm > 0)) fail(ACHI_E_DEGENERATE_SPECTRUM, "dmrg: empty truncation");
   const int kp = pad2i(kept);
+  svd_complex_stage2(c, cplan, kept, cu.p, cv.p);  // the kept vectors only
   {
     AbsorbC a{reinterpret_cast<const double2*>(cu.p), reinterpret_cast<const double2*>(cv.p), csig.p,
               bout.p, rk, nn, kept, kp, chl, chlp, chr, chrp, d, right ? 1 : 0, site[b].p, site[b + 1].p};

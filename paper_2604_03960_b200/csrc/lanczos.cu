@@ -1414,9 +1414,9 @@ void LanczosWs::reserve(long n) {
   }
 }
 
-void device_norm2(Ctx& ctx, const double* x, long n, double* result) {
+void device_norm2(Ctx& ctx, const double* x, long n, double* result, double* part) {
   const int nb = red_blocks(ctx, n);
-  double* part = ctx.red.reserve(static_cast<size_t>(nb) * 2 + 8);
+  if (!part) part = ctx.red.reserve(static_cast<size_t>(nb) * 2 + 8);
   multi_dot_kernel<<<nb, RED_THREADS, 0, ctx.stream>>>(x, 0, 0, x, n, part, 1, 1);
   ACHI_LAUNCHED(ctx);
   reduce_partials_kernel<<<1, RED_THREADS, 0, ctx.stream>>>(part, nb, 1, 1, result);
@@ -1560,7 +1560,7 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
     LanczosResult& R = *ws.res_h.p;
     R = LanczosResult{};
     R.ctl.best = std::numeric_limits<double>::infinity();
-    device_norm2(ctx, v0, n, misc + 2);
+    device_norm2(ctx, v0, n, misc + 2, ws.partials.p);
     double h_n2;
     ACHI_CUDA(cudaMemcpyAsync(&h_n2, misc + 2, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
     ctx.sync();
@@ -1705,8 +1705,9 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
   if (!lg.exec || lg.key != key) {
     const auto tb = std::chrono::steady_clock::now();
     ++builds;
-    // every buffer a captured kernel uses is sized before capture
-    ctx.red.reserve(static_cast<size_t>(red_blocks(ctx, n)) * 2 + 8);
+    // every buffer a captured kernel uses is sized before capture and owned by
+    // ws (growth resets the cached graphs); the v0 norm reduces into ws.partials,
+    // not the context's shared scratch, whose growth another solver could trigger
     // keep the executable graph: a graph of the same topology (another shape
     // of this bond) is applied to it by cudaGraphExecUpdate, much cheaper than
     // a new instantiation; anything else re-instantiates
@@ -1746,7 +1747,7 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
       ACHI_CUDA(cudaGraphConditionalHandleCreate(&outer, lg.graph, 0, 0));
       // prologue
       begin(lg.graph, nullptr, 0);
-      device_norm2(ctx, v0, n, misc + 2);
+      device_norm2(ctx, v0, n, misc + 2, ws.partials.p);
       eig_init_kernel<<<1, 1, 0, ctx.stream>>>(misc, ws.ctl.p, block, max_iter, tol, outer);
       ACHI_LAUNCHED(ctx);
       K.scale(ws.q(0), v0, misc + 3, true);

@@ -123,7 +123,8 @@ EigsOut eigs_lowest(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, long 
 
 // Deterministic device reductions used across the hot path.
 // sum_i x_i^2 -> *result (device)
-void device_norm2(Ctx& ctx, const double* x, long n, double* result);
+// part: scratch of >= 2 * ceil(n / 1024) + 8 doubles, or null for the context's
+void device_norm2(Ctx& ctx, const double* x, long n, double* result, double* part = nullptr);
 // dst = src * (*scale) (scale device scalar), or src / (*scale) when invert
 void device_scale(Ctx& ctx, double* dst, const double* src, long n, const double* scale, bool invert);
 

@@ -21,6 +21,7 @@
 // orthonormal to ~eps/1e-6 even where the real vectors of neighbouring values
 // mix.
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "svd_jacobi.cuh"
@@ -47,15 +48,17 @@ __global__ void embed_kernel(const double2* __restrict__ a, int m, int n, double
 // lone pairs: complex index q takes real index src[q] (src < 0: Gram-Schmidt run)
 //   U[i][q] = p_i + i q_i from UE[:, src], Vd[q][j] = conj(x_j + i y_j) from VTE[src, :]
 __global__ void pick_kernel(const double* __restrict__ ue, const double* __restrict__ vte, int m,
-                            int n, int r2, const int* __restrict__ src, int r,
+                            int n, int r2, const int* __restrict__ src, int r, int k,
                             double2* __restrict__ U, double2* __restrict__ Vd) {
-  const long tu = static_cast<long>(m) * r, tv = static_cast<long>(r) * n;
+  const long tu = static_cast<long>(m) * k, tv = static_cast<long>(k) * n;
   for (long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; t < tu + tv;
        t += static_cast<long>(gridDim.x) * blockDim.x) {
     if (t < tu) {
-      const int i = static_cast<int>(t / r), q = static_cast<int>(t % r);
+      const int i = static_cast<int>(t / k), q = static_cast<int>(t % k);
       const int s = src[q];
-      if (s >= 0) U[t] = make_double2(ue[static_cast<long>(i) * r2 + s], ue[static_cast<long>(i + m) * r2 + s]);
+      if (s >= 0)
+        U[static_cast<long>(i) * r + q] =
+            make_double2(ue[static_cast<long>(i) * r2 + s], ue[static_cast<long>(i + m) * r2 + s]);
     } else {
       const long u = t - tu;
       const int q = static_cast<int>(u / n), j = static_cast<int>(u % n);
@@ -84,10 +87,6 @@ __device__ double2 block_sum2(double2 v, double2* sh) {
   return r;  // every thread, same order
 }
 
-struct GsRun {
-  int first, count;  // real members [first, first + count)
-  int out;           // first complex output index; count / 2 outputs
-};
 
 // Complex Gram-Schmidt of one run (one CTA): candidate t (real index) read as
 // z = x + i y (length n) with its left vector w (length m); projected (twice)
@@ -98,14 +97,14 @@ struct GsRun {
 // values), the other side gets the same combination.  cand: scratch (n + m)
 // complex per run.
 __global__ void gs_kernel(const double* __restrict__ ue, const double* __restrict__ vte, int m, int n,
-                          int r2, const GsRun* __restrict__ runs, int r, double2* __restrict__ U,
+                          int r2, const CsvdRun* __restrict__ runs, int r, double2* __restrict__ U,
                           double2* __restrict__ Vd, double2* __restrict__ cand, int prim_u,
                           int* __restrict__ fail) {
   __shared__ double2 sh[32];
-  const GsRun g = runs[blockIdx.x];
+  const CsvdRun g = runs[blockIdx.x];
   double2* cz = cand + static_cast<long>(blockIdx.x) * (n + m);
   double2* cw = cz + n;
-  const int want = g.count / 2;
+  const int want = g.want;
   // primary side: length lp, entry i of kept vector k and of the candidate
   const int lp = prim_u ? m : n;
   auto kept_p = [&](int k, int i) -> double2 {
@@ -162,10 +161,11 @@ __global__ void gs_kernel(const double* __restrict__ ue, const double* __restric
 
 // fix_phases (linalg.cpp:19-35), one warp per column q: f = conj(u_imax) / |u_imax|
 // for the first index of the largest |u|; U[:, q] *= f, Vd[q, :] *= conj(f)
-__global__ void cphase_kernel(double2* __restrict__ U, double2* __restrict__ Vd, int m, int n, int r) {
+__global__ void cphase_kernel(double2* __restrict__ U, double2* __restrict__ Vd, int m, int n, int r,
+                              int k) {
   const int warps = blockDim.x >> 5;
   const int q = blockIdx.x * warps + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (q >= r) return;
+  if (q >= k) return;
   double best = 0.0;
   int idx = 0x7fffffff;
   for (int i = lane; i < m; i += 32) {
@@ -200,25 +200,33 @@ __global__ void cphase_kernel(double2* __restrict__ U, double2* __restrict__ Vd,
 
 }  // namespace
 
-int svd_complex_device(Ctx& c, SvdWs& ws, const double* a, int m, int n, double* sigma, double* U,
-                       double* Vd, int side_pref) {
+int svd_complex_stage1(Ctx& c, SvdWs& ws, CsvdPlan& P, const double* a, int m, int n, double* sigma,
+                       int side_pref, const double* v_init, double* v_keep) {
   const int r = std::min(m, n), r2 = 2 * r, m2 = 2 * m, n2 = 2 * n;
-  DevBuf E, UE, VTE, S2;
-  E.reserve(static_cast<size_t>(m2) * n2);
+  P.m = m;
+  P.n = n;
+  P.r = r;
+  P.r2 = r2;
+  P.E.reserve(static_cast<size_t>(m2) * n2);
   embed_kernel<<<std::max(1, std::min(cdiv(static_cast<long>(m) * n, 256), 8 * c.num_sms)), 256, 0, c.stream>>>(
-      reinterpret_cast<const double2*>(a), m, n, E.p);
+      reinterpret_cast<const double2*>(a), m, n, P.E.p);
   ACHI_LAUNCHED(c);
   const SvdSide side = side_pref < 0 ? (m2 <= n2 ? SvdSide::kRows : SvdSide::kCols)
                                      : (side_pref == 0 ? SvdSide::kRows : SvdSide::kCols);
-  SvdResultDev res = svd_device(c, ws, E.p, m2, n2, m2, n2, side);
+  P.prim_u = side == SvdSide::kRows;
+  SvdResultDev res = svd_device(c, ws, P.E.p, m2, n2, m2, n2, side, 1, 0, nullptr, true, v_init);
+  if (v_keep)  // the real factor of E, a warm start for the next decomposition of this shape
+    ACHI_CUDA(cudaMemcpyAsync(v_keep, res.V, sizeof(double) * res.ng * res.ng, cudaMemcpyDeviceToDevice,
+                              c.stream));
   svd_phase_signs(c, ws, res, r2);
-  UE.reserve(static_cast<size_t>(m2) * r2);
-  VTE.reserve(static_cast<size_t>(r2) * n2);
-  svd_gather(c, ws, res, r2, UE.p, VTE.p);
-  std::vector<double> s(r2);
+  P.UE.reserve(static_cast<size_t>(m2) * r2);
+  P.VTE.reserve(static_cast<size_t>(r2) * n2);
+  svd_gather(c, ws, res, r2, P.UE.p, P.VTE.p);
+  std::vector<double>& s = P.s;
+  s.resize(r2);
   ACHI_CUDA(cudaMemcpyAsync(s.data(), res.sigma, sizeof(double) * r2, cudaMemcpyDeviceToHost, c.stream));
   c.sync();
-  const int sweeps = res.sweeps();
+  P.sweeps = res.sweeps();
   // runs: values closer than 1e-4 sigma_1 to the next one (or than the Jacobi
   // noise floor 64 sqrt(mg) eps ||E||_F, svd_jacobi.cu zero_floor_kernel); the
   // values at or below the floor join the run above them (the vectors of values
@@ -227,14 +235,16 @@ int svd_complex_device(Ctx& c, SvdWs& ws, const double* a, int m, int n, double*
   // ~eps sigma_1 / g, so a lone pair's first real vector is its complex vector
   // to ~2e-12; inside a run the complex Gram-Schmidt visits the candidates in
   // sigma order and keeps one vector per pair, so each kept vector stays with
-  // its own value unless the values are degenerate to that level.
+  // its own value unless the values are degenerate to that level.  (A gap
+  // relative to the values themselves is not enough: measured 1e-6..1e-8
+  // non-orthogonality on graded spectra, tools/csvd_study.py.)
   double fro2 = 0.0;
   for (int t = 0; t < r2; ++t) fro2 += s[t] * s[t];
   const double floor_v = 64.0 * std::sqrt(static_cast<double>(res.mg)) * 2.220446049250313e-16 *
                          std::sqrt(fro2);
-  std::vector<int> src(r, -1);
-  std::vector<GsRun> runs;
-  std::vector<double> sig(r);
+  P.src.assign(r, -1);
+  P.runs.clear();
+  P.sig.assign(r, 0.0);
   int q = 0;
   for (int t = 0; t < r2;) {
     int e = t + 1;
@@ -246,48 +256,64 @@ int svd_complex_device(Ctx& c, SvdWs& ws, const double* a, int m, int n, double*
       ++cnt;
     }
     if (q + cnt / 2 > r) fail(ACHI_E_NUMERICAL_FAILURE, "svd (complex): singular value pairing");
-    for (int k = 0; k < cnt / 2; ++k) sig[q + k] = s[t + 2 * k];
+    for (int k = 0; k < cnt / 2; ++k) P.sig[q + k] = s[t + 2 * k];
     if (cnt == 2)
-      src[q] = t;
+      P.src[q] = t;
     else
-      runs.push_back(GsRun{t, cnt, q});
+      P.runs.push_back(CsvdRun{t, cnt, q, cnt / 2});
     q += cnt / 2;
     t = e;
   }
   if (q != r) fail(ACHI_E_NUMERICAL_FAILURE, "svd (complex): singular value pairing");
-  DevArr<int> dsrc;
-  int* ps = dsrc.reserve(r);
-  ACHI_CUDA(cudaMemcpyAsync(ps, src.data(), sizeof(int) * r, cudaMemcpyHostToDevice, c.stream));
+  // (P.sig and P.src stay alive until the next stage 1, which synchronises first)
+  ACHI_CUDA(cudaMemcpyAsync(sigma, P.sig.data(), sizeof(double) * r, cudaMemcpyHostToDevice, c.stream));
+  ACHI_CUDA(cudaMemcpyAsync(P.src_d.reserve(r), P.src.data(), sizeof(int) * r, cudaMemcpyHostToDevice,
+                            c.stream));
+  return P.sweeps;
+}
+
+void svd_complex_stage2(Ctx& c, CsvdPlan& P, int k, double* U, double* Vd) {
+  const int m = P.m, n = P.n, r = P.r, r2 = P.r2;
+  k = std::max(0, std::min(k, r));
   double2* U2 = reinterpret_cast<double2*>(U);
   double2* V2 = reinterpret_cast<double2*>(Vd);
   {
-    const long tot = static_cast<long>(m) * r + static_cast<long>(r) * n;
+    const long tot = static_cast<long>(m) * k + static_cast<long>(k) * n;
     pick_kernel<<<std::max(1, std::min(cdiv(tot, 256), 8 * c.num_sms)), 256, 0, c.stream>>>(
-        UE.p, VTE.p, m, n, r2, ps, r, U2, V2);
+        P.UE.p, P.VTE.p, m, n, r2, P.src_d.p, r, k, U2, V2);
     ACHI_LAUNCHED(c);
   }
-  if (!runs.empty()) {
-    DevArr<GsRun> druns;
-    DevArr<int> dfail;
-    DevBuf cand;
-    GsRun* pr = druns.reserve(runs.size());
-    int* pf = dfail.reserve(1);
-    cand.reserve(2 * runs.size() * static_cast<size_t>(n + m));
-    ACHI_CUDA(cudaMemcpyAsync(pr, runs.data(), sizeof(GsRun) * runs.size(), cudaMemcpyHostToDevice, c.stream));
+  // only the runs that hold one of the first k values, each up to value k
+  P.runs_k.clear();
+  for (const CsvdRun& g : P.runs)
+    if (g.out < k) P.runs_k.push_back(CsvdRun{g.first, g.count, g.out, std::min(g.want, k - g.out)});
+  if (!P.runs_k.empty()) {
+    const size_t nr = P.runs_k.size();
+    CsvdRun* pr = P.runs_d.reserve(nr);
+    int* pf = P.fail_d.reserve(1);
+    P.cand.reserve(2 * nr * static_cast<size_t>(n + m));
+    ACHI_CUDA(cudaMemcpyAsync(pr, P.runs_k.data(), sizeof(CsvdRun) * nr, cudaMemcpyHostToDevice, c.stream));
     ACHI_CUDA(cudaMemsetAsync(pf, 0, sizeof(int), c.stream));
-    gs_kernel<<<static_cast<unsigned>(runs.size()), 256, 0, c.stream>>>(
-        UE.p, VTE.p, m, n, r2, pr, r, U2, V2, reinterpret_cast<double2*>(cand.p),
-        side == SvdSide::kRows ? 1 : 0, pf);
+    gs_kernel<<<static_cast<unsigned>(nr), 256, 0, c.stream>>>(
+        P.UE.p, P.VTE.p, m, n, r2, pr, r, U2, V2, reinterpret_cast<double2*>(P.cand.p), P.prim_u ? 1 : 0, pf);
     ACHI_LAUNCHED(c);
     int hf = 0;
     ACHI_CUDA(cudaMemcpyAsync(&hf, pf, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     if (hf) fail(ACHI_E_NUMERICAL_FAILURE, "svd (complex): multiplet basis");
   }
-  cphase_kernel<<<cdiv(r, 8), 256, 0, c.stream>>>(U2, V2, m, n, r);
-  ACHI_LAUNCHED(c);
-  ACHI_CUDA(cudaMemcpyAsync(sigma, sig.data(), sizeof(double) * r, cudaMemcpyHostToDevice, c.stream));
-  c.sync();  // the host vectors above (sig, src, runs) must outlive their copies
+  if (k > 0) {
+    cphase_kernel<<<cdiv(k, 8), 256, 0, c.stream>>>(U2, V2, m, n, r, k);
+    ACHI_LAUNCHED(c);
+  }
+}
+
+int svd_complex_device(Ctx& c, SvdWs& ws, const double* a, int m, int n, double* sigma, double* U,
+                       double* Vd, int side_pref, const double* v_init, double* v_keep) {
+  CsvdPlan P;
+  const int sweeps = svd_complex_stage1(c, ws, P, a, m, n, sigma, side_pref, v_init, v_keep);
+  svd_complex_stage2(c, P, P.r, U, Vd);
+  c.sync();  // the plan's host vectors must outlive their copies
   return sweeps;
 }
 

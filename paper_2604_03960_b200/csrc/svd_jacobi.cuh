@@ -10,6 +10,8 @@
 // and the phase convention of fix_phases is applied to the kept vectors.
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace achi {
@@ -90,7 +92,31 @@ void svd_gather(Ctx& ctx, SvdWs& ws, const SvdResultDev& r, int k, double* U, do
 // side_pref: -1 by shape; 0 = U, 1 = V^dagger orthonormal to working precision
 // across the whole spectrum (noise-level values included; the other factor's
 // vectors of such values are only defined up to their sigma weight).
+// Two-stage form for truncation (the complex chain): stage 1 decomposes, pairs the values and
+// writes sigma (r, device); stage 2 forms only the first k complex singular vectors (the
+// Gram-Schmidt of near-degenerate runs is the costly part, and only the kept vectors matter).
+struct CsvdRun {
+  int first, count;  // real members [first, first + count)
+  int out;           // first complex output index
+  int want;          // complex vectors to form (<= count / 2)
+};
+struct CsvdPlan {
+  DevBuf E, UE, VTE, cand;
+  DevArr<int> src_d, fail_d;
+  DevArr<CsvdRun> runs_d;
+  std::vector<double> s, sig;
+  std::vector<int> src;
+  std::vector<CsvdRun> runs, runs_k;
+  int m = 0, n = 0, r = 0, r2 = 0, sweeps = 0;
+  bool prim_u = true;
+};
+int svd_complex_stage1(Ctx& ctx, SvdWs& ws, CsvdPlan& plan, const double* a, int m, int n, double* sigma,
+                       int side_pref = -1, const double* v_init = nullptr, double* v_keep = nullptr);
+void svd_complex_stage2(Ctx& ctx, CsvdPlan& plan, int k, double* U, double* Vd);
+// v_init / v_keep (optional, svd_working_cols(2m, 2n, side)^2 doubles): warm start of the
+// realified decomposition and the buffer receiving its orthogonal factor (see svd_device).
 int svd_complex_device(Ctx& ctx, SvdWs& ws, const double* a, int m, int n, double* sigma, double* U,
-                       double* Vd, int side_pref = -1);
+                       double* Vd, int side_pref = -1, const double* v_init = nullptr,
+                       double* v_keep = nullptr);
 
 }  // namespace achi

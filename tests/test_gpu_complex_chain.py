@@ -142,3 +142,18 @@ def test_complex_sites_snapshot_and_reload(ctx, oracle, tmp_path):
     assert abs(r2["energy"] - e_last) <= 1e-10 * abs(e_last)
     with pytest.raises(Exception, match="UnsupportedModel"):
         ch.env(0, 1)
+
+
+def test_complex_chain_growing_chi_stays_variational(ctx):
+    """N=60 Heisenberg, PID chi_max=256, 8 sweeps in complex128 (the graph-mode Lanczos at
+    every bond while chi grows): sweep energies never rise and end on the real chain's.
+    Regression: a cached Lanczos graph once kept a pointer into the context's shared
+    reduction scratch, which a later, larger eigensolve reallocated (the graph then wrote
+    into freed memory and broke the orthonormality of a kept SVD factor)."""
+    spec = abi.model_spec(60, convention=abi.SPIN_HALF)
+    cfg = complex_cfg(abi.adaptive_config(256, 1e-10, max_sweeps=8, eps_conv=1e-16))
+    g = ctx.run_dmrg(spec, cfg)
+    e = g["energies"]
+    assert all(b <= a + 1e-10 * abs(a) for a, b in zip(e, e[1:])), e
+    r = ctx.run_dmrg(spec, abi.adaptive_config(256, 1e-10, max_sweeps=8, eps_conv=1e-16))
+    assert abs(e[-1] - r["energies"][-1]) <= 1e-10 * abs(r["energies"][-1])
