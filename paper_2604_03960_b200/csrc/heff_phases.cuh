@@ -108,6 +108,7 @@ __device__ __forceinline__ void load_mix(const DevMix& m, MixSmem& w) {
 // outputs only needs the tile itself.
 __device__ __forceinline__ int phase_a_blb(const HsArgs& a) { return HS_TM / a.D1; }
 constexpr int HS_JRB = 16;  // jr per phase-A tile (d = 2)
+constexpr int HS_SSTR = 20; // column stride of the s blocks in the staged tile (4 x 20 <= HS_LD)
 
 // A: Y[((bl,s'),e), jr] = sum_{(a,s)} W12[(s',e),(a,s)] sum_jl L[(bl,a),jl] theta[jl,(s,jr)]
 // The GEMM tile is staged in shared memory and mixed there (no X buffer).
@@ -183,33 +184,60 @@ __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const
     tile_mma<KM>(At, Bs, chl, acc);
     __syncthreads();
     pmark(1);
-    // stage the 32 x 64 tile (rows (bl, a), cols (s, q)) into As, then mix
-    tile_store(acc, As, HS_LD, 0, 0, HS_TM, HS_TN);
+    // stage the 32 x 64 tile (rows (bl, a), cols (s, q)) into As, then mix; the s blocks
+    // sit HS_SSTR apart so the mixing's fragment loads (4 s values x 8 q per warp
+    // request) hit every bank exactly twice
+    {
+      const int warp = t >> 5, lane = t & 31, gid = lane >> 2, tig = lane & 3;
+      const int mr = (warp >> 2) * 16 + gid, nc0 = (warp & 3) * 16;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int c = nc0 + q * 8 + 2 * tig, cs = (c / HS_JRB) * HS_SSTR + c % HS_JRB;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          As[(mr + 8 * h) * HS_LD + cs] = acc[q][2 * h];
+          As[(mr + 8 * h) * HS_LD + cs + 1] = acc[q][2 * h + 1];
+        }
+      }
+    }
     __syncthreads();
     if (dd * D3 <= HS_MIXD && D1 * dd <= HS_MIXD) {
-      // register-blocked mixing: thread (bll, q, half) loads the D1 dd inputs of its
-      // column once and forms half of the dd D3 outputs as dense dot products with
-      // the broadcast W12 rows (no per-term index chains)
+      // MPO mixing on the tensor cores: Y (njo x pairs) = W12 (njo x nin) . X (nin x pairs),
+      // X[(a, s)][(bll, q)] = As[(bll D1 + a) LD + s 16 + q] (the staged GEMM tile), one
+      // m16n8k4 DMMA chain of K = 20 per 16 x 8 output tile; warp w keeps the W12 rows of
+      // m-tile w & 1 in registers for all its tiles
       const int nin = D1 * dd, njo = dd * D3, pairs = blb * HS_JRB;
-      for (int u = t; u < 2 * pairs; u += HS_THREADS) {
-        const int pr = u % pairs, half = u / pairs;
-        const int bll = pr / HS_JRB, q = pr % HS_JRB;
-        const int bl = bl0 + bll, jr = jr0 + q;
-        if (bl >= chl || jr >= chr) continue;
-        double x[HS_MIXD];
+      const int warp = t >> 5, lane = t & 31, gid = lane >> 2, tig = lane & 3;
+      const int mt = warp & 1, tiles = 2 * (pairs / 8);
+      constexpr int KS = (HS_MIXD + 3) / 4;
+      double wa0[KS], wa1[KS];
 #pragma unroll
-        for (int i = 0; i < HS_MIXD; ++i) {
+      for (int ks = 0; ks < KS; ++ks) {
+        const int i = ks * 4 + tig, ja = mt * 16 + gid;
+        wa0[ks] = (ja < njo && i < nin) ? w.wd[ja * HS_MIXD + i] : 0.0;
+        wa1[ks] = (ja + 8 < njo && i < nin) ? w.wd[(ja + 8) * HS_MIXD + i] : 0.0;
+      }
+      for (int tile = warp; tile < tiles; tile += HS_THREADS / 32) {
+        const int nt = tile >> 1;
+        const int nb = nt * 8 + gid, bllb = nb / HS_JRB, qb = nb % HS_JRB;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int i = ks * 4 + tig;
           const int aa = i / dd, ss = i - aa * dd;
-          x[i] = i < nin ? As[(bll * D1 + aa) * HS_LD + ss * HS_JRB + q] : 0.0;
+          const double bv = i < nin ? As[(bllb * D1 + aa) * HS_LD + ss * HS_SSTR + qb] : 0.0;
+          mma16x8x4(acc, wa0[ks], wa1[ks], bv);
         }
-        const int j0 = half ? (njo + 1) / 2 : 0, j1 = half ? njo : (njo + 1) / 2;
-        double* yrow = a.X + (static_cast<long>(bl) * njo) * chr + jr;  // Y[(bl s') (e jr)], j = s' D3 + e
-        for (int j = j0; j < j1; ++j) {
-          const double* wj = w.wd + j * HS_MIXD;
-          double v = 0.0;
 #pragma unroll
-          for (int i = 0; i < HS_MIXD; ++i) v = fma(wj[i], x[i], v);
-          yrow[static_cast<long>(j) * chr] = v;
+        for (int h = 0; h < 2; ++h) {
+          const int j = mt * 16 + gid + 8 * h;
+          if (j >= njo) continue;
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int n2 = nt * 8 + 2 * tig + cc, bll = n2 / HS_JRB, q = n2 % HS_JRB;
+            const int bl = bl0 + bll, jr = jr0 + q;
+            if (bl < chl && jr < chr) a.X[(static_cast<long>(bl) * njo + j) * chr + jr] = acc[2 * h + cc];
+          }
         }
       }
       pmark(2);
@@ -226,7 +254,7 @@ __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const
       double v = 0.0;
       for (int p = w.wr[j]; p < w.wr[j + 1]; ++p) {
         const int in = w.wc[p], aa = in / dd, s = in - aa * dd;  // input (a, s)
-        v += w.wv[p] * As[(bll * D1 + aa) * HS_LD + s * HS_JRB + q];
+        v += w.wv[p] * As[(bll * D1 + aa) * HS_LD + s * HS_SSTR + q];
       }
       a.X[((static_cast<long>(bl) * dd + sp) * D3 + e) * chr + jr] = v;  // Y[(bl s') (e jr)]
     }
