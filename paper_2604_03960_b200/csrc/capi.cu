@@ -90,6 +90,9 @@ int achi_ctx_create(int device, achi_ctx** out) {
     ACHI_CUDA(cudaStreamCreateWithFlags(&ctx->c.aux, cudaStreamNonBlocking));
     ACHI_CUDA(cudaEventCreateWithFlags(&ctx->c.ev_fork, cudaEventDisableTiming));
     ACHI_CUDA(cudaEventCreateWithFlags(&ctx->c.ev_join, cudaEventDisableTiming));
+    ACHI_CUDA(cudaStreamCreateWithFlags(&ctx->c.vstream, cudaStreamNonBlocking));
+    ACHI_CUDA(cudaEventCreateWithFlags(&ctx->c.ev_v0, cudaEventDisableTiming));
+    ACHI_CUDA(cudaEventCreateWithFlags(&ctx->c.ev_v1, cudaEventDisableTiming));
     // keep freed pool memory cached (stream-ordered allocations, common.cuh)
     cudaMemPool_t pool;
     ACHI_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -114,8 +117,9 @@ int achi_ctx_set_grid_cap(achi_ctx* ctx, int max_ctas) {
 int achi_ctx_destroy(achi_ctx* ctx) {
   if (!ctx) return ACHI_OK;
   cudaSetDevice(ctx->c.device);
-  cudaStream_t s = ctx->c.stream, aux = ctx->c.aux;
-  cudaEvent_t e1 = ctx->c.ev_fork, e2 = ctx->c.ev_join;
+  cudaStream_t s = ctx->c.stream, aux = ctx->c.aux, vs = ctx->c.vstream;
+  cudaEvent_t e1 = ctx->c.ev_fork, e2 = ctx->c.ev_join, e3 = ctx->c.ev_v0, e4 = ctx->c.ev_v1;
+  cudaStreamSynchronize(vs);  // no V replay may outlive the buffers it writes
   {
     AllocStream as(s);
     delete ctx;
@@ -124,6 +128,9 @@ int achi_ctx_destroy(achi_ctx* ctx) {
   cudaStreamSynchronize(aux);
   cudaEventDestroy(e1);
   cudaEventDestroy(e2);
+  cudaEventDestroy(e3);
+  cudaEventDestroy(e4);
+  cudaStreamDestroy(vs);
   cudaStreamDestroy(aux);
   cudaStreamDestroy(s);
   return ACHI_OK;
@@ -221,6 +228,10 @@ int achi_chain_create(achi_ctx* ctx, const achi_model_spec* spec, const achi_dmr
 int achi_chain_destroy(achi_chain* chain) {
   if (chain) {
     AllocStream as(chain->ch.ctx->stream);
+    try {
+      svd_wait_v(*chain->ch.ctx, chain->ch.svd);  // its buffers are freed on the main stream
+    } catch (...) {
+    }
     delete chain;
   }
   return ACHI_OK;

@@ -282,6 +282,7 @@ void Chain::create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g) 
   if (init != ACHI_INIT_NEEL && init != ACHI_INIT_RANDOM_REAL && init != ACHI_INIT_RANDOM)
     fail(ACHI_E_INVALID_CONFIG, "dmrg: unknown initial state");
   cplx = g.arithmetic == ACHI_ARITH_COMPLEX || init == ACHI_INIT_RANDOM;
+  svd.defer_v = !cplx;  // the real visit joins the replay at svd_phase_signs
   const size_t planes = cplx ? 2 : 1;
   // mixing matrices
   std::vector<MixMatrix> all;
@@ -535,16 +536,6 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   }
   SvdResultDev sr = svd_device(c, svd, vec.p, sm_, sn_, smt, snt, side, 1, 0, nullptr, true,
                                warm ? vk.v.p : nullptr);
-  if (warm_svd) {  // keep this factor for the next visit of the bond in this direction
-    const size_t nv = static_cast<size_t>(sr.ng) * sr.ng;
-    vk.v.reserve(nv);
-    ACHI_CUDA(cudaMemcpyAsync(vk.v.p, sr.V, sizeof(double) * nv, cudaMemcpyDeviceToDevice, c.stream));
-    vk.m = sm_;
-    vk.n = sn_;
-    vk.mt = smt;
-    vk.nt = snt;
-    vk.valid = true;
-  }
   c.acc.end(c.stream, 0.0);
   // the fused bond selection is queued behind the SVD; one host sync serves both
   bond_select(c, sr.sigma, sr.r_true, cfg, states.p, b, sweep_index, right ? 1 : 0,
@@ -595,7 +586,17 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   if (bo.err) fail(bo.err, "controller_update: invalid controller state or config");
   const int kept = bo.kept;
   if (!(bo.lam_norm > 0)) fail(ACHI_E_DEGENERATE_SPECTRUM, "dmrg: empty truncation");
-  svd_phase_signs(c, svd, sr, kept);
+  svd_phase_signs(c, svd, sr, kept);  // (joins the V replay, which ran beside the bond selection)
+  if (warm_svd) {  // keep this factor for the next visit of the bond in this direction
+    const size_t nv = static_cast<size_t>(sr.ng) * sr.ng;
+    vk.v.reserve(nv);
+    ACHI_CUDA(cudaMemcpyAsync(vk.v.p, sr.V, sizeof(double) * nv, cudaMemcpyDeviceToDevice, c.stream));
+    vk.m = sm_;
+    vk.n = sn_;
+    vk.mt = smt;
+    vk.nt = snt;
+    vk.valid = true;
+  }
   absorb(c, sr, svd.sign.p, kept, bout.p, chl, chr, d, right, site[b].p, site[b + 1].p);
   chi[b + 1] = kept;
   const int kp = pad2i(kept);

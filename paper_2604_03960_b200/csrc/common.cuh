@@ -244,6 +244,9 @@ struct Ctx {
   // tridiagonal step runs beside the next matvec)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // side stream of the cluster SVD's V replay (svd_jacobi.cu, SvdWs::defer_v)
+  cudaStream_t vstream = nullptr;
+  cudaEvent_t ev_v0 = nullptr, ev_v1 = nullptr;
   DevBuf flush;
   void sync() { ACHI_CUDA(cudaStreamSynchronize(stream)); }
 };

@@ -215,6 +215,7 @@ int svd_complex_stage1(Ctx& c, SvdWs& ws, CsvdPlan& P, const double* a, int m, i
                                      : (side_pref == 0 ? SvdSide::kRows : SvdSide::kCols);
   P.prim_u = side == SvdSide::kRows;
   SvdResultDev res = svd_device(c, ws, P.E.p, m2, n2, m2, n2, side, 1, 0, nullptr, true, v_init);
+  svd_wait_v(c, ws);
   if (v_keep)  // the real factor of E, a warm start for the next decomposition of this shape
     ACHI_CUDA(cudaMemcpyAsync(v_keep, res.V, sizeof(double) * res.ng * res.ng, cudaMemcpyDeviceToDevice,
                               c.stream));

@@ -974,6 +974,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
                         int n_true, SvdSide side, int batch, long bstride, double* sigma_out,
                         bool want_vectors, const double* v_init) {
   if (v_init && (batch != 1 || !want_vectors)) fail(ACHI_E_INTERNAL, "svd: warm start needs batch 1 with vectors");
+  svd_wait_v(ctx, ws);  // a deferred replay of the previous call still writes ws.V
   // ACHI_SVD_TRACE (study): synchronise after each stage and print the stage
   // times of calls slower than 4 ms
   static const char* trace_env = std::getenv("ACHI_SVD_TRACE");  // value: print threshold in ms
@@ -1177,9 +1178,19 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
         return 1;
       });
       dim3 grid(cdiv(ng, RP_ROWS), batch);
-      v_replay_kernel<<<grid, JT, rs, ctx.stream>>>(V, vstride, ng, nb, npairs, jrec, jflag, jstride,
-                                                    sweeps_dev, v_init);
+      const bool defer = ws.defer_v && ctx.vstream;
+      cudaStream_t vs = defer ? ctx.vstream : ctx.stream;
+      if (defer) {
+        ACHI_CUDA(cudaEventRecord(ctx.ev_v0, ctx.stream));
+        ACHI_CUDA(cudaStreamWaitEvent(vs, ctx.ev_v0, 0));
+      }
+      v_replay_kernel<<<grid, JT, rs, vs>>>(V, vstride, ng, nb, npairs, jrec, jflag, jstride,
+                                            sweeps_dev, v_init);
       ACHI_LAUNCHED(ctx);
+      if (defer) {
+        ACHI_CUDA(cudaEventRecord(ctx.ev_v1, vs));
+        ws.v_pending = true;
+      }
       mark("replay");
     }
   } else {
@@ -1296,6 +1307,12 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   return r;
 }
 
+void svd_wait_v(Ctx& ctx, SvdWs& ws) {
+  if (!ws.v_pending) return;
+  ACHI_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_v1, 0));
+  ws.v_pending = false;
+}
+
 int SvdResultDev::sweeps() const {
   int s = 0;
   for (int i = 0; i < n_launches; ++i) s = std::max(s, sweeps_host[i]);
@@ -1304,6 +1321,7 @@ int SvdResultDev::sweeps() const {
 }
 
 void svd_phase_signs(Ctx& ctx, SvdWs& ws, const SvdResultDev& r, int kept) {
+  svd_wait_v(ctx, ws);
   double* sign = ws.sign.reserve(static_cast<size_t>(std::max(kept, 1)));
   if (kept <= 0) return;
   const bool rows = r.side == SvdSide::kRows;
@@ -1315,6 +1333,7 @@ void svd_phase_signs(Ctx& ctx, SvdWs& ws, const SvdResultDev& r, int kept) {
 }
 
 void svd_gather(Ctx& ctx, SvdWs& ws, const SvdResultDev& r, int k, double* U, double* VT) {
+  svd_wait_v(ctx, ws);
   const long tot = static_cast<long>(r.m_true) * k + static_cast<long>(k) * r.n_true;
   const int blocks = static_cast<int>(std::min<long>(cdiv(tot, 256), 4L * ctx.num_sms));
   gather_kernel<<<blocks, 256, 0, ctx.stream>>>(r.G, r.mg, r.V, r.ng, r.sigma, r.perm, ws.sign.p, k,

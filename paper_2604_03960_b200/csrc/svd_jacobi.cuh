@@ -28,7 +28,14 @@ struct SvdWs {
   DevArr<unsigned> pcnt;        // stream mode, row split: per-pair arrival counters
   DevArr<int> sweeps;
   PinnedArr<int> sweeps_host;
+  // defer_v (set by the chain): the cluster path's V replay runs on ctx.vstream
+  // beside the caller's next steps (norms, sort, bond selection, the host round
+  // trip); svd_wait_v joins it before V is read (svd_phase_signs and svd_gather
+  // call it themselves)
+  bool defer_v = false, v_pending = false;
 };
+
+void svd_wait_v(Ctx& ctx, SvdWs& ws);
 
 // Orientation: kRows -> columns of G are the rows of theta (G = theta^T, V
 // accumulates the left singular vectors U); kCols -> columns of G are the
