@@ -83,11 +83,13 @@ class Context:
         return ms.value
 
     def device_times(self, enable=None, reset=False):
-        """Per-phase CUDA-event device time: dict phase -> (ms, work, launches)."""
+        """Per-phase CUDA-event device time: dict phase -> (ms, work, launches).
+        enable: None (unchanged), False / True, or n > 1: a chain times one bond visit in n
+        (timing events cost device time; the totals then cover the sampled visits)."""
         names = ("matvec", "svd", "env", "heff")
         n = len(names)
         out = np.zeros(3 * n)
-        e = -1 if enable is None else int(bool(enable))
+        e = -1 if enable is None else int(enable)
         self._check(self.lib.achi_device_times_ex(self.h, e, int(bool(reset)), _dp(out), n))
         return {k: dict(ms=out[i], work=out[n + i], launches=int(out[2 * n + i]))
                 for i, k in enumerate(names)}

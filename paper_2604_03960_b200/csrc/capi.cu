@@ -210,7 +210,11 @@ int achi_device_times_ex(achi_ctx* ctx, int enable, int reset, double* out, int 
       }
     if (reset)
       for (int t = 0; t < EventAcc::kNumTags; ++t) a.ms[t] = a.work[t] = 0, a.count[t] = 0;
-    if (enable >= 0) a.enabled = enable != 0;
+    if (enable >= 0) {
+      a.enabled = enable != 0;
+      a.sample = std::max(1, enable);  // enable = n > 1: time one chain visit in n
+      a.visit_seq = 0;
+    }
   });
 }
 

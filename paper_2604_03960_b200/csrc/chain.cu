@@ -479,11 +479,12 @@ void Chain::rebuild_envs() {  // Environment::rebuild(psi, mpo, 0), dmrg.cpp:51-
 
 // visit_bond (dmrg.cpp:84-171)
 void Chain::visit(int b, bool right, int sweep_index, int slot) {
+  Ctx& c = *ctx;
+  EventAccPause untimed(c.acc, c.acc.enabled && !c.acc.visit_timed());
   if (cplx) {
     visit_complex(b, right, sweep_index, slot);
     return;
   }
-  Ctx& c = *ctx;
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
   const int chl = chi[b], chm = chi[b + 1], chr = chi[b + 2];
@@ -542,7 +543,6 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
               trace.p + slot, visits.p + slot, bout.p);
   ACHI_CUDA(cudaMemcpyAsync(bout_h.p, bout.p, sizeof(BondOut), cudaMemcpyDeviceToHost, c.stream));
   c.sync();  // the one host wait of the visit: eigensolve outcome, SVD sweeps, kept rank
-  c.acc.resolve();
   const EigsOut eig = eigs_finish(c, lz);  // throws EigenNonConvergence / InvalidMatrix
   if (c.acc.enabled) c.acc.work[EventAcc::kMatvec] += eig.matvecs * mv_flops;
   auto write_dump = [&] {

@@ -341,7 +341,6 @@ void Chain::visit_complex(int b, bool right, int sweep_index, int slot) {
               visits.p + slot, bout.p);
   ACHI_CUDA(cudaMemcpyAsync(bout_h.p, bout.p, sizeof(BondOut), cudaMemcpyDeviceToHost, c.stream));
   c.sync();
-  c.acc.resolve();
   const EigsOut eig = eigs_finish(c, lz);
   if (c.acc.enabled) c.acc.work[EventAcc::kMatvec] += eig.matvecs * mv_flops;
   const auto t2 = clk::now();

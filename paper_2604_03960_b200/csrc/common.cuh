@@ -147,7 +147,8 @@ struct LanczosStatus {
 };
 
 // Device-time accounting: event pairs recorded on the context stream around a
-// phase, resolved (after a sync the caller already pays) into per-tag totals.
+// phase, resolved into per-tag totals after a sync the caller already pays (the
+// chain resolves once per sweep: the per-visit host cost is the records alone).
 // Phases nest (kHeff, the H_eff applications, sits inside kMatvec, the whole
 // eigensolve); nothing is recorded while the stream is being captured.
 struct EventAcc {
@@ -161,6 +162,12 @@ struct EventAcc {
   double work[kNumTags] = {0, 0, 0, 0};  // algorithmic flops or bytes
   long count[kNumTags] = {0, 0, 0, 0};
   bool enabled = false;
+  bool in_capture = false;  // set by the Lanczos graph builder while ctx.stream is captured
+  // timing events cost device time (~4 us per bond visit at C3): a chain times one
+  // visit in `sample` (rotating over the bonds when sample is coprime with 2(N-1))
+  int sample = 1;
+  long visit_seq = 0;
+  bool visit_timed() { return enabled && (visit_seq++ % sample) == 0; }
   cudaEvent_t next() {
     if (used == pool.size()) {
       cudaEvent_t e;
@@ -169,14 +176,9 @@ struct EventAcc {
     }
     return pool[used++];
   }
-  static bool capturing(cudaStream_t s) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(s, &cs);
-    return cs != cudaStreamCaptureStatusNone;
-  }
   void begin(int tag, cudaStream_t s) {
     if (!enabled) return;
-    if (capturing(s)) {
+    if (in_capture) {
       stack.emplace_back(tag, -1);
       return;
     }
@@ -207,6 +209,16 @@ struct EventAcc {
   ~EventAcc() {
     for (auto e : pool) cudaEventDestroy(e);
   }
+};
+
+// suspends the accounting for one untimed visit
+struct EventAccPause {
+  EventAcc& a;
+  bool prev;
+  EventAccPause(EventAcc& acc, bool pause) : a(acc), prev(acc.enabled) {
+    if (pause) a.enabled = false;
+  }
+  ~EventAccPause() { a.enabled = prev; }
 };
 
 struct Ctx {

@@ -1720,6 +1720,7 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
     auto begin = [&](cudaGraph_t g, const cudaGraphNode_t* deps, size_t nd) {
       ACHI_CUDA(cudaStreamBeginCaptureToGraph(ctx.stream, g, deps, nullptr, nd,
                                               cudaStreamCaptureModeRelaxed));
+      ctx.acc.in_capture = true;
     };
     auto finish = [&](bool want_leaves) {
       if (want_leaves) {
@@ -1730,6 +1731,7 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
         leaves.assign(deps, deps + nd);
       }
       cudaGraph_t captured;
+      ctx.acc.in_capture = false;
       ACHI_CUDA(cudaStreamEndCapture(ctx.stream, &captured));
     };
     auto add_while = [&](cudaGraph_t parent, cudaGraphConditionalHandle h) {
@@ -1823,6 +1825,7 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
       cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
       cudaStreamIsCapturing(ctx.stream, &cs);
       if (cs != cudaStreamCaptureStatusNone) cudaStreamEndCapture(ctx.stream, &dummy);
+      ctx.acc.in_capture = false;
       cudaGetLastError();
       lg.reset();
       if (old_exec) cudaGraphExecDestroy(old_exec);
