@@ -46,8 +46,8 @@ __device__ int bs_max_int(int v, int* sh) {
 }
 
 // dynamic smem: suf[r + 1] (suffix sums of sigma^2), seg[BS_THREADS]
-__global__ void __launch_bounds__(BS_THREADS) bond_select_kernel(
-    const double* __restrict__ sigma, int r, achi_dmrg_config cfg, achi_bond_state* states, int bond,
+__device__ __forceinline__ void bond_select_body(
+    const double* __restrict__ sigma, int r, const achi_dmrg_config& cfg, achi_bond_state* states, int bond,
     int sweep, int moving_right, achi_trace_row* trace, achi_visit_record* visit, BondOut* out) {
   extern __shared__ double dyn[];
   double* suf = dyn;                 // r + 1
@@ -185,6 +185,16 @@ __global__ void __launch_bounds__(BS_THREADS) bond_select_kernel(
   }
 }
 
+// out_host (optional, pinned): the record for the host, written by the kernel
+// itself (no separate device-to-host copy on the stream)
+__global__ void __launch_bounds__(BS_THREADS) bond_select_kernel(
+    const double* __restrict__ sigma, int r, achi_dmrg_config cfg, achi_bond_state* states, int bond,
+    int sweep, int moving_right, achi_trace_row* trace, achi_visit_record* visit, BondOut* out,
+    BondOut* out_host) {
+  bond_select_body(sigma, r, cfg, states, bond, sweep, moving_right, trace, visit, out);
+  if (out_host && threadIdx.x == 0) *out_host = *out;  // thread 0 wrote every field of *out
+}
+
 // Standalone spectrum reductions (entropy, truncation error at `kept`,
 // discarded-weight floor rank, significant count) with the same deterministic
 // orders as bond_select_kernel.  out[4]; *err = ACHI_E_* or 0.
@@ -310,7 +320,8 @@ __global__ void absorb_kernel(AbsorbArgs a) {
 
 void bond_select(Ctx& ctx, const double* sigma, int r, const achi_dmrg_config& cfg,
                  achi_bond_state* states, int bond, int sweep, int moving_right,
-                 achi_trace_row* trace_slot, achi_visit_record* visit_slot, BondOut* out) {
+                 achi_trace_row* trace_slot, achi_visit_record* visit_slot, BondOut* out,
+                 BondOut* out_host) {
   const size_t smem = sizeof(double) * (static_cast<size_t>(r) + 1 + BS_THREADS);
   per_device_once("bond_select_kernel", ctx.device, [] {
     ACHI_CUDA(cudaFuncSetAttribute(bond_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -319,7 +330,8 @@ void bond_select(Ctx& ctx, const double* sigma, int r, const achi_dmrg_config& c
   });
   if (smem > 200 * 1024) fail(ACHI_E_SIZE_GUARD, "bond_select: spectrum too long");
   bond_select_kernel<<<1, BS_THREADS, smem, ctx.stream>>>(sigma, r, cfg, states, bond, sweep,
-                                                          moving_right, trace_slot, visit_slot, out);
+                                                          moving_right, trace_slot, visit_slot, out,
+                                                          out_host);
   ACHI_LAUNCHED(ctx);
 }
 

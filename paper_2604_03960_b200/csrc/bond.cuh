@@ -16,9 +16,11 @@ struct BondOut {
 
 // One CTA; sigma (device, r values, non-increasing).  Updates states[bond],
 // writes trace[slot]/visit[slot] (either may be null) and *out.
+// out_host (optional, pinned host memory): *out is also written there by the kernel.
 void bond_select(Ctx& ctx, const double* sigma, int r, const achi_dmrg_config& cfg,
                  achi_bond_state* states, int bond, int sweep, int moving_right,
-                 achi_trace_row* trace_slot, achi_visit_record* visit_slot, BondOut* out);
+                 achi_trace_row* trace_slot, achi_visit_record* visit_slot, BondOut* out,
+                 BondOut* out_host = nullptr);
 
 // entropy / truncation error / floor rank / significant count of one spectrum
 void spectrum_stats(Ctx& ctx, const double* sigma, int r, int kept, double eps, double* out,

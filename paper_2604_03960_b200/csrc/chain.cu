@@ -540,8 +540,7 @@ void Chain::visit(int b, bool right, int sweep_index, int slot) {
   c.acc.end(c.stream, 0.0);
   // the fused bond selection is queued behind the SVD; one host sync serves both
   bond_select(c, sr.sigma, sr.r_true, cfg, states.p, b, sweep_index, right ? 1 : 0,
-              trace.p + slot, visits.p + slot, bout.p);
-  ACHI_CUDA(cudaMemcpyAsync(bout_h.p, bout.p, sizeof(BondOut), cudaMemcpyDeviceToHost, c.stream));
+              trace.p + slot, visits.p + slot, bout.p, bout_h.p);
   c.sync();  // the one host wait of the visit: eigensolve outcome, SVD sweeps, kept rank
   const EigsOut eig = eigs_finish(c, lz);  // throws EigenNonConvergence / InvalidMatrix
   if (c.acc.enabled) c.acc.work[EventAcc::kMatvec] += eig.matvecs * mv_flops;

@@ -338,8 +338,7 @@ void Chain::visit_complex(int b, bool right, int sweep_index, int slot) {
   }
   c.acc.end(c.stream, 0.0);
   bond_select(c, csig.p, rk, cfg, states.p, b, sweep_index, right ? 1 : 0, trace.p + slot,
-              visits.p + slot, bout.p);
-  ACHI_CUDA(cudaMemcpyAsync(bout_h.p, bout.p, sizeof(BondOut), cudaMemcpyDeviceToHost, c.stream));
+              visits.p + slot, bout.p, bout_h.p);
   c.sync();
   const EigsOut eig = eigs_finish(c, lz);
   if (c.acc.enabled) c.acc.work[EventAcc::kMatvec] += eig.matvecs * mv_flops;

@@ -852,6 +852,7 @@ struct PzArgs {
   int block, max_iter;
   int W;                 // worker CTAs; CTA W is the tridiagonal CTA
   unsigned long long* prof;  // optional clock64 phase totals of worker 0 (ACHI_LANCZOS_PROF)
+  LanczosResult* res_host;   // pinned: the outcome for the host, written by the kernel itself
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -1128,6 +1129,8 @@ __global__ void __launch_bounds__(PZ_THREADS) lanczos_persistent_kernel(PzArgs a
         a.st->bnorm = __ldcg(tr + 2);
         a.st->alpha = __ldcg(tr + 3);
       }
+      a.res_host->ctl = c;
+      a.res_host->st = *a.st;
     }
     post(-1, 0);  // release the tridiagonal CTA
   };
@@ -1667,7 +1670,7 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
               pzd + 130L * W, pzd + 130L * W + 128, pzi, pzi + 2,
               reinterpret_cast<unsigned*>(pzi + 6), reinterpret_cast<unsigned*>(pzi + 7),
               reinterpret_cast<unsigned*>(pzi + 8), ws.ctl.p, K.dev_status(), tol, block, max_iter, W,
-              prof_on ? prof_buf.p : nullptr};
+              prof_on ? prof_buf.p : nullptr, ws.res_h.p};
     if (prof_on && prof_calls % 200 == 0) {
       static PinnedArr<unsigned long long> ph;
       ph.reserve(16);
@@ -1686,11 +1689,7 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
     ACHI_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lanczos_persistent_kernel), dim3(W + 1),
                                           dim3(PZ_THREADS), kargs, smem, ctx.stream));
     ACHI_LAUNCHED(ctx);
-    ws.pend_graph = false;
-    LanczosResult* R = ws.res_h.p;
-    ACHI_CUDA(cudaMemcpyAsync(&R->ctl, ws.ctl.p, sizeof(LanczosCtl), cudaMemcpyDeviceToHost, ctx.stream));
-    ACHI_CUDA(cudaMemcpyAsync(&R->st, K.dev_status(), sizeof(LanczosStatus), cudaMemcpyDeviceToHost,
-                              ctx.stream));
+    ws.pend_graph = false;  // (the kernel writes ws.res_h itself: no copies on the stream)
     return;
   }
 

@@ -314,6 +314,7 @@ struct ClArgs {
   long jstride;            // rounds capacity per batch item (MAX_SWEEPS*(nb-1))
   int* sweeps_out;         // [batch]
   long long* prof;         // optional clock64 phase accounting (cluster 0, CTA 0)
+  int* sweeps_host_out;    // [batch], pinned host memory (the host reads it after its sync)
 };
 
 // acc (16x8 tile per warp of the 32x32 Gram) over rows [0, rows) of X
@@ -478,7 +479,10 @@ __global__ void __launch_bounds__(JT, 1) jacobi_cluster_kernel(ClArgs a) {
     const int col = c < JB ? ba * JB + c : bb * JB + c - JB;
     if (r < a.ldg) G[col * a.ldg + r] = X[c * cld + r];
   }
-  if (p == 0 && threadIdx.x == 0) a.sweeps_out[b] = sweep;
+  if (p == 0 && threadIdx.x == 0) {
+    a.sweeps_out[b] = sweep;
+    a.sweeps_host_out[b] = sweep;
+  }
 }
 
 // V (ng x ng col-major, ld ng) = I * prod over recorded rounds of the block
@@ -591,6 +595,7 @@ struct PersArgs {
   const double* zero2;
   unsigned long long* conv;  // [MAX_SWEEPS] per-sweep max measure (whole launch)
   int* sweeps_out;
+  int* sweeps_host_out;      // pinned host copy of *sweeps_out
   int rsplit;                // CTAs per block pair, each streaming a slice of the rows
   double* gpart;             // [pairs in launch][rsplit][32*32] partial Grams (rsplit > 1)
   unsigned* pcnt;            // [pairs in launch] arrival counters (zeroed per launch)
@@ -807,7 +812,10 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
       break;
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *a.sweeps_out = sweep;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *a.sweeps_out = sweep;
+    *a.sweeps_host_out = sweep;
+  }
 }
 
 // ---- setup / finalisation kernels ----
@@ -1135,7 +1143,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
       return e ? std::atof(e) : 0.0;
     }();
     ClArgs a{G, ldg, gstride, mg, rows_pad, nb, npairs, max_inner, tol, stop_tol, zero2, cross_mode,
-             skip_tol, jrec, jflag, jstride, sweeps_dev, nullptr};
+             skip_tol, jrec, jflag, jstride, sweeps_dev, nullptr, sweeps_host};
     static const bool prof_on = std::getenv("ACHI_JACOBI_PROF") != nullptr;
     static DevArr<long long> profbuf;
     if (prof_on) {
@@ -1248,7 +1256,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
       if (pcnt) ACHI_CUDA(cudaMemsetAsync(pcnt, 0, sizeof(unsigned) * npairs * nbat, ctx.stream));
       PersArgs a{G, ldg, gstride, mg, V, ng, vstride, ng, nb, npairs, b0,
                  max_inner, tol, stop_tol, zero2, conv, sweeps_dev + (launches % nsw),
-                 rsplit, gpart, pcnt, stream_cross};
+                 sweeps_host + (launches % nsw), rsplit, gpart, pcnt, stream_cross};
       void* args[] = {&a};
       ACHI_CUDA(cudaLaunchCooperativeKernel(kern, dim3(npairs * nbat * rsplit), dim3(JT), args, smem,
                                             ctx.stream));
@@ -1272,8 +1280,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     sort_kernel<<<batch, 1024, sort_smem, ctx.stream>>>(sig, ng, ng, sorted, perm);
     ACHI_LAUNCHED(ctx);
   }
-  ACHI_CUDA(cudaMemcpyAsync(sweeps_host, sweeps_dev, sizeof(int) * launches, cudaMemcpyDeviceToHost,
-                            ctx.stream));
+  // (the Jacobi kernels write their sweep counts into sweeps_host themselves)
   mark("norms+sort");
   if (trace) {
     double tot = 0;
