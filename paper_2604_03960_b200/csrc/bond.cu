@@ -71,8 +71,11 @@ __device__ __forceinline__ void bond_select_body(
   seg[threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double run = 0.0;  // exclusive suffix over later segments, fixed order
-    for (int t = BS_THREADS - 1; t >= 0; --t) {
+    // exclusive suffix over later segments, fixed order; only the first nseg threads
+    // hold values (the others added exact zeros: skipping them changes no bit)
+    const int nseg = (r + per - 1) / per;
+    double run = 0.0;
+    for (int t = nseg - 1; t >= 0; --t) {
       const double v = seg[t];
       seg[t] = run;
       run += v;
@@ -222,7 +225,7 @@ __global__ void __launch_bounds__(BS_THREADS) spectrum_stats_kernel(const double
   __syncthreads();
   if (threadIdx.x == 0) {
     double run = 0.0;
-    for (int t = BS_THREADS - 1; t >= 0; --t) {
+    for (int t = (r + per - 1) / per - 1; t >= 0; --t) {  // (segments past r hold zeros)
       const double v = seg[t];
       seg[t] = run;
       run += v;

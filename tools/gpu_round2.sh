@@ -24,7 +24,7 @@ python tools/ncu_summary.py $O/launches_prod.csv > $O/launches_prod_summary.txt 
 # full captures
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:lanczos_persistent -s 2400 -c 1 \
   -o $O/full_lanczos_persistent_kernel python tools/ncu_c3.py 14 > $O/ncu_pz.log 2>&1; echo "full pz rc=$?" >> $O/status.txt
-for K in jacobi_cluster_kernel:1200 v_replay_kernel:1200 qr_precond_kernel:100 bond_select_kernel:2000; do
+for K in jacobi_cluster_kernel:1200 v_replay_kernel:1200 qr_precond_kernel:100 bond_select_kernel:1000; do
   name=${K%%:*}; skip=${K##*:}
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:$name -s $skip -c 2 \
     -o $O/full_$name python tools/ncu_c3.py 9 > $O/ncu_$name.log 2>&1
