@@ -119,7 +119,7 @@ template <int KM>
 __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const double* theta,
                                         double* As, double* Bs, int blk, int nblk,
                                         unsigned long long* prof = nullptr, double* Lc = nullptr,
-                                        bool lfill = false) {
+                                        bool lfill = false, double tscale = 1.0) {
   // prof (optional, thread 0 of the caller's CTA): cycles in [0] loads, [1] MMA, [2] mixing
   const bool pf = prof && threadIdx.x == 0;
   unsigned long long pt = pf ? clock64() : 0;
@@ -169,7 +169,7 @@ __device__ __forceinline__ void phase_a(const HsArgs& a, const MixSmem& w, const
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
           const int k = kq + 4 * (32 * h + u);
-          v[u] = (ok && k < chl) ? theta[static_cast<long>(k) * N1 + s * chr + jr] : 0.0;
+          v[u] = (ok && k < chl) ? theta[static_cast<long>(k) * N1 + s * chr + jr] * tscale : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 32; ++u) {

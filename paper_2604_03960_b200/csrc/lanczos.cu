@@ -853,6 +853,7 @@ struct PzArgs {
   int W;                 // worker CTAs; CTA W is the tridiagonal CTA
   unsigned long long* prof;  // optional clock64 phase totals of worker 0 (ACHI_LANCZOS_PROF)
   LanczosResult* res_host;   // pinned: the outcome for the host, written by the kernel itself
+  int lazy;                  // next matvec from w'/beta (see the step loop), no q_{j+1} barrier
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -1157,6 +1158,7 @@ __global__ void __launch_bounds__(PZ_THREADS) lanczos_persistent_kernel(PzArgs a
     const int mv0 = matvecs;
     int j = 0, k = 0;
     unsigned seq_last = 0;  // job of the final step
+    double inv_prev = 1.0;  // 1 / beta_{j-1} (lazy matvec input)
     for (;; ++j) {
       // ---- step j: w = H q_j, orthogonalise, q_{j+1} ----
       const bool pf = a.prof && rank == 0 && threadIdx.x == 0;
@@ -1168,8 +1170,14 @@ __global__ void __launch_bounds__(PZ_THREADS) lanczos_persistent_kernel(PzArgs a
           t0 = t1;
         }
       };
-      hs::phase_a<hs::HS_KMAX>(h, mw, a.Q + j * a.stride, As, Bs, rank, a.W, pf ? a.prof + 12 : nullptr, Lc,
-                               cfill);
+      // lazy: the matvec input of step j >= 1 is w'/beta_{j-1} (w' = w after the first
+      // projection, complete since the previous step's last barrier) instead of the stored
+      // q_j = (w' - Q c2) / beta_{j-1}; they differ by the second projection (rounding-level
+      // components along the basis, which the full reorthogonalisation removes from the
+      // next w anyway), and q_j itself is written by each worker into its own slice of Q
+      const bool from_w = a.lazy && j > 0;
+      hs::phase_a<hs::HS_KMAX>(h, mw, from_w ? a.w : a.Q + j * a.stride, As, Bs, rank, a.W,
+                               pf ? a.prof + 12 : nullptr, Lc, cfill, from_w ? inv_prev : 1.0);
       mark(0);
       pz_sync(a, gen);
       mark(1);
@@ -1214,9 +1222,10 @@ __global__ void __launch_bounds__(PZ_THREADS) lanczos_persistent_kernel(PzArgs a
       const double wn2 = coef[nv];
       const bool pyth = h2sq <= 0.25 * wn2;
       double nrm = 0.0;
+      double* w2 = a.lazy ? a.tmp : a.w;  // lazy: w' stays in w for the next matvec
       for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) {
         const double v = project_out(a.Q, a.stride, nv, coef, a.w[x], x);
-        a.w[x] = v;
+        w2[x] = v;
         nrm += v * v;
       }
       double bn;
@@ -1228,10 +1237,11 @@ __global__ void __launch_bounds__(PZ_THREADS) lanczos_persistent_kernel(PzArgs a
       } else {
         bn = sqrt(fmax(wn2 - h2sq, 0.0));
       }
+      inv_prev = bn > 0 ? 1.0 / bn : 0.0;
       if (j + 1 <= LANCZOS_BLOCK && bn > 0) {
         const double inv = 1.0 / bn;
         double* qn = a.Q + (j + 1) * a.stride;
-        for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) qn[x] = a.w[x] * inv;
+        for (long x = b0 + threadIdx.x; x < b1; x += PZ_THREADS) qn[x] = w2[x] * inv;
       }
       if (rank == 0 && threadIdx.x == 0) {
         a.alpha[j] = alpha_j;
@@ -1241,7 +1251,8 @@ __global__ void __launch_bounds__(PZ_THREADS) lanczos_persistent_kernel(PzArgs a
       mark(8);
       post(j, mv0);
       const unsigned seq_j = seq;
-      pz_sync(a, gen);  // q_{j+1} complete
+      if (!a.lazy) pz_sync(a, gen);  // q_{j+1} complete (lazy: w' was, at the last barrier)
+      else __syncthreads();
       mark(9);
       ++steps;
       // the decision of step j-1 (posted one step ago)
@@ -1662,6 +1673,10 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
     }();
     const int W = static_cast<int>(std::max<long>(1, std::min<long>(
         std::max<long>(pz_items, cdiv(n, static_cast<long>(pz_elems) * PZ_THREADS)), ctx.cap_grid(maxres) - 1)));
+    static const int pz_lazy = [] {  // ACHI_PZ_LAZY=0: the stored q_j as matvec input (+1 barrier)
+      const char* e = std::getenv("ACHI_PZ_LAZY");
+      return e ? std::atoi(e) : 1;
+    }();
     double* pzd = ws.pzd.reserve(static_cast<size_t>(130) * W + 256);
     int* pzi = ws.pzi.reserve(16);
     ACHI_CUDA(cudaMemsetAsync(pzi, 0, 16 * sizeof(int), ctx.stream));
@@ -1670,7 +1685,7 @@ void eigs_lowest_async(Ctx& ctx, LanczosWs& ws, const ApplyFn& apply, long n, lo
               pzd + 130L * W, pzd + 130L * W + 128, pzi, pzi + 2,
               reinterpret_cast<unsigned*>(pzi + 6), reinterpret_cast<unsigned*>(pzi + 7),
               reinterpret_cast<unsigned*>(pzi + 8), ws.ctl.p, K.dev_status(), tol, block, max_iter, W,
-              prof_on ? prof_buf.p : nullptr, ws.res_h.p};
+              prof_on ? prof_buf.p : nullptr, ws.res_h.p, pz_lazy};
     if (prof_on && prof_calls % 200 == 0) {
       static PinnedArr<unsigned long long> ph;
       ph.reserve(16);
