@@ -16,7 +16,12 @@ reported as "svd_chi2048_ms".
 --impl reference times the reference algorithm on the host cores (the C++
 oracle port of /root/reference/proj in complex128, all threads) on the same
 workload.  Multi-GPU: a single chain does not shard (a sweep is sequential,
-dmrg.cpp:156-163), so N GPUs run N independent replicas ("replicas only").
+dmrg.cpp:156-163), so N GPUs run N independent replicas ("replicas only");
+the naturally sharded workloads run beside it at every N: the C2 batch of
+isolated SVDs and the C4 XXZ ensemble, one unit per rank, one NCCL gather.
+Also on the line: the complex128 literal of the SVD benchmark, H_eff at
+chi=1024 inside a real sweep (native and emulated FP64), the C5 adaptive arm
+(N=200, PID chi_max=2048) to convergence, the CPU baselines.
 """
 from __future__ import annotations
 
