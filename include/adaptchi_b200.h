@@ -180,7 +180,9 @@ int achi_timer_stop(achi_ctx* ctx, double* ms);
 int achi_flush_l2(achi_ctx* ctx, size_t bytes);
 /* Per-phase device time measured with CUDA events on the context stream
  * (phases: 0 H_eff matvec, 1 SVD, 2 environment update).  enable turns the
- * accounting on/off (-1 leaves it); reset zeroes it.  out9 (may be NULL) =
+ * accounting on (1) or off (0), -1 leaves it; enable = n > 1 times one chain
+ * bond visit in n (timing events cost device time; the totals and the work
+ * then cover the sampled visits).  reset zeroes it.  out9 (may be NULL) =
  * {ms[3], algorithmic work[3] (flops, bytes, flops), launches[3]}. */
 /* Lanczos inner loop of this context's chains: 1 = one conditional CUDA graph
  * per (bond, direction) (default), 0 = stepped from the host (same kernels and
