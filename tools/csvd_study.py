@@ -1,6 +1,7 @@
-"""Complex SVD run-grouping study (svd_complex.cu knobs ACHI_CSVD_*): orthonormality of the
-accurate factor on graded spectra, canonical errors of a complex TFIM chain, and the
-device time of complex C3 sweeps 0..S-1."""
+"""Complex SVD check: orthonormality of the accurate factor on graded spectra, canonical
+errors of a complex TFIM chain, and the device time of complex C3 sweeps 0..S-1.  (The
+run-grouping study it was written for compared absolute and relative gap rules through
+study knobs since removed; DESIGN.md keeps the numbers.)"""
 import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
