@@ -283,6 +283,9 @@ void Chain::create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g) 
     fail(ACHI_E_INVALID_CONFIG, "dmrg: unknown initial state");
   cplx = g.arithmetic == ACHI_ARITH_COMPLEX || init == ACHI_INIT_RANDOM;
   svd.defer_v = !cplx;  // the real visit joins the replay at svd_phase_signs
+  // the real truncation needs the kept subspace, not 1e-15 vectors; the complex pairing
+  // of svd_complex.cu reads the real vectors themselves, so it keeps the full rotation
+  svd.skip_tol = cplx ? 0.0 : 1e-9;
   const size_t planes = cplx ? 2 : 1;
   // mixing matrices
   std::vector<MixMatrix> all;

@@ -1138,10 +1138,11 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
       const char* e = std::getenv("ACHI_JACOBI_CROSS");
       return e ? std::atoi(e) : 4;
     }();
-    static const double skip_tol = [] {
+    static const double skip_env = [] {  // ACHI_JACOBI_SKIP overrides the caller's setting
       const char* e = std::getenv("ACHI_JACOBI_SKIP");
-      return e ? std::atof(e) : 0.0;
+      return e ? std::atof(e) : -1.0;
     }();
+    const double skip_tol = skip_env >= 0 ? skip_env : ws.skip_tol;
     ClArgs a{G, ldg, gstride, mg, rows_pad, nb, npairs, max_inner, tol, stop_tol, zero2, cross_mode,
              skip_tol, jrec, jflag, jstride, sweeps_dev, nullptr, sweeps_host};
     static const bool prof_on = std::getenv("ACHI_JACOBI_PROF") != nullptr;

@@ -33,6 +33,11 @@ struct SvdWs {
   // trip); svd_wait_v joins it before V is read (svd_phase_signs and svd_gather
   // call it themselves)
   bool defer_v = false, v_pending = false;
+  // skip_tol (set by the chain): cluster-path block pairs whose largest cosine is below
+  // it are not rotated.  V stays exactly orthogonal and G = theta V exactly, so the
+  // truncation U_k U_k^T theta is an exact projection; only the singular vectors carry
+  // residual mixing of that size (sigma errors are its square).  0 = rotate to tol.
+  double skip_tol = 0.0;
 };
 
 void svd_wait_v(Ctx& ctx, SvdWs& ws);
