@@ -264,6 +264,11 @@ __global__ void set_boundary_kernel(double* p) { p[0] = 1.0; }
 
 }  // namespace
 
+// Jacobi stop threshold of the chain's SVDs (svd_jacobi.cuh SvdWs::stop_tol): after the
+// last sweep the remaining cosines are ~its square, far below what the truncation and the
+// energy see (kept ranks, entropies and energies are checked against the oracle in tests)
+constexpr double CHAIN_SVD_STOP = 1e-5;
+
 void Chain::create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g) {
   ctx = &c;
   spec = s;
@@ -286,6 +291,7 @@ void Chain::create(Ctx& c, const achi_model_spec& s, const achi_dmrg_config& g) 
   // the real truncation needs the kept subspace, not 1e-15 vectors; the complex pairing
   // of svd_complex.cu reads the real vectors themselves, so it keeps the full rotation
   svd.skip_tol = cplx ? 0.0 : 1e-9;
+  svd.stop_tol = cplx ? 1e-7 : CHAIN_SVD_STOP;
   const size_t planes = cplx ? 2 : 1;
   // mixing matrices
   std::vector<MixMatrix> all;

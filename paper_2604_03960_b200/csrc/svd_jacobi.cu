@@ -1104,10 +1104,11 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     const char* e = std::getenv("ACHI_JACOBI_INNER");
     return e ? std::max(1, std::atoi(e)) : 1;  // 1 measured fastest (profiles/svd_inner_study_r01.txt)
   }();
-  static const double stop_tol = [] {
+  static const double stop_env = [] {  // ACHI_JACOBI_STOP overrides the caller's setting
     const char* e = std::getenv("ACHI_JACOBI_STOP");
-    return e ? std::atof(e) : 1e-7;
+    return e ? std::atof(e) : -1.0;
   }();
+  const double stop_tol = stop_env > 0 ? stop_env : ws.stop_tol;
   int launches = 0;
   if (cluster) {
     const int rows_pad = static_cast<int>(((ldg + 15) / 16) * 16);

@@ -38,6 +38,10 @@ struct SvdWs {
   // truncation U_k U_k^T theta is an exact projection; only the singular vectors carry
   // residual mixing of that size (sigma errors are its square).  0 = rotate to tol.
   double skip_tol = 0.0;
+  // stop_tol: the iteration ends after a sweep whose weighted measure (the largest
+  // cosine times the square root of its smaller column's relative norm, svd_jacobi.cu
+  // finish_gram) is below it; the rotations of that sweep leave cosines ~ its square
+  double stop_tol = 1e-7;
 };
 
 void svd_wait_v(Ctx& ctx, SvdWs& ws);
