@@ -576,9 +576,14 @@ def svd_part(ctx, args):
     e2e = statistics.median(e2e_s)
     hbm, _ = peaks()
     med = statistics.median(ms)
-    # every round of a sweep streams all of G (n x n) and V (n x n) through the
-    # SMs once (read + write); a sweep has n/16 - 1 rounds
-    gbs = 16.0 * sweeps * (n // 16 - 1) * (n * n + n * n) / (med * 1e-3) / 1e9
+    # every round of a sweep reads G (n x n) for the block-pair Grams and reads + writes it
+    # for the rotations (24 bytes per element); a sweep has n/16 - 1 rounds.  V is not
+    # rotated: it is recovered after the sweeps by three n^3 GEMMs (svd_jacobi.cu v_recover)
+    gbs = 24.0 * sweeps * (n // 16 - 1) * (n * n) / (med * 1e-3) / 1e9
+    # 16 (mn + n^2) bytes per Jacobi sweep
+    gbs_d3 = 16.0 * sweeps * (n * n + n * n) / (med * 1e-3) / 1e9
+    # FP64 flops: Gram + rotation of every block pair, 8 m n^2 per sweep, plus the recovery
+    tfs = (8.0 * sweeps * n ** 3 + 3 * 2.0 * n ** 3) / (med * 1e-3) / 1e12
     return {"svd_chi2048_ms": round(med, 3), "svd_chi2048_e2e_ms": round(e2e * 1e3, 3),
             "svd_chi2048_sweeps": sweeps, "svd_chi2048_sum_sigma2_relerr": err,
             "svd_chi2048_recon_err": rec, "svd_chi2048_factors": "U, sigma, V^T (svd_full)",
@@ -586,8 +591,15 @@ def svd_part(ctx, args):
                                      "achieved": round(gbs, 2), "peak": hbm,
                                      "unit": "GB/s", "frac": round(gbs / hbm, 5),
                                      "traffic": measured_traffic().get("jacobi_stream_kernel"),
-                                     "work_def": "16*(n/16-1)*(2 n^2) bytes per Jacobi sweep "
-                                                 "(G and V read+written once per round)"}}
+                                     "work_def": "24*(n/16-1)*n^2 bytes per Jacobi sweep (G read "
+                                                 "for the Grams, read+written for the rotations, "
+                                                 "every round); V recovered by GEMM afterwards",
+                                     "frac_s8d3": round(gbs_d3 / hbm, 6),
+                                     "tensor": {"achieved": round(tfs, 3), "peak": FP64_PEAK_TFLOPS,
+                                                "unit": "TFLOP/s",
+                                                "frac": round(tfs / FP64_PEAK_TFLOPS, 4),
+                                                "work_def": "8 n^3 FP64 flops per Jacobi sweep "
+                                                            "+ 6 n^3 (V recovery GEMMs)"}}}
 
 
 def cpu_baseline_sample(spec, cfg, ch, last):

@@ -521,6 +521,7 @@ int achi_svd(achi_ctx* ctx, int m, int n, const double* a, double* sigma, double
     dA.reserve(static_cast<size_t>(m) * n);
     h2d(c, dA.p, a, static_cast<size_t>(m) * n);
     SvdWs ws;
+    ws.vrecover = true;
     const SvdSide side = m <= n ? SvdSide::kRows : SvdSide::kCols;
     SvdResultDev r = svd_device(c, ws, dA.p, m, n, m, n, side);
     const int k = r.r_true;
@@ -571,6 +572,7 @@ int achi_svd_device(achi_ctx* ctx, int m, int n, const double* d_a, double* d_si
     Ctx& c = ctx->c;
     if (m < 1 || n < 1) fail(ACHI_E_INVALID_MATRIX, "svd: matrix must be at least 1x1");
     static thread_local SvdWs ws;
+    ws.vrecover = true;
     static const int side_env = [] {  // study knob: force the orthogonalised side (rows|cols)
       const char* e = std::getenv("ACHI_SVD_SIDE");
       return e ? (e[0] == 'r' ? 0 : 1) : -1;
@@ -594,6 +596,7 @@ int achi_svd_complex_device(achi_ctx* ctx, int m, int n, const double* d_a, doub
     Ctx& c = ctx->c;
     if (m < 1 || n < 1) fail(ACHI_E_INVALID_MATRIX, "svd: matrix must be at least 1x1");
     SvdWs ws;
+    ws.vrecover = true;
     const int sw = svd_complex_device(c, ws, d_a, m, n, d_sigma, d_u, d_vdag);
     if (sweeps_out) *sweeps_out = sw;
   });
@@ -615,6 +618,7 @@ int achi_svd_complex(achi_ctx* ctx, int m, int n, const double* a, double* sigma
     dV.reserve(2 * static_cast<size_t>(r) * n);
     h2d(c, dA.p, a, mn2);
     SvdWs ws;
+    ws.vrecover = true;
     const int sw = svd_complex_device(c, ws, dA.p, m, n, dS.p, dU.p, dV.p);
     if (sigma) d2h(c, sigma, dS.p, r);
     if (u) d2h(c, u, dU.p, 2 * static_cast<size_t>(m) * r);

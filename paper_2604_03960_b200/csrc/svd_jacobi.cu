@@ -47,6 +47,10 @@ constexpr int CL_ROWS = 384;  // cluster mode: max working rows (shared memory b
 constexpr int CL_MAXP = 16;   // cluster mode: max block pairs (non-portable cluster of 16)
 constexpr int CL_MAXP_DB = 8; // V replay double-buffers the rotations up to this many pairs
 constexpr int MAX_SWEEPS = 40;
+// the stream path without preconditioning converges linearly for a long stretch on
+// strongly graded spectra (sigma log-spaced over 9-12 decades at 800 x 800: 40-50 sweeps,
+// tools/graded_study.py); its cap is higher (one unsigned long long per sweep of state)
+constexpr int STREAM_MAX_SWEEPS = 100;
 constexpr int RP_ROWS = 2;    // V replay: rows of V per CTA
 constexpr double EPS = 2.220446049250313e-16;
 
@@ -593,7 +597,7 @@ struct PersArgs {
   int max_inner;
   double tol, stop_tol;
   const double* zero2;
-  unsigned long long* conv;  // [MAX_SWEEPS] per-sweep max measure (whole launch)
+  unsigned long long* conv;  // [STREAM_MAX_SWEEPS] per-sweep max measure (whole launch)
   int* sweeps_out;
   int* sweeps_host_out;      // pinned host copy of *sweeps_out
   int rsplit;                // CTAs per block pair, each streaming a slice of the rows
@@ -751,7 +755,7 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
   double* mypart = R > 1 ? a.gpart + (static_cast<long>(pl) * R + h) * (JW * JW) : nullptr;
   unsigned gen = 0;
   int sweep = 0;
-  for (; sweep < MAX_SWEEPS; ++sweep) {
+  for (; sweep < STREAM_MAX_SWEEPS; ++sweep) {
     for (int round = 0; round < a.nb - 1; ++round) {
       int ba, bb;
       circle_pair(a.nb, round, p, ba, bb);
@@ -967,6 +971,101 @@ __global__ void gather_kernel(const double* __restrict__ G, long ldg, const doub
   }
 }
 
+// ---- V recovery (SvdWs::vrecover) ----
+// counts[0] = real columns, [1] = sigma > 0 and >= tau_big sigma_1, [2] = >= tau_ok sigma_1
+// (sorted is non-increasing with pad columns at -1 last; one block)
+__global__ void __launch_bounds__(1024) vrec_count_kernel(const double* __restrict__ sorted, int ng,
+                                                          double tau_big, double tau_ok,
+                                                          int* __restrict__ counts) {
+  __shared__ int red[3][32];
+  const double s1 = sorted[0];
+  int c0 = 0, c1 = 0, c2 = 0;
+  for (int i = threadIdx.x; i < ng; i += blockDim.x) {
+    const double s = sorted[i];
+    c0 += s >= 0.0;
+    c1 += s > 0.0 && s >= tau_big * s1;
+    c2 += s > 0.0 && s >= tau_ok * s1;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+    c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+    c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { red[0][w] = c0; red[1][w] = c1; red[2][w] = c2; }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    int t = 0;
+    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) t += red[threadIdx.x][i];
+    counts[threadIdx.x] = t;
+  }
+}
+
+// V[:, c] *= 1 / sigma_c^2 (zero for pad or zero columns); one block per column
+__global__ void vrec_scale_kernel(double* __restrict__ V, int ng, const double* __restrict__ sig) {
+  const int c = blockIdx.x;
+  const double s = sig[c];
+  const double f = s > 0.0 ? 1.0 / (s * s) : 0.0;
+  double* v = V + static_cast<long>(c) * ng;
+  for (int r = threadIdx.x; r < ng; r += blockDim.x) v[r] *= f;
+}
+
+// Cg[c][j] <- Cg[c][j] / sigma_c^2 off the diagonal, 0 on it (and for pad or zero columns):
+// with Cg = G^T G = Sigma (I + Delta) Sigma (Delta the residual cosines) the recovered
+// V_rec = V Sigma (I + Delta) Sigma^-1, so V = V_rec - V_rec M to first order, M_jc = Cg_jc / sigma_c^2
+__global__ void vrec_cm_kernel(double* __restrict__ Cg, int ng, const double* __restrict__ sig) {
+  const long tot = static_cast<long>(ng) * ng;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < tot;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i / ng), j = static_cast<int>(i - static_cast<long>(c) * ng);
+    const double s = sig[c];
+    Cg[i] = (c != j && s > 0.0) ? Cg[i] / (s * s) : 0.0;
+  }
+}
+
+// T (ng x tp row-major) <-> the tail columns V[:, perm[k0 + j]], j < t (columns j >= t zero)
+__global__ void vrec_tail_io_kernel(double* __restrict__ V, int ng, const int* __restrict__ perm,
+                                    int k0, int t, int tp, double* __restrict__ T, int to_tail) {
+  const long tot = static_cast<long>(ng) * tp;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < tot;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / tp), j = static_cast<int>(i - static_cast<long>(r) * tp);
+    if (to_tail) {
+      T[i] = j < t ? V[static_cast<long>(perm[k0 + j]) * ng + r] : 0.0;
+    } else if (j < t) {
+      V[static_cast<long>(perm[k0 + j]) * ng + r] = T[i];
+    }
+  }
+}
+
+// P[c][:] = 0 unless column c is a kept-accurate one (sigma_c > 0, >= tau_big sigma_1)
+__global__ void vrec_mask_kernel(double* __restrict__ P, int ng, int tp, const double* __restrict__ sig,
+                                 const double* __restrict__ sorted, double tau_big) {
+  const double s1 = sorted[0];
+  const long tot = static_cast<long>(ng) * tp;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < tot;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const double s = sig[i / tp];
+    if (!(s > 0.0 && s >= tau_big * s1)) P[i] = 0.0;
+  }
+}
+
+// a -= b (n elements)
+__global__ void vrec_sub_kernel(double* __restrict__ a, const double* __restrict__ b, long n) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x)
+    a[i] -= b[i];
+}
+
+// X = 1.5 I - 0.5 W (tp x tp), the Newton-Schulz step towards the orthonormal polar factor
+__global__ void vrec_ns_kernel(double* __restrict__ W, int tp) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tp * tp; i += gridDim.x * blockDim.x) {
+    const int r = i / tp, c = i - r * tp;
+    W[i] = (r == c ? 1.5 : 0.0) - 0.5 * W[i];
+  }
+}
+
 size_t stream_smem() { return sizeof(Chunk) * STREAM_STAGES + sizeof(Small) + 16; }
 size_t cluster_smem(int rows_pad) {
   return sizeof(double) * 2 * JW * (rows_pad + 4) + sizeof(Small) + 16;
@@ -974,6 +1073,74 @@ size_t cluster_smem(int rows_pad) {
 size_t replay_smem(int npairs, int ng) {  // rotations double-buffered up to CL_MAXP_DB pairs
   const long jbufs = npairs <= CL_MAXP_DB ? 2 : 1;
   return sizeof(double) * (jbufs * npairs * JW * JW + 2L * RP_ROWS * ng);
+}
+
+// V recovery after a Jacobi run that rotated only G (SvdWs::vrecover): G0 V = G with V
+// orthogonal gives G0^T G = V Sigma^2, so V[:, c] = G0^T G[:, c] / sigma_c^2 (one GEMM), with
+// an error ~ eps sqrt(ng) sigma_1 / sigma_c.  Columns with sigma_c >= 1e-3 sigma_1 are used
+// as they are (errors <~ 1e-13); the tail down to 1e-5 sigma_1 is projected off them and
+// re-orthonormalised by Newton-Schulz steps (its errors are <~ 1e-11, so the steps converge
+// at once and move the tail vectors by no more than that: sigma_c times it in the
+// reconstruction).  Returns false -- the caller decomposes again with V accumulated -- when
+// a value lies below 1e-5 sigma_1 (there the recovered column is not a usable start).
+constexpr double VREC_TAU_BIG = 1e-3, VREC_TAU_OK = 1e-5;
+
+bool v_recover(Ctx& ctx, SvdWs& ws, const double* G0, const double* G, long ldg, int mg, int ng,
+               const double* sig, const double* sorted, const int* perm, double* V) {
+  // V (col-major, ld ng) = rows of (G^T G0): C[c][r] = sum_k G[k][c] G0[k][r]
+  gemm(ctx, ng, ng, mg, Operand{G, ldg, Major::kK}, Operand{G0, ldg, Major::kK}, V, ng);
+  int* counts = ws.vcounts.reserve(4);
+  vrec_count_kernel<<<1, 1024, 0, ctx.stream>>>(sorted, ng, VREC_TAU_BIG, VREC_TAU_OK, counts);
+  ACHI_LAUNCHED(ctx);
+  vrec_scale_kernel<<<ng, 256, 0, ctx.stream>>>(V, ng, sig);
+  ACHI_LAUNCHED(ctx);
+  {
+    // first-order removal of the residual cosines of G (V_rec carries them amplified by
+    // sigma_j / sigma_c): V -= V M, M_jc = (G^T G)_jc / sigma_c^2
+    const long nn = static_cast<long>(ng) * ng;
+    double* Cg = ws.vproj.reserve(static_cast<size_t>(nn));
+    double* D = ws.vtail.reserve(static_cast<size_t>(nn));
+    gemm(ctx, ng, ng, mg, Operand{G, ldg, Major::kK}, Operand{G, ldg, Major::kK}, Cg, ng);
+    const int eb = static_cast<int>(std::min<long>(cdiv(nn, 256), 4L * ctx.num_sms));
+    vrec_cm_kernel<<<eb, 256, 0, ctx.stream>>>(Cg, ng, sig);
+    ACHI_LAUNCHED(ctx);
+    // D[c][r] = sum_j M[j][c] V[j][r] (rows of D = columns of V M)
+    gemm(ctx, ng, ng, ng, Operand{Cg, ng, Major::kK}, Operand{V, ng, Major::kMN}, D, ng);
+    vrec_sub_kernel<<<eb, 256, 0, ctx.stream>>>(V, D, nn);
+    ACHI_LAUNCHED(ctx);
+  }
+  ctx.sync();
+  const int n_real = counts[0], k_big = counts[1], k_ok = counts[2];
+  if (k_ok < n_real) return false;
+  const int t = n_real - k_big;
+  if (t == 0) return true;
+  const int tp = t + (t & 1);
+  const long tl = static_cast<long>(ng) * tp;
+  double* T = ws.vtail.reserve(static_cast<size_t>(tl));
+  double* P = ws.vproj.reserve(static_cast<size_t>(tl));
+  double* W = ws.vns.reserve(static_cast<size_t>(tp) * tp);
+  const int blocks = static_cast<int>(std::min<long>(cdiv(tl, 256), 4L * ctx.num_sms));
+  vrec_tail_io_kernel<<<blocks, 256, 0, ctx.stream>>>(V, ng, perm, k_big, t, tp, T, 1);
+  ACHI_LAUNCHED(ctx);
+  // T <- T - V_big (V_big^T T): P = V^T T with the rows of non-big columns zeroed
+  gemm(ctx, ng, tp, ng, Operand{V, ng, Major::kK}, Operand{T, tp, Major::kMN}, P, tp);
+  vrec_mask_kernel<<<blocks, 256, 0, ctx.stream>>>(P, ng, tp, sig, sorted, VREC_TAU_BIG);
+  ACHI_LAUNCHED(ctx);
+  double* D = ws.G0.p;  // G0 is no longer needed: D = V P (ng x tp) fits in it
+  gemm(ctx, ng, tp, ng, Operand{V, ng, Major::kMN}, Operand{P, tp, Major::kMN}, D, tp);
+  vrec_sub_kernel<<<blocks, 256, 0, ctx.stream>>>(T, D, tl);
+  ACHI_LAUNCHED(ctx);
+  // two Newton-Schulz steps T <- T (1.5 I - 0.5 T^T T)
+  for (int it = 0; it < 2; ++it) {
+    gemm(ctx, tp, tp, ng, Operand{T, tp, Major::kMN}, Operand{T, tp, Major::kMN}, W, tp);
+    vrec_ns_kernel<<<cdiv(static_cast<long>(tp) * tp, 256), 256, 0, ctx.stream>>>(W, tp);
+    ACHI_LAUNCHED(ctx);
+    gemm(ctx, ng, tp, tp, Operand{T, tp, Major::kK}, Operand{W, tp, Major::kMN}, P, tp);
+    std::swap(T, P);
+  }
+  vrec_tail_io_kernel<<<blocks, 256, 0, ctx.stream>>>(V, ng, perm, k_big, t, tp, T, 0);
+  ACHI_LAUNCHED(ctx);
+  return true;
 }
 
 }  // namespace
@@ -1010,7 +1177,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   double* sig = ws.sig.reserve(static_cast<size_t>(ng) * batch);
   double* sorted = ws.sorted.reserve(static_cast<size_t>(ng) * batch);
   int* perm = ws.perm.reserve(static_cast<size_t>(ng) * batch);
-  unsigned long long* conv = ws.conv.reserve(MAX_SWEEPS * 8);
+  unsigned long long* conv = ws.conv.reserve(STREAM_MAX_SWEEPS * 8);
   double* zero2 = ws.zero2.reserve(2 * static_cast<size_t>(batch));
   mark("reserve");
   const int nsw = std::max(64, batch);
@@ -1044,6 +1211,11 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     });
     cluster = placeable > 0;
   }
+  static const bool vrec_env = [] {  // ACHI_SVD_VRECOVER=0: always accumulate V (studies)
+    const char* e = std::getenv("ACHI_SVD_VRECOVER");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool vrec = V && !cluster && !v_init && batch == 1 && ws.vrecover && vrec_env;
   // pad columns: rows side -> columns >= m_true (theta rows (l,s1), padded l last);
   // cols side with padding -> columns (s2, jr) with jr >= chr_true (d = 2 on the padded path)
   int pad_mod = ng, pad_lim = rows ? m_true : n_true;
@@ -1062,7 +1234,10 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     load_g_kernel<<<grid, blk, 0, ctx.stream>>>(theta, bstride, m, n, G, gstride, ldg, mg, ng,
                                                 rows ? 1 : 0);
     ACHI_LAUNCHED(ctx);
-    if (V && !cluster) {
+    if (vrec) {
+      ACHI_CUDA(cudaMemcpyAsync(ws.G0.reserve(static_cast<size_t>(gstride)), G, sizeof(double) * gstride,
+                                cudaMemcpyDeviceToDevice, ctx.stream));
+    } else if (V && !cluster) {
       if (v_init) {
         ACHI_CUDA(cudaMemcpyAsync(V, v_init, sizeof(double) * vstride, cudaMemcpyDeviceToDevice,
                                   ctx.stream));
@@ -1254,15 +1429,30 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     }
     for (int b0 = 0; b0 < batch; b0 += per_launch_r, ++launches) {
       const int nbat = std::min(per_launch_r, batch - b0);
-      ACHI_CUDA(cudaMemsetAsync(conv, 0, sizeof(unsigned long long) * MAX_SWEEPS, ctx.stream));
+      ACHI_CUDA(cudaMemsetAsync(conv, 0, sizeof(unsigned long long) * STREAM_MAX_SWEEPS, ctx.stream));
       if (pcnt) ACHI_CUDA(cudaMemsetAsync(pcnt, 0, sizeof(unsigned) * npairs * nbat, ctx.stream));
-      PersArgs a{G, ldg, gstride, mg, V, ng, vstride, ng, nb, npairs, b0,
+      PersArgs a{G, ldg, gstride, mg, vrec ? nullptr : V, ng, vstride, ng, nb, npairs, b0,
                  max_inner, tol, stop_tol, zero2, conv, sweeps_dev + (launches % nsw),
                  sweeps_host + (launches % nsw), rsplit, gpart, pcnt, stream_cross};
       void* args[] = {&a};
       ACHI_CUDA(cudaLaunchCooperativeKernel(kern, dim3(npairs * nbat * rsplit), dim3(JT), args, smem,
                                             ctx.stream));
       ACHI_LAUNCHED(ctx);
+      static const bool convlog = std::getenv("ACHI_JACOBI_CONVLOG") != nullptr;  // study: per-sweep measures
+      if (convlog) {
+        unsigned long long h[STREAM_MAX_SWEEPS];
+        ACHI_CUDA(cudaMemcpyAsync(h, conv, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+        std::fprintf(stderr, "[jacobi-stream] %dx%d ng=%d rsplit=%d sweeps=%d measures:", m, n, ng, rsplit,
+                     sweeps_host[launches % nsw]);
+        for (int i = 0; i < STREAM_MAX_SWEEPS && h[i]; ++i)
+        {
+          double d;
+          std::memcpy(&d, &h[i], sizeof d);
+          std::fprintf(stderr, " %.1e", d);
+        }
+        std::fprintf(stderr, "\n");
+      }
     }
     launches = std::min(launches, nsw);
   }
@@ -1284,6 +1474,21 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   }
   // (the Jacobi kernels write their sweep counts into sweeps_host themselves)
   mark("norms+sort");
+  if (vrec && !v_recover(ctx, ws, ws.G0.p, G, ldg, mg, ng, sig, sorted, perm, V)) {
+    // a value below 1e-5 sigma_1: decompose again with V accumulated
+    ws.vrecover = false;
+    SvdResultDev r2;
+    try {
+      r2 = svd_device(ctx, ws, theta, m, n, m_true, n_true, side, batch, bstride, sigma_out,
+                      want_vectors, nullptr);
+    } catch (...) {
+      ws.vrecover = true;
+      throw;
+    }
+    ws.vrecover = true;
+    return r2;
+  }
+  if (vrec) mark("v recover");
   if (trace) {
     double tot = 0;
     for (auto& [w, ms] : marks) tot += ms;
@@ -1309,6 +1514,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   r.r_true = r_true;
   r.sweeps_host = sweeps_host;
   r.n_launches = launches;
+  r.max_sweeps = cluster ? MAX_SWEEPS : STREAM_MAX_SWEEPS;
   r.G = G;
   r.V = V;
   r.sigma = sorted;
@@ -1325,7 +1531,7 @@ void svd_wait_v(Ctx& ctx, SvdWs& ws) {
 int SvdResultDev::sweeps() const {
   int s = 0;
   for (int i = 0; i < n_launches; ++i) s = std::max(s, sweeps_host[i]);
-  if (s >= MAX_SWEEPS) fail(ACHI_E_NUMERICAL_FAILURE, "svd: decomposition did not converge");
+  if (s >= max_sweeps) fail(ACHI_E_NUMERICAL_FAILURE, "svd: decomposition did not converge");
   return s;
 }
 

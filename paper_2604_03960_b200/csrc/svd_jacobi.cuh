@@ -42,6 +42,17 @@ struct SvdWs {
   // cosine times the square root of its smaller column's relative norm, svd_jacobi.cu
   // finish_gram) is below it; the rotations of that sweep leave cosines ~ its square
   double stop_tol = 1e-7;
+  // vrecover (set by the public SVD entries, not by the chain): on the stream path a cold,
+  // single-matrix decomposition with vectors rotates only G (3 of the 5 matrix passes per
+  // round) and recovers the accumulated factor afterwards as V = G0^T G Sigma^-2 by one
+  // GEMM (G0 the loaded working matrix), corrected to first order for G's residual cosines
+  // (two more GEMMs); column c is then accurate to ~eps sigma_1 / sigma_c; columns below
+  // 1e-3 sigma_1 are projected off the others and re-orthonormalised (Newton-Schulz), and a
+  // spectrum reaching below 1e-5 sigma_1 (rank-deficient or ill-conditioned input) is
+  // decomposed again with V accumulated (svd_jacobi.cu v_recover)
+  bool vrecover = false;
+  DevBuf G0, vtail, vproj, vns;
+  PinnedArr<int> vcounts;
 };
 
 void svd_wait_v(Ctx& ctx, SvdWs& ws);
@@ -59,6 +70,7 @@ struct SvdResultDev {
   int r_true;        // min(m_true, n_true)
   const int* sweeps_host;  // per cooperative launch; valid after the next stream sync
   int n_launches;
+  int max_sweeps;    // the path's sweep cap (reaching it is a NumericalFailure)
   const double* G;   // mg x ng col-major (ld = mg, rows >= the true row count are zero)
   const double* V;   // ng x ng col-major (ld = ng)
   const double* sigma;  // sorted, r_true entries valid (device)
