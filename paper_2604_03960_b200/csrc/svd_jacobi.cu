@@ -601,9 +601,12 @@ struct PersArgs {
   int* sweeps_out;
   int* sweeps_host_out;      // pinned host copy of *sweeps_out
   int rsplit;                // CTAs per block pair, each streaming a slice of the rows
-  double* gpart;             // [pairs in launch][rsplit][32*32] partial Grams (rsplit > 1)
-  unsigned* pcnt;            // [pairs in launch] arrival counters (zeroed per launch)
+  double* gpart;             // [2][pairs in launch][rsplit][32*32] partial Grams by round parity (rsplit > 1)
+  unsigned* pcnt;            // [2][pairs in launch]: Gram arrival counters, then round completion
+                             // counters (zeroed per launch)
   int cross_mode;            // 4: two of every three rounds sweep only the cross-block pairs
+  long long* prof;           // optional clock64 phase sums over every CTA's thread 0 (ACHI_JACOBI_PROF)
+  int p2p;                   // 1: rounds ordered by per-pair completion counters, grid barrier per sweep
 };
 
 // cp.async chunk loads: rows [r0, r0+64) of the 32 pair columns -> X[col][row]
@@ -620,62 +623,56 @@ __device__ __forceinline__ void load_chunk_async(Chunk& X, const double* M, long
   }
 }
 
-__device__ __forceinline__ void store_chunk(const Chunk& X, double* M, long ld, int rows, int r0,
-                                            int ca, int cb) {
-#pragma unroll
-  for (int it = 0; it < JW * JCH / 2 / JT; ++it) {
-    const int idx = threadIdx.x + it * JT;
-    const int c = idx / (JCH / 2), r = 2 * (idx - c * (JCH / 2));
-    const int col = c < JB ? ca + c : cb + c - JB;
-    const double2 v = *reinterpret_cast<const double2*>(&X[c][r]);
-    double* dst = M + col * ld + r0 + r;
-    if (r0 + r + 1 < rows)
-      *reinterpret_cast<double2*>(dst) = v;
-    else if (r0 + r < rows)
-      dst[0] = v.x;
-  }
-}
-
-__device__ __forceinline__ void gram_chunk(const Chunk& X, double (&acc)[4]) {
+// two accumulator chains that run on across the chunks of a pass (the caller sums them
+// once at the end, so no chunk waits for its DMMA chain to drain)
+__device__ __forceinline__ void gram_chunk(const Chunk& X, double (&acc)[4], double (&acc2)[4]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3, mt = warp >> 2, nt = warp & 3;
-  double acc2[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int k8 = 0; k8 < JCH / 8; ++k8) {
     const int k = k8 * 8 + tig;
     mma16x8x4(acc, X[mt * 16 + gid][k], X[mt * 16 + gid + 8][k], X[nt * 8 + gid][k]);
     mma16x8x4(acc2, X[mt * 16 + gid][k + 4], X[mt * 16 + gid + 8][k + 4], X[nt * 8 + gid][k + 4]);
   }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) acc[i] += acc2[i];
 }
 
-// X <- X * J in place (rows of the chunk times the 32x32 rotation)
-__device__ __forceinline__ void rotate_chunk(Chunk& X, const Small& sm) {
+// rows [r0, r0 + 64) of the pair columns (ca.., cb..) of M <- X * J, stored straight from
+// the DMMA fragments (four accumulator chains: two K halves of two column tiles); X is
+// only read, so the stage buffer is free once every warp has passed the next barrier
+__device__ __forceinline__ void rotate_store_chunk(const Chunk& X, const Small& sm, double* M, long ld,
+                                                   int rows, int r0, int ca, int cb) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3, mt = warp >> 1;
-  double acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+  double acc[2][2][4] = {};
 #pragma unroll
-  for (int k4 = 0; k4 < JW / 4; ++k4) {
-    const int k = k4 * 4 + tig;
-    const double a0 = X[k][mt * 16 + gid], a1 = X[k][mt * 16 + gid + 8];
+  for (int k4 = 0; k4 < JW / 8; ++k4) {
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int nt = (warp & 1) * 2 + q;
-      mma16x8x4(acc[q], a0, a1, sm.J[k][nt * 8 + gid]);
+    for (int h = 0; h < 2; ++h) {
+      const int k = (h * (JW / 8) + k4) * 4 + tig;
+      const double a0 = X[k][mt * 16 + gid], a1 = X[k][mt * 16 + gid + 8];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int nt = (warp & 1) * 2 + q;
+        mma16x8x4(acc[h][q], a0, a1, sm.J[k][nt * 8 + gid]);
+      }
     }
   }
-  __syncthreads();
+  const int r = r0 + mt * 16 + gid;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int nt = (warp & 1) * 2 + q;
-    const int r = mt * 16 + gid, j = nt * 8 + 2 * tig;
-    X[j][r] = acc[q][0];
-    X[j + 1][r] = acc[q][1];
-    X[j][r + 8] = acc[q][2];
-    X[j + 1][r + 8] = acc[q][3];
+    const int j = nt * 8 + 2 * tig;  // columns j, j + 1 of the pair (same block: j even, JB even)
+    double* c0 = M + static_cast<long>(j < JB ? ca + j : cb + j - JB) * ld;
+    double* c1 = c0 + ld;
+    if (r < rows) {
+      c0[r] = acc[0][q][0] + acc[1][q][0];
+      c1[r] = acc[0][q][1] + acc[1][q][1];
+    }
+    if (r + 8 < rows) {
+      c0[r + 8] = acc[0][q][2] + acc[1][q][2];
+      c1[r + 8] = acc[0][q][3] + acc[1][q][3];
+    }
   }
-  __syncthreads();
 }
 
 // STREAM_STAGES chunks in flight per CTA (one CTA per SM: the passes are
@@ -713,17 +710,18 @@ __device__ __forceinline__ void rot_load(Chunk* X, const RotSeg& s, int t, int c
 __device__ void stream_rotate_prefetch(Chunk* X, const RotSeg& s, int ca, int cb) {
   for (int k = 0; k < STREAM_STAGES - 1; ++k) rot_load(X, s, k, ca, cb);
 }
+// one barrier per chunk: it publishes chunk k (landed: at most STREAM_STAGES - 2 newer
+// groups pending) and releases the buffer of chunk k - 1, which the load issued after it
+// reuses
 __device__ void stream_rotate(Chunk* X, const RotSeg& s, int ca, int cb, const Small& sm) {
   const int n = s.nG + s.nV;
   for (int k = 0; k < n; ++k) {
-    rot_load(X, s, k + STREAM_STAGES - 1, ca, cb);
-    cp_wait<STREAM_STAGES - 1>();
+    cp_wait<STREAM_STAGES - 2>();
     __syncthreads();
-    rotate_chunk(X[k % STREAM_STAGES], sm);
+    rot_load(X, s, k + STREAM_STAGES - 1, ca, cb);
     double* M; long ld; int rows, r0;
     rot_chunk_io(s, k, M, ld, rows, r0);
-    store_chunk(X[k % STREAM_STAGES], M, ld, rows, r0, ca, cb);
-    __syncthreads();
+    rotate_store_chunk(X[k % STREAM_STAGES], sm, M, ld, rows, r0, ca, cb);
   }
 }
 
@@ -752,30 +750,57 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
   const int nch = (a.mg + JCH - 1) / JCH, nchv = (a.vrows + JCH - 1) / JCH;
   const int g0 = h * nch / R, g1 = (h + 1) * nch / R;
   const int v0 = h * nchv / R, v1 = (h + 1) * nchv / R;
-  double* mypart = R > 1 ? a.gpart + (static_cast<long>(pl) * R + h) * (JW * JW) : nullptr;
-  unsigned gen = 0;
+  const int npl = gridDim.x / R;        // pairs in the launch
+  const int pbase = pl - p;             // first pair of this matrix in the launch
+  unsigned* done = a.pcnt + npl;        // per pair: CTA-rounds completed
+  unsigned gen = 0, rg = 0;             // rg: rounds completed by this CTA
   int sweep = 0;
   for (; sweep < STREAM_MAX_SWEEPS; ++sweep) {
     for (int round = 0; round < a.nb - 1; ++round) {
       int ba, bb;
       circle_pair(a.nb, round, p, ba, bb);
       const int ca = ba * JB, cb = bb * JB;
-      double acc[4] = {0, 0, 0, 0};
+      const bool prof = a.prof && threadIdx.x == 0;
+      const long long t0 = prof ? clock64() : 0;
+      if (a.p2p && round > 0) {
+        // blocks ba and bb were rotated in the previous round by the pairs that held them
+        // there: wait for every CTA of those two pairs (point-to-point, instead of a grid
+        // barrier per round; the rotation stores are fenced before the counters move)
+        if (threadIdx.x == 0) {
+          int p1, p2, s1, s2;
+          circle_locate(a.nb, round - 1, ba, p1, s1);
+          circle_locate(a.nb, round - 1, bb, p2, s2);
+          const unsigned need = rg * static_cast<unsigned>(R);
+          const volatile unsigned* d1 = done + pbase + p1;
+          const volatile unsigned* d2 = done + pbase + p2;
+          while (*d1 < need || *d2 < need) __nanosleep(20);
+          __threadfence();
+        }
+        __syncthreads();
+      }
+      double acc[4] = {0, 0, 0, 0}, acc2[4] = {0, 0, 0, 0};
       for (int k = 0; k < STREAM_STAGES - 1; ++k) {
         if (g0 + k < g1) load_chunk_async(X[k], G, a.ldg, a.mg, (g0 + k) * JCH, ca, cb);
         cp_commit();
       }
-      for (int k = 0; k < g1 - g0; ++k) {
+      for (int k = 0; k < g1 - g0; ++k) {  // one barrier per chunk (as in stream_rotate)
+        cp_wait<STREAM_STAGES - 2>();
+        __syncthreads();
         const int kn = k + STREAM_STAGES - 1;
         if (g0 + kn < g1) load_chunk_async(X[kn % STREAM_STAGES], G, a.ldg, a.mg, (g0 + kn) * JCH, ca, cb);
         cp_commit();
-        cp_wait<STREAM_STAGES - 1>();
-        __syncthreads();
-        gram_chunk(X[k % STREAM_STAGES], acc);
-        __syncthreads();
+        gram_chunk(X[k % STREAM_STAGES], acc, acc2);
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] += acc2[i];
+      __syncthreads();  // every warp is done with the stage buffers the rotation prefetch reuses
+      const long long t1 = prof ? clock64() : 0;
       if (R > 1) {
-        // publish the partial Gram, wait for the pair's other CTAs, fixed-order sum
+        // publish the partial Gram, wait for the pair's other CTAs, fixed-order sum (two
+        // slots by round parity: a CTA running one round ahead of its pair mates never
+        // overwrites partials they may still be reading)
+        double* slot = a.gpart + static_cast<long>(gen & 1) * npl * R * (JW * JW);
+        double* mypart = slot + (static_cast<long>(pl) * R + h) * (JW * JW);
 #pragma unroll
         for (int i = 0; i < 4; ++i) __stcg(mypart + i * JT + threadIdx.x, acc[i]);
         __threadfence();
@@ -787,7 +812,7 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
           __threadfence();
         }
         __syncthreads();
-        const double* base = a.gpart + static_cast<long>(pl) * R * (JW * JW);
+        const double* base = slot + static_cast<long>(pl) * R * (JW * JW);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           double t = __ldcg(base + i * JT + threadIdx.x);
@@ -798,7 +823,9 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
       const RotSeg seg{G, a.ldg, a.mg, g0, g1 - g0, V, a.ldv, a.vrows, v0, V ? v1 - v0 : 0};
       stream_rotate_prefetch(X, seg, ca, cb);  // lands during the inner Jacobi
       const bool cross = a.cross_mode == 4 && (round % 3) != 0;
+      const long long t2 = prof ? clock64() : 0;
       const bool rot = finish_gram(sm, acc, z2, ig2, a.tol, a.max_inner, cross);
+      const long long t3 = prof ? clock64() : 0;
       if (threadIdx.x == 0 && h == 0)
         atomicMax(&a.conv[sweep], static_cast<unsigned long long>(__double_as_longlong(sm.red2[0])));
       if (rot) {
@@ -807,7 +834,26 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
         cp_wait<0>();  // drain the unused prefetch before the buffers are reused
         __syncthreads();
       }
-      grid.sync();
+      const long long t4 = prof ? clock64() : 0;
+      if (a.p2p) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(done + pl, 1u);
+        }
+        ++rg;
+        if (round == a.nb - 2) grid.sync();  // the sweep's stop test reads every pair's measure
+      } else {
+        grid.sync();
+      }
+      if (prof) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&a.prof[0]), t1 - t0);  // Gram pass
+        atomicAdd(reinterpret_cast<unsigned long long*>(&a.prof[1]), t2 - t1);  // partial-Gram exchange
+        atomicAdd(reinterpret_cast<unsigned long long*>(&a.prof[2]), t3 - t2);  // measure + inner Jacobi
+        atomicAdd(reinterpret_cast<unsigned long long*>(&a.prof[3]), t4 - t3);  // rotation pass
+        atomicAdd(reinterpret_cast<unsigned long long*>(&a.prof[4]), clock64() - t4);  // grid barrier
+        atomicAdd(reinterpret_cast<unsigned long long*>(&a.prof[5]), 1ull);
+      }
     }
     const double meas = __longlong_as_double(
         static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(&a.conv[sweep])));
@@ -1422,22 +1468,46 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     const int per_launch_r = std::max(1, mb / (npairs * rsplit));
     double* gpart = nullptr;
     unsigned* pcnt = nullptr;
+    {
+      const int pairs_all = npairs * std::min(per_launch_r, batch);
+      pcnt = ws.pcnt.reserve(2 * static_cast<size_t>(pairs_all));
+    }
     if (rsplit > 1) {
       const int pairs_max = npairs * std::min(per_launch_r, batch);
-      gpart = ws.gpart.reserve(static_cast<size_t>(pairs_max) * rsplit * JW * JW);
-      pcnt = ws.pcnt.reserve(static_cast<size_t>(pairs_max));
+      gpart = ws.gpart.reserve(2 * static_cast<size_t>(pairs_max) * rsplit * JW * JW);
     }
     for (int b0 = 0; b0 < batch; b0 += per_launch_r, ++launches) {
       const int nbat = std::min(per_launch_r, batch - b0);
       ACHI_CUDA(cudaMemsetAsync(conv, 0, sizeof(unsigned long long) * STREAM_MAX_SWEEPS, ctx.stream));
-      if (pcnt) ACHI_CUDA(cudaMemsetAsync(pcnt, 0, sizeof(unsigned) * npairs * nbat, ctx.stream));
+      ACHI_CUDA(cudaMemsetAsync(pcnt, 0, sizeof(unsigned) * 2 * npairs * nbat, ctx.stream));
+      static const int stream_p2p = [] {  // ACHI_JACOBI_P2P=0: grid barrier after every round
+        const char* e = std::getenv("ACHI_JACOBI_P2P");
+        return e ? std::atoi(e) : 1;
+      }();
+      static const bool sprof = std::getenv("ACHI_JACOBI_PROF") != nullptr;
+      static DevArr<long long> sprofbuf;
+      long long* pb = nullptr;
+      if (sprof) {
+        pb = sprofbuf.reserve(8);
+        ACHI_CUDA(cudaMemsetAsync(pb, 0, 8 * sizeof(long long), ctx.stream));
+      }
       PersArgs a{G, ldg, gstride, mg, vrec ? nullptr : V, ng, vstride, ng, nb, npairs, b0,
                  max_inner, tol, stop_tol, zero2, conv, sweeps_dev + (launches % nsw),
-                 sweeps_host + (launches % nsw), rsplit, gpart, pcnt, stream_cross};
+                 sweeps_host + (launches % nsw), rsplit, gpart, pcnt, stream_cross, pb, stream_p2p};
       void* args[] = {&a};
       ACHI_CUDA(cudaLaunchCooperativeKernel(kern, dim3(npairs * nbat * rsplit), dim3(JT), args, smem,
                                             ctx.stream));
       ACHI_LAUNCHED(ctx);
+      if (sprof) {
+        long long h[8];
+        ACHI_CUDA(cudaMemcpyAsync(h, pb, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+        const double rr = h[5] > 0 ? static_cast<double>(h[5]) : 1.0;
+        std::fprintf(stderr,
+                     "[jacobi-stream] ng=%d mg=%d rsplit=%d CTA-rounds=%lld cycles per CTA-round: gram %.0f "
+                     "exchange %.0f inner %.0f rotate %.0f barrier %.0f\n",
+                     ng, mg, rsplit, h[5], h[0] / rr, h[1] / rr, h[2] / rr, h[3] / rr, h[4] / rr);
+      }
       static const bool convlog = std::getenv("ACHI_JACOBI_CONVLOG") != nullptr;  // study: per-sweep measures
       if (convlog) {
         unsigned long long h[STREAM_MAX_SWEEPS];
