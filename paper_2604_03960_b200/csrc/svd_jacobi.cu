@@ -623,17 +623,67 @@ __device__ __forceinline__ void load_chunk_async(Chunk& X, const double* M, long
   }
 }
 
-// two accumulator chains that run on across the chunks of a pass (the caller sums them
-// once at the end, so no chunk waits for its DMMA chain to drain)
-__device__ __forceinline__ void gram_chunk(const Chunk& X, double (&acc)[4], double (&acc2)[4]) {
+// The Gram is symmetric: its lower-left 16 x 16 block (warp tiles (1,0), (1,1)) is the
+// transpose of the upper-right one, so the pass computes six of the eight 16 x 8 warp
+// tiles, balanced over the four SM sub-partitions (warp w and w + 4 share one): warps 0-3
+// take tiles (0, w) over the whole chunk, warps 4-7 the two tiles (1, 2), (1, 3) split
+// into K halves (three K-units per sub-partition instead of four).
+__device__ __forceinline__ void gram_chunk_sym(const Chunk& X, double (&acc)[4], double (&acc2)[4]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gid = lane >> 2, tig = lane & 3, mt = warp >> 2, nt = warp & 3;
+  const int gid = lane >> 2, tig = lane & 3;
+  if (warp < 4) {
+    const int nt = warp;
 #pragma unroll
-  for (int k8 = 0; k8 < JCH / 8; ++k8) {
-    const int k = k8 * 8 + tig;
-    mma16x8x4(acc, X[mt * 16 + gid][k], X[mt * 16 + gid + 8][k], X[nt * 8 + gid][k]);
-    mma16x8x4(acc2, X[mt * 16 + gid][k + 4], X[mt * 16 + gid + 8][k + 4], X[nt * 8 + gid][k + 4]);
+    for (int k8 = 0; k8 < JCH / 8; ++k8) {
+      const int k = k8 * 8 + tig;
+      mma16x8x4(acc, X[gid][k], X[gid + 8][k], X[nt * 8 + gid][k]);
+      mma16x8x4(acc2, X[gid][k + 4], X[gid + 8][k + 4], X[nt * 8 + gid][k + 4]);
+    }
+  } else {
+    const int nt = 2 + ((warp - 4) >> 1), k0 = ((warp - 4) & 1) * (JCH / 2);
+#pragma unroll
+    for (int k8 = 0; k8 < JCH / 16; ++k8) {
+      const int k = k0 + k8 * 8 + tig;
+      mma16x8x4(acc, X[16 + gid][k], X[16 + gid + 8][k], X[nt * 8 + gid][k]);
+      mma16x8x4(acc2, X[16 + gid][k + 4], X[16 + gid + 8][k + 4], X[nt * 8 + gid][k + 4]);
+    }
   }
+}
+
+// the six computed tiles (acc + acc2 of gram_chunk_sym) -> every thread's acc[4] in the
+// 8-tile layout of gram_chunk (warp w: rows 16 (w >> 2).., columns 8 (w & 3)..), through
+// the two (still unused) Gram buffers: S[0] takes whole tiles, K half 0 and the transposed
+// upper-right block, S[1] K half 1; the halves are added in a fixed order
+__device__ __forceinline__ void gram_sym_finish(Small& sm, double (&acc)[4], const double (&acc2)[4]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  double v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = acc[i] + acc2[i];
+  {
+    const int mt = warp < 4 ? 0 : 1, nt = warp < 4 ? warp : 2 + ((warp - 4) >> 1);
+    double(*P)[SLD] = sm.S[warp < 4 ? 0 : ((warp - 4) & 1)];
+    const int r = mt * 16 + gid, c = nt * 8 + 2 * tig;
+    P[r][c] = v[0];
+    P[r][c + 1] = v[1];
+    P[r + 8][c] = v[2];
+    P[r + 8][c + 1] = v[3];
+    if (warp == 2 || warp == 3) {  // (0, 2), (0, 3) transposed -> (1, 0), (1, 1)
+      P[c][r] = v[0];
+      P[c + 1][r] = v[1];
+      P[c][r + 8] = v[2];
+      P[c + 1][r + 8] = v[3];
+    }
+  }
+  __syncthreads();
+  const int mt = warp >> 2, nt = warp & 3;
+  const int r = mt * 16 + gid, c = nt * 8 + 2 * tig;
+  const bool two = mt == 1 && nt >= 2;
+  acc[0] = sm.S[0][r][c] + (two ? sm.S[1][r][c] : 0.0);
+  acc[1] = sm.S[0][r][c + 1] + (two ? sm.S[1][r][c + 1] : 0.0);
+  acc[2] = sm.S[0][r + 8][c] + (two ? sm.S[1][r + 8][c] : 0.0);
+  acc[3] = sm.S[0][r + 8][c + 1] + (two ? sm.S[1][r + 8][c + 1] : 0.0);
+  __syncthreads();  // finish_gram rewrites S[0]
 }
 
 // rows [r0, r0 + 64) of the pair columns (ca.., cb..) of M <- X * J, stored straight from
@@ -789,11 +839,9 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
         const int kn = k + STREAM_STAGES - 1;
         if (g0 + kn < g1) load_chunk_async(X[kn % STREAM_STAGES], G, a.ldg, a.mg, (g0 + kn) * JCH, ca, cb);
         cp_commit();
-        gram_chunk(X[k % STREAM_STAGES], acc, acc2);
+        gram_chunk_sym(X[k % STREAM_STAGES], acc, acc2);
       }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i] += acc2[i];
-      __syncthreads();  // every warp is done with the stage buffers the rotation prefetch reuses
+      gram_sym_finish(sm, acc, acc2);  // (its barriers also release the stage buffers)
       const long long t1 = prof ? clock64() : 0;
       if (R > 1) {
         // publish the partial Gram, wait for the pair's other CTAs, fixed-order sum (two
