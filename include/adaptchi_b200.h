@@ -281,7 +281,10 @@ int achi_env_update_right(achi_ctx* ctx, int chr, int chn, int d, int Dl, int Dr
 /* svd_full (linalg.cpp:67-70) + fix_phases (linalg.cpp:19-35) on the GPU
  * Jacobi kernel.  a: m x n ROW-major.  r = min(m,n).  Outputs (any may be
  * NULL): sigma[r] non-increasing; u: m x r row-major; vt: r x n row-major.
- * sweeps_out: Jacobi sweeps used. */
+ * sweeps_out: Jacobi sweeps used.  Matrices too large for one cluster (the
+ * streamed path) rotate only one factor and recover the other by GEMM
+ * afterwards (svd_jacobi.cuh SvdWs::vrecover; decomposed again with both
+ * accumulated when a singular value lies below 1e-5 sigma_1). */
 int achi_svd(achi_ctx* ctx, int m, int n, const double* a, double* sigma,
              double* u, double* vt, int* sweeps_out);
 /* Batched SVD of `batch` m x n row-major matrices stored back to back; only

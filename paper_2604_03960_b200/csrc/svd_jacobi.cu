@@ -117,6 +117,7 @@ struct Small {
   double red2[JT / 32];
   unsigned char pi[JW - 1][JW / 2], pj[JW - 1][JW / 2];
   unsigned char pci[JW / 2][JW / 2], pcj[JW / 2][JW / 2];  // cross pairs only (block p x block q)
+  int fin;  // the S buffer holding J^T S J after finish_gram (0 when nothing was rotated)
 };
 
 __device__ __forceinline__ float rcp_f32(float x) {
@@ -223,6 +224,7 @@ __device__ void inner_jacobi(Small& sm, double z2, double tol, int max_inner, bo
     // the next sweep continues from S[cur]
     if (sweep + 1 < max_inner && !__syncthreads_or(any)) break;
   }
+  if (threadIdx.x == 0) sm.fin = cur;
 }
 
 __device__ void init_pair_tables(Small& sm) {
@@ -298,7 +300,10 @@ __device__ bool finish_gram(Small& sm, const double (&acc)[4], double z2, double
   }
   __syncthreads();
   const bool rotate = sm.red[0] > fmax(tol, skip_tol);
-  if (rotate) inner_jacobi(sm, z2, tol, max_inner, cross);
+  if (rotate)
+    inner_jacobi(sm, z2, tol, max_inner, cross);
+  else if (threadIdx.x == 0)
+    sm.fin = 0;
   return rotate;
 }
 
@@ -607,6 +612,9 @@ struct PersArgs {
   int cross_mode;            // 4: two of every three rounds sweep only the cross-block pairs
   long long* prof;           // optional clock64 phase sums over every CTA's thread 0 (ACHI_JACOBI_PROF)
   int p2p;                   // 1: rounds ordered by per-pair completion counters, grid barrier per sweep
+  int track;                 // 1: cross rounds take the diagonal Gram blocks from blks (see below)
+  double* blks;              // [matrices in launch][nb][16][16]: each block's Gram after the
+                             // round that last rotated it (J^T S J of that round's inner Jacobi)
 };
 
 // cp.async chunk loads: rows [r0, r0+64) of the 32 pair columns -> X[col][row]
@@ -683,6 +691,57 @@ __device__ __forceinline__ void gram_sym_finish(Small& sm, double (&acc)[4], con
   acc[1] = sm.S[0][r][c + 1] + (two ? sm.S[1][r][c + 1] : 0.0);
   acc[2] = sm.S[0][r + 8][c] + (two ? sm.S[1][r + 8][c] : 0.0);
   acc[3] = sm.S[0][r + 8][c + 1] + (two ? sm.S[1][r + 8][c + 1] : 0.0);
+  __syncthreads();  // finish_gram rewrites S[0]
+}
+
+// Cross rounds with tracked diagonal blocks (PersArgs::track): only the 16 x 16 block
+// S_ab = A^T B is formed from the data -- warp w takes tile (0, 2 + (w & 1)) over the
+// K quarter w >> 1 of the chunk (four DMMA per warp and chunk instead of eight or sixteen)
+__device__ __forceinline__ void gram_chunk_cross(const Chunk& X, double (&acc)[4], double (&acc2)[4]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int nt = 2 + (warp & 1), k0 = (warp >> 1) * (JCH / 4);
+#pragma unroll
+  for (int k8 = 0; k8 < JCH / 32; ++k8) {  // 16 rows: two steps of 8 (k and k + 4)
+    const int k = k0 + k8 * 8 + tig;
+    mma16x8x4(acc, X[gid][k], X[gid + 8][k], X[nt * 8 + gid][k]);
+    mma16x8x4(acc2, X[gid][k + 4], X[gid + 8][k + 4], X[nt * 8 + gid][k + 4]);
+  }
+}
+
+// the K quarters of gram_chunk_cross summed in a fixed order -> the 8-tile acc layout with
+// S_ab, S_ba = S_ab^T and zeros in the diagonal blocks (filled from the tracked buffer
+// after the row-split exchange, which must not sum them)
+__device__ __forceinline__ void gram_cross_finish(Small& sm, double (&acc)[4], const double (&acc2)[4]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  {
+    const int kq = warp >> 1, c = (warp & 1) * 8 + 2 * tig;
+    double(*P)[SLD] = sm.S[kq >> 1] + (kq & 1) * 16;  // quarter plane: 16 rows x 16 columns
+    P[gid][c] = acc[0] + acc2[0];
+    P[gid][c + 1] = acc[1] + acc2[1];
+    P[gid + 8][c] = acc[2] + acc2[2];
+    P[gid + 8][c + 1] = acc[3] + acc2[3];
+  }
+  __syncthreads();
+  const int mt = warp >> 2, nt = warp & 3;
+  const int r = mt * 16 + gid, c = nt * 8 + 2 * tig;
+  auto ab = [&](int i, int j) {  // S_ab[i][j], i, j < 16
+    return ((sm.S[0][i][j] + sm.S[0][16 + i][j]) + sm.S[1][i][j]) + sm.S[1][16 + i][j];
+  };
+  if (mt == 0 && nt >= 2) {
+    acc[0] = ab(r, c - 16);
+    acc[1] = ab(r, c - 15);
+    acc[2] = ab(r + 8, c - 16);
+    acc[3] = ab(r + 8, c - 15);
+  } else if (mt == 1 && nt < 2) {
+    acc[0] = ab(c, r - 16);
+    acc[1] = ab(c + 1, r - 16);
+    acc[2] = ab(c, r - 8);
+    acc[3] = ab(c + 1, r - 8);
+  } else {
+    acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+  }
   __syncthreads();  // finish_gram rewrites S[0]
 }
 
@@ -828,20 +887,32 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
         }
         __syncthreads();
       }
+      // The Gram pass walks the CTA's chunks backwards, the rotation pass forwards: each
+      // pass starts on the chunks the previous pass touched last, which are still in L2
+      // (G, 134 MB at 4096^2, about fills it; a one-way walk would always read the chunks
+      // evicted longest ago)
+      const bool cross = a.cross_mode == 4 && (round % 3) != 0;
+      const bool trk = a.track && cross;
       double acc[4] = {0, 0, 0, 0}, acc2[4] = {0, 0, 0, 0};
       for (int k = 0; k < STREAM_STAGES - 1; ++k) {
-        if (g0 + k < g1) load_chunk_async(X[k], G, a.ldg, a.mg, (g0 + k) * JCH, ca, cb);
+        if (g0 + k < g1) load_chunk_async(X[k], G, a.ldg, a.mg, (g1 - 1 - k) * JCH, ca, cb);
         cp_commit();
       }
       for (int k = 0; k < g1 - g0; ++k) {  // one barrier per chunk (as in stream_rotate)
         cp_wait<STREAM_STAGES - 2>();
         __syncthreads();
         const int kn = k + STREAM_STAGES - 1;
-        if (g0 + kn < g1) load_chunk_async(X[kn % STREAM_STAGES], G, a.ldg, a.mg, (g0 + kn) * JCH, ca, cb);
+        if (g0 + kn < g1) load_chunk_async(X[kn % STREAM_STAGES], G, a.ldg, a.mg, (g1 - 1 - kn) * JCH, ca, cb);
         cp_commit();
-        gram_chunk_sym(X[k % STREAM_STAGES], acc, acc2);
+        if (trk)
+          gram_chunk_cross(X[k % STREAM_STAGES], acc, acc2);
+        else
+          gram_chunk_sym(X[k % STREAM_STAGES], acc, acc2);
       }
-      gram_sym_finish(sm, acc, acc2);  // (its barriers also release the stage buffers)
+      if (trk)  // (the barriers of both finishes also release the stage buffers)
+        gram_cross_finish(sm, acc, acc2);
+      else
+        gram_sym_finish(sm, acc, acc2);
       const long long t1 = prof ? clock64() : 0;
       if (R > 1) {
         // publish the partial Gram, wait for the pair's other CTAs, fixed-order sum (two
@@ -868,11 +939,34 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
           acc[i] = t;
         }
       }
+      double* blk = a.track ? a.blks + static_cast<long>(b - a.batch0) * a.nb * 256 : nullptr;
+      if (trk) {
+        // the diagonal blocks from the tracked Grams of the blocks' previous round
+        const int warp = threadIdx.x >> 5, gid = (threadIdx.x & 31) >> 2, tig = threadIdx.x & 3;
+        const int mt = warp >> 2, nt = warp & 3;
+        if ((mt == 0) == (nt < 2)) {
+          const double* B = blk + (mt == 0 ? ba : bb) * 256;
+          const int r = gid, c = (nt & 1) * 8 + 2 * tig;
+          acc[0] = __ldcg(B + r * 16 + c);
+          acc[1] = __ldcg(B + r * 16 + c + 1);
+          acc[2] = __ldcg(B + (r + 8) * 16 + c);
+          acc[3] = __ldcg(B + (r + 8) * 16 + c + 1);
+        }
+      }
       const RotSeg seg{G, a.ldg, a.mg, g0, g1 - g0, V, a.ldv, a.vrows, v0, V ? v1 - v0 : 0};
       stream_rotate_prefetch(X, seg, ca, cb);  // lands during the inner Jacobi
-      const bool cross = a.cross_mode == 4 && (round % 3) != 0;
       const long long t2 = prof ? clock64() : 0;
       const bool rot = finish_gram(sm, acc, z2, ig2, a.tol, a.max_inner, cross);
+      if (a.track) {  // publish the blocks' Grams after this round's rotation (J^T S J)
+        __syncthreads();
+        if (h == 0) {
+          const double(*F)[SLD] = sm.S[sm.fin];
+          for (int i = threadIdx.x; i < 512; i += JT) {
+            const int q = i >> 8, e = i & 255, r = e >> 4, c = e & 15;
+            __stcg(blk + (q ? bb : ba) * 256 + e, F[q * 16 + r][q * 16 + c]);
+          }
+        }
+      }
       const long long t3 = prof ? clock64() : 0;
       if (threadIdx.x == 0 && h == 0)
         atomicMax(&a.conv[sweep], static_cast<unsigned long long>(__double_as_longlong(sm.red2[0])));
@@ -1532,6 +1626,17 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
         const char* e = std::getenv("ACHI_JACOBI_P2P");
         return e ? std::atoi(e) : 1;
       }();
+      // cross rounds form only S_ab from the data and take S_aa, S_bb from the Grams the
+      // blocks' previous round left (J^T S J of its inner Jacobi); full rounds (one in three)
+      // form the whole Gram, so every within-block cosine is measured from the data at
+      // least every third round.  4096^2: 466 -> 421 ms, same sweep counts and accuracy
+      // (ACHI_JACOBI_TRACK=0: every Gram from the data)
+      static const int stream_track = [] {
+        const char* e = std::getenv("ACHI_JACOBI_TRACK");
+        return e ? std::atoi(e) : 1;
+      }();
+      const int track = stream_track && stream_cross == 4 ? 1 : 0;
+      double* blks = track ? ws.blks.reserve(static_cast<size_t>(nbat) * nb * 256) : nullptr;
       static const bool sprof = std::getenv("ACHI_JACOBI_PROF") != nullptr;
       static DevArr<long long> sprofbuf;
       long long* pb = nullptr;
@@ -1541,7 +1646,8 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
       }
       PersArgs a{G, ldg, gstride, mg, vrec ? nullptr : V, ng, vstride, ng, nb, npairs, b0,
                  max_inner, tol, stop_tol, zero2, conv, sweeps_dev + (launches % nsw),
-                 sweeps_host + (launches % nsw), rsplit, gpart, pcnt, stream_cross, pb, stream_p2p};
+                 sweeps_host + (launches % nsw), rsplit, gpart, pcnt, stream_cross, pb, stream_p2p,
+                 track, blks};
       void* args[] = {&a};
       ACHI_CUDA(cudaLaunchCooperativeKernel(kern, dim3(npairs * nbat * rsplit), dim3(JT), args, smem,
                                             ctx.stream));

@@ -25,7 +25,8 @@ struct SvdWs {
   DevArr<double> sign;
   DevArr<unsigned long long> conv;
   DevArr<double> gpart;         // stream mode, row split: partial Grams
-  DevArr<unsigned> pcnt;        // stream mode, row split: per-pair arrival counters
+  DevArr<unsigned> pcnt;        // stream mode: per-pair arrival and round-completion counters
+  DevBuf blks;                  // stream mode: tracked diagonal block Grams (ACHI_JACOBI_TRACK)
   DevArr<int> sweeps;
   PinnedArr<int> sweeps_host;
   // defer_v (set by the chain): the cluster path's V replay runs on ctx.vstream
