@@ -914,6 +914,23 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
       else
         gram_sym_finish(sm, acc, acc2);
       const long long t1 = prof ? clock64() : 0;
+      double* blk = a.track ? a.blks + static_cast<long>(b - a.batch0) * a.nb * 256 : nullptr;
+      // the diagonal blocks from the tracked Grams of the blocks' previous round, read
+      // BEFORE the partial-Gram exchange: CTA h = 0 of this pair overwrites them with this
+      // round's J^T S J once the exchange completes, so a CTA reading after its own
+      // exchange could see the next round's Grams and rotate its rows with another J
+      const int dwarp = threadIdx.x >> 5, dmt = dwarp >> 2, dnt = dwarp & 3;
+      const bool dtile = trk && ((dmt == 0) == (dnt < 2));
+      double dg[4] = {0, 0, 0, 0};
+      if (dtile) {
+        const int gid = (threadIdx.x & 31) >> 2, tig = threadIdx.x & 3;
+        const double* B = blk + (dmt == 0 ? ba : bb) * 256;
+        const int r = gid, c = (dnt & 1) * 8 + 2 * tig;
+        dg[0] = __ldcg(B + r * 16 + c);
+        dg[1] = __ldcg(B + r * 16 + c + 1);
+        dg[2] = __ldcg(B + (r + 8) * 16 + c);
+        dg[3] = __ldcg(B + (r + 8) * 16 + c + 1);
+      }
       if (R > 1) {
         // publish the partial Gram, wait for the pair's other CTAs, fixed-order sum (two
         // slots by round parity: a CTA running one round ahead of its pair mates never
@@ -939,19 +956,9 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
           acc[i] = t;
         }
       }
-      double* blk = a.track ? a.blks + static_cast<long>(b - a.batch0) * a.nb * 256 : nullptr;
-      if (trk) {
-        // the diagonal blocks from the tracked Grams of the blocks' previous round
-        const int warp = threadIdx.x >> 5, gid = (threadIdx.x & 31) >> 2, tig = threadIdx.x & 3;
-        const int mt = warp >> 2, nt = warp & 3;
-        if ((mt == 0) == (nt < 2)) {
-          const double* B = blk + (mt == 0 ? ba : bb) * 256;
-          const int r = gid, c = (nt & 1) * 8 + 2 * tig;
-          acc[0] = __ldcg(B + r * 16 + c);
-          acc[1] = __ldcg(B + r * 16 + c + 1);
-          acc[2] = __ldcg(B + (r + 8) * 16 + c);
-          acc[3] = __ldcg(B + (r + 8) * 16 + c + 1);
-        }
+      if (dtile) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] = dg[i];
       }
       const RotSeg seg{G, a.ldg, a.mg, g0, g1 - g0, V, a.ldv, a.vrows, v0, V ? v1 - v0 : 0};
       stream_rotate_prefetch(X, seg, ca, cb);  // lands during the inner Jacobi

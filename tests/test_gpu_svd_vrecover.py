@@ -88,3 +88,39 @@ def test_strongly_graded_converges(ctx, oracle):
     stretch there; its sweep cap is 100)."""
     a = graded(800, 800, 1e-12, 13)
     check(ctx, oracle, a, resolved=1e-6)
+
+
+@pytest.mark.parametrize("shape,rank", [((2048, 2048), 900), ((4096, 2048), None)])
+def test_stream_rowsplit_deterministic(ctx, oracle, shape, rank):
+    """Row-split pairs (2048^2: four CTAs per block pair) with tracked diagonal Grams in the
+    cross rounds: every CTA of a pair must rotate its rows with the same J.  The tracked
+    blocks are read before the pair's partial-Gram exchange (svd_jacobi.cu, jacobi_stream
+    kernel), after which CTA 0 overwrites them; a late read would mix two rounds.  The
+    kernel's sums run in a fixed order, so repeated decompositions are bit-identical."""
+    a = graded(shape[0], shape[1], 1e-4, 21, rank)
+    u0, s0, vt0 = check(ctx, oracle, a, resolved=1e-6)
+    for _ in range(4):
+        u, s, vt, _ = ctx.svd_full(a)
+        assert np.array_equal(s, s0) and np.array_equal(u, u0) and np.array_equal(vt, vt0)
+
+
+def test_chain_chi1024_stream_svds(ctx):
+    """The bench's in-sweep H_eff chain (bench.py heff_insweep): N=100 Heisenberg, fixed
+    chi=1024 from the Neel state through sweep 5 -- 2048 x 2048 theta SVDs on the stream
+    path, many of them rank-deficient.  Energies stay variational and decrease."""
+    from paper_2604_03960_b200 import abi
+    from paper_2604_03960_b200.api import Chain
+    ctx.set_lanczos_graph(0)
+    ch = Chain(ctx, abi.model_spec(100, convention=abi.SPIN_HALF), abi.fixed_config(1024, max_sweeps=6))
+    try:
+        es = []
+        for s in range(6):
+            r = ch.sweep(s)
+            es.append(r["energy"] / 100)
+        assert int(r["chi_profile"].max()) == 1024
+    finally:
+        ch.close()
+        ctx.set_lanczos_graph(-1)
+    assert all(np.isfinite(es))
+    assert all(b <= a + 1e-12 for a, b in zip(es, es[1:]))
+    assert -0.4432 < es[-1] < -0.4412  # N=100 OBC ground state -0.44127739861..., Bethe limit -0.44315
