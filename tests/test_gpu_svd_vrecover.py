@@ -90,14 +90,14 @@ def test_strongly_graded_converges(ctx, oracle):
     check(ctx, oracle, a, resolved=1e-6)
 
 
-@pytest.mark.parametrize("shape,rank", [((2048, 2048), 900), ((4096, 2048), None)])
-def test_stream_rowsplit_deterministic(ctx, oracle, shape, rank):
+@pytest.mark.parametrize("shape,lo,rank", [((2048, 2048), 1e-4, 900), ((4096, 2048), 1e-1, None)])
+def test_stream_rowsplit_deterministic(ctx, oracle, shape, lo, rank):
     """Row-split pairs (2048^2: four CTAs per block pair) with tracked diagonal Grams in the
     cross rounds: every CTA of a pair must rotate its rows with the same J.  The tracked
     blocks are read before the pair's partial-Gram exchange (svd_jacobi.cu, jacobi_stream
     kernel), after which CTA 0 overwrites them; a late read would mix two rounds.  The
     kernel's sums run in a fixed order, so repeated decompositions are bit-identical."""
-    a = graded(shape[0], shape[1], 1e-4, 21, rank)
+    a = graded(shape[0], shape[1], lo, 21, rank)
     u0, s0, vt0 = check(ctx, oracle, a, resolved=1e-6)
     for _ in range(4):
         u, s, vt, _ = ctx.svd_full(a)
