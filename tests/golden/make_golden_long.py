@@ -16,6 +16,8 @@ on the box:
 * dmrg_c4_jz0p5.json, dmrg_c4_jz1p5.json   two C4 chains (configs[3]): N=100
                       spin-1/2 XXZ at Jz=0.5 (critical) and 1.5 (gapped), C3
                       controller settings, 10 sweeps (ensemble_run.py default).
+* dmrg_c5_adaptive.json  C5 adaptive arm (configs[4]) as bench.py runs it: N=200,
+                      PID chi_max=2048, eps 1e-10, to convergence (max 12 sweeps).
 
 Every visit row carries the decision inputs (floor rank, its margin
 |tail - eps*total|/(eps*total), significant count, sigma_kept/sigma_1,
@@ -24,7 +26,7 @@ a threshold within rounding.  The real-gauge oracle is used (identical to the
 complex128 restatement to 1e-12 with identical chi profiles,
 tests/test_oracle_golden.py::test_real_gauge_run_equals_complex_reference).
 
-    python tests/golden/make_golden_long.py [c3|crit5|c4] ...
+    python tests/golden/make_golden_long.py [svd|c3|crit5|c4|c5] ...
 """
 import json
 import os
@@ -105,7 +107,12 @@ def main(which):
                      abi.adaptive_config(1024, 1e-10, max_sweeps=10),
                      f"BASELINE.json configs[3] (C4) chain Jz={jz}: N=100 PID chi_max=1024 "
                      "eps 1e-10, 10 sweeps (ensemble_run.py defaults)")
+    if "c5" in which:
+        run_case("c5_adaptive", abi.model_spec(200, convention=abi.SPIN_HALF),
+                 abi.adaptive_config(2048, 1e-10, max_sweeps=12),
+                 "BASELINE.json configs[4] (C5) adaptive arm as bench.py runs it: N=200 spin-1/2 "
+                 "PID chi_max=2048 eps 1e-10, predictor linear beta=0.4, to eps_conv=1e-8 (max 12 sweeps)")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["svd", "c3", "crit5", "c4"])
+    main(sys.argv[1:] or ["svd", "c3", "crit5", "c4", "c5"])

@@ -6,6 +6,7 @@ tests/golden/make_golden_long.py from the pinned oracle; no oracle on the box).
   chi_max=128, eps 1e-10, <= 30 sweeps; E/N = -0.440241 as recorded by the
   reference (proj/test_output.txt:19).
 * Two C4 chains (Jz = 0.5 critical, Jz = 1.5 gapped).
+* The C5 adaptive arm bench.py times (N=200, PID chi_max=2048, to convergence).
 * sigma of the 1024^2, 2048^2 and 4096^2 random matrices bench.py times
   (4096^2 = the chi=2048 truncated SVD of the metric) against LAPACK dgesdd.
 
@@ -40,6 +41,8 @@ LONG_CASES = {
                          abi.adaptive_config(1024, 1e-10, max_sweeps=10)),
     "c4_jz1p5": lambda: (abi.model_spec(100, jz=1.5, convention=abi.SPIN_HALF),
                          abi.adaptive_config(1024, 1e-10, max_sweeps=10)),
+    "c5_adaptive": lambda: (abi.model_spec(200, convention=abi.SPIN_HALF),
+                            abi.adaptive_config(2048, 1e-10, max_sweeps=12)),
 }
 
 
