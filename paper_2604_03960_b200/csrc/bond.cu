@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(BS_THREADS) bond_select_kernel(
     const double* __restrict__ sigma, int r, achi_dmrg_config cfg, achi_bond_state* states, int bond,
     int sweep, int moving_right, achi_trace_row* trace, achi_visit_record* visit, BondOut* out,
     BondOut* out_host) {
+  pdl_wait();  // launched with launch_pdl (common.cuh)
   bond_select_body(sigma, r, cfg, states, bond, sweep, moving_right, trace, visit, out);
   if (out_host && threadIdx.x == 0) *out_host = *out;  // thread 0 wrote every field of *out
 }
@@ -282,6 +283,7 @@ struct AbsorbArgs {
 };
 
 __global__ void absorb_kernel(AbsorbArgs a) {
+  pdl_wait();  // launched with launch_pdl (common.cuh)
   const long n_b = static_cast<long>(a.chlp) * a.d * a.keptp;
   const long n_b1 = static_cast<long>(a.keptp) * a.d * a.chrp;
   const double inv_lam = 1.0 / a.bo->lam_norm;
@@ -332,9 +334,8 @@ void bond_select(Ctx& ctx, const double* sigma, int r, const achi_dmrg_config& c
     return 1;
   });
   if (smem > 200 * 1024) fail(ACHI_E_SIZE_GUARD, "bond_select: spectrum too long");
-  bond_select_kernel<<<1, BS_THREADS, smem, ctx.stream>>>(sigma, r, cfg, states, bond, sweep,
-                                                          moving_right, trace_slot, visit_slot, out,
-                                                          out_host);
+  ACHI_CUDA(launch_pdl(bond_select_kernel, 1, BS_THREADS, smem, ctx.stream, sigma, r, cfg, states, bond, sweep,
+                       moving_right, trace_slot, visit_slot, out, out_host));
   ACHI_LAUNCHED(ctx);
 }
 
@@ -374,7 +375,7 @@ void absorb(Ctx& ctx, const SvdResultDev& r, const double* sign, int kept, const
   a.site_b1 = site_b1;
   const long tot = static_cast<long>(a.chlp) * d * a.keptp + static_cast<long>(a.keptp) * d * a.chrp;
   const int blocks = static_cast<int>(std::min<long>(cdiv(tot, 256), 8L * ctx.num_sms));
-  absorb_kernel<<<blocks, 256, 0, ctx.stream>>>(a);
+  ACHI_CUDA(launch_pdl(absorb_kernel, blocks, 256, 0, ctx.stream, a));
   ACHI_LAUNCHED(ctx);
 }
 

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <map>
 #include <mutex>
@@ -41,6 +42,38 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
     ::achi::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
     ++(ctx).launches;                                                 \
   } while (0)
+
+// Programmatic dependent launch: a kernel launched with launch_pdl may have its CTAs
+// scheduled while the previous kernel of the stream drains (the kernel-boundary gap of
+// the small per-visit kernels overlaps), so such a kernel calls pdl_wait() before it
+// touches memory: griddepcontrol.wait returns once the previous grid has completed and
+// its writes are visible (a no-op in a kernel launched without the attribute).
+// ACHI_PDL=0: plain stream serialization.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ACHI_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&lc, kern, args...);
+}
 
 // Device memory comes from the device's stream-ordered pool (cudaMallocAsync /
 // cudaFreeAsync on the stream of the context being driven, see AllocStream),

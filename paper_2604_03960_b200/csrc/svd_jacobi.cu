@@ -1019,6 +1019,7 @@ __global__ void __launch_bounds__(JT, 2) jacobi_stream_kernel(PersArgs a) {
 
 // ---- setup / finalisation kernels ----
 __global__ void identity_kernel(double* V, long ld, int n, long bstride) {
+  pdl_wait();  // launched with launch_pdl (common.cuh)
   double* Vb = V + blockIdx.y * bstride;
   for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
        idx < static_cast<long>(n) * n; idx += static_cast<long>(gridDim.x) * blockDim.x) {
@@ -1034,6 +1035,7 @@ __global__ void identity_kernel(double* V, long ld, int n, long bstride) {
 __global__ void load_g_kernel(const double* __restrict__ theta, long tstride, int m, int n,
                               double* __restrict__ G, long gstride, long ldg, int mg, int ng,
                               int rows_side) {
+  pdl_wait();  // launched with launch_pdl (common.cuh)
   __shared__ double tile[32][33];
   const double* T = theta + blockIdx.z * tstride;
   double* Gb = G + blockIdx.z * gstride;
@@ -1063,6 +1065,7 @@ __global__ void load_g_kernel(const double* __restrict__ theta, long tstride, in
 // they are not rotated and do not enter the convergence measure.
 __global__ void zero_floor_kernel(const double* __restrict__ G, long gstride, long len, int mg,
                                   double frel, double* __restrict__ zero2) {
+  pdl_wait();  // launched with launch_pdl (common.cuh)
   __shared__ double sh[32];
   const double* g = G + blockIdx.x * gstride;
   double s = 0.0;
@@ -1084,6 +1087,7 @@ __global__ void zero_floor_kernel(const double* __restrict__ G, long gstride, lo
 __global__ void col_norm_kernel(const double* __restrict__ G, long gstride, long ldg, int ng,
                                 int ng_real, int pad_mod, int pad_lim, double* __restrict__ sig,
                                 long sstride) {
+  pdl_wait();  // launched with launch_pdl (common.cuh)
   const int warps = blockDim.x >> 5;
   const int c = blockIdx.x * warps + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (c >= ng) return;
@@ -1102,6 +1106,7 @@ __global__ void col_norm_kernel(const double* __restrict__ G, long gstride, long
 __global__ void __launch_bounds__(1024) sort_kernel(const double* __restrict__ sig, long sstride,
                                                     int ng, double* __restrict__ sorted,
                                                     int* __restrict__ perm) {
+  pdl_wait();  // launched with launch_pdl (common.cuh)
   extern __shared__ double keys[];
   const double* s = sig + blockIdx.x * sstride;
   for (int i = threadIdx.x; i < ng; i += blockDim.x) keys[i] = s[i];
@@ -1121,6 +1126,7 @@ __global__ void __launch_bounds__(1024) sort_kernel(const double* __restrict__ s
 // fix_phases (linalg.cpp:19-35): first largest-|u| entry of each kept U column positive
 __global__ void phase_kernel(const double* __restrict__ base, long ld, int len,
                              const int* __restrict__ perm, int kept, double* __restrict__ sign) {
+  pdl_wait();  // launched with launch_pdl (common.cuh)
   const int warps = blockDim.x >> 5;
   const int k = blockIdx.x * warps + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (k >= kept) return;
@@ -1426,8 +1432,8 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   }();
   {
     dim3 grid(cdiv(ng, 32), cdiv(ldg, 32), batch), blk(32, 8);
-    load_g_kernel<<<grid, blk, 0, ctx.stream>>>(theta, bstride, m, n, G, gstride, ldg, mg, ng,
-                                                rows ? 1 : 0);
+    ACHI_CUDA(launch_pdl(load_g_kernel, grid, blk, 0, ctx.stream, theta, bstride, m, n, G, gstride, ldg, mg, ng,
+                         rows ? 1 : 0));
     ACHI_LAUNCHED(ctx);
     if (vrec) {
       ACHI_CUDA(cudaMemcpyAsync(ws.G0.reserve(static_cast<size_t>(gstride)), G, sizeof(double) * gstride,
@@ -1438,7 +1444,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
                                   ctx.stream));
       } else {
         dim3 g2(static_cast<unsigned>(std::min<long>(cdiv(vstride, 256), 4L * ctx.num_sms)), batch);
-        identity_kernel<<<g2, 256, 0, ctx.stream>>>(V, ng, ng, vstride);
+        ACHI_CUDA(launch_pdl(identity_kernel, g2, 256, 0, ctx.stream, V, static_cast<long>(ng), ng, vstride));
         ACHI_LAUNCHED(ctx);
       }
     }
@@ -1446,7 +1452,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
       const char* e = std::getenv("ACHI_JACOBI_FLOOR");
       return e ? std::atof(e) : 0.0;
     }();
-    zero_floor_kernel<<<batch, 1024, 0, ctx.stream>>>(G, gstride, gstride, mg, frel, zero2);
+    ACHI_CUDA(launch_pdl(zero_floor_kernel, batch, 1024, 0, ctx.stream, G, gstride, gstride, mg, frel, zero2));
     ACHI_LAUNCHED(ctx);
     mark("load+floor");
     if (v_init) {
@@ -1460,7 +1466,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
       // cold start: QR preconditioning (svd_precond.cu), G <- G Q, V starts from Q
       double* vq = ws.Vq.reserve(static_cast<size_t>(vstride));
       dim3 g2(static_cast<unsigned>(std::min<long>(cdiv(vstride, 256), 4L * ctx.num_sms)), 1);
-      identity_kernel<<<g2, 256, 0, ctx.stream>>>(vq, ng, ng, vstride);
+      ACHI_CUDA(launch_pdl(identity_kernel, g2, 256, 0, ctx.stream, vq, static_cast<long>(ng), ng, vstride));
       ACHI_LAUNCHED(ctx);
       qr_precond(ctx, G, ldg, mg, ng, nr_real, pad_mod, pad_lim, vq);
       v_init = vq;
@@ -1689,8 +1695,8 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
   }
   {
     dim3 grid(cdiv(ng, 8), batch);
-    col_norm_kernel<<<grid, 256, 0, ctx.stream>>>(G, gstride, ldg, ng, ng_real, pad_mod, pad_lim,
-                                                  sig, ng);
+    ACHI_CUDA(launch_pdl(col_norm_kernel, grid, 256, 0, ctx.stream, G, gstride, ldg, ng, ng_real, pad_mod,
+                         pad_lim, sig, static_cast<long>(ng)));
     ACHI_LAUNCHED(ctx);
     const size_t sort_smem = sizeof(double) * ng;
     if (sort_smem > 48 * 1024) {  // n > 6144 (e.g. the realified complex 4096^2 literal)
@@ -1700,7 +1706,7 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
         return 1;
       });
     }
-    sort_kernel<<<batch, 1024, sort_smem, ctx.stream>>>(sig, ng, ng, sorted, perm);
+    ACHI_CUDA(launch_pdl(sort_kernel, batch, 1024, sort_smem, ctx.stream, sig, static_cast<long>(ng), ng, sorted, perm));
     ACHI_LAUNCHED(ctx);
   }
   // (the Jacobi kernels write their sweep counts into sweeps_host themselves)
@@ -1774,7 +1780,8 @@ void svd_phase_signs(Ctx& ctx, SvdWs& ws, const SvdResultDev& r, int kept) {
   // U columns: rows side -> V[:, perm k] (length m); cols side -> G[:, perm k] (length m)
   const double* base = rows ? r.V : r.G;
   const long ld = rows ? r.ng : r.mg;
-  phase_kernel<<<cdiv(kept, 8), 256, 0, ctx.stream>>>(base, ld, r.m, r.perm, kept, sign);
+  ACHI_CUDA(launch_pdl(phase_kernel, static_cast<unsigned>(cdiv(kept, 8)), 256, 0, ctx.stream, base, ld, r.m, r.perm, kept,
+                       sign));
   ACHI_LAUNCHED(ctx);
 }
 
