@@ -59,6 +59,12 @@ inline bool pdl_enabled() {
   }();
   return on;
 }
+// not while the stream is being captured (the Lanczos graphs keep plain kernel edges)
+inline bool pdl_allowed(cudaStream_t s) {
+  if (!pdl_enabled()) return false;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+}
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args... args) {
@@ -71,7 +77,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
-  lc.numAttrs = pdl_enabled() ? 1 : 0;
+  lc.numAttrs = pdl_allowed(s) ? 1 : 0;
   return cudaLaunchKernelEx(&lc, kern, args...);
 }
 

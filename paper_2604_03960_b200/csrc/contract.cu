@@ -129,6 +129,7 @@ constexpr int MIX_MAXIN = 32;
 __global__ void __launch_bounds__(MIX_THREADS) mpo_mix_kernel(const double* __restrict__ x,
                                                               double* __restrict__ y, DevMix W,
                                                               MixGeom g) {
+  pdl_wait();  // launched with launch_pdl / the PDL attribute (common.cuh)
   __shared__ double xs[MIX_MAXIN][MIX_THREADS];
   __shared__ double sval[512];
   __shared__ int scol[512];
@@ -166,7 +167,7 @@ void mix(Ctx& ctx, const double* x, double* y, const DevMix& W, const MixGeom& g
   const long total = g.outer * g.inner;
   if (total <= 0) return;
   const int blocks = static_cast<int>(std::min<long>(cdiv(total, MIX_THREADS), 16L * ctx.num_sms));
-  mpo_mix_kernel<<<blocks, MIX_THREADS, 0, ctx.stream>>>(x, y, W, g);
+  ACHI_CUDA(launch_pdl(mpo_mix_kernel, blocks, MIX_THREADS, 0, ctx.stream, x, y, W, g));
   ACHI_LAUNCHED(ctx);
 }
 

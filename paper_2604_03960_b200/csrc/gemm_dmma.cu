@@ -8,6 +8,7 @@ namespace gemm_detail {
 
 __global__ void splitk_reduce_kernel(const double* __restrict__ ws, long split_stride, int splits,
                                      double* __restrict__ C, long ldc, long ldw, int M, int N) {
+  pdl_wait();  // launched with launch_pdl / the PDL attribute (common.cuh)
   const long total = static_cast<long>(M) * N;
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
@@ -68,7 +69,7 @@ void launch(Ctx& ctx, int M, int N, int K, const Operand& A, const Operand& B, d
   splits = cdiv(kt_total, kt_per);
   dim3 grid(cdiv(N, BN), cdiv(M, BM), splits);
   if (splits == 1) {
-    kern<<<grid, G::THREADS, G::SMEM, ctx.stream>>>(ma, mb, C, ldc, 0, M, N, K, kt_per);
+    ACHI_CUDA(launch_pdl(kern, grid, G::THREADS, G::SMEM, ctx.stream, ma, mb, C, ldc, 0L, M, N, K, kt_per));
     ACHI_LAUNCHED(ctx);
     return;
   }
@@ -77,10 +78,12 @@ void launch(Ctx& ctx, int M, int N, int K, const Operand& A, const Operand& B, d
   // below): reserving that bound once keeps the buffer (and every captured
   // graph that uses it) stable
   double* ws = ctx.ws_split.reserve(std::max<size_t>(static_cast<size_t>(slab) * splits, 4096UL * 592));
-  kern<<<grid, G::THREADS, G::SMEM, ctx.stream>>>(ma, mb, ws, N, slab, M, N, K, kt_per);
+  ACHI_CUDA(launch_pdl(kern, grid, G::THREADS, G::SMEM, ctx.stream, ma, mb, ws, static_cast<long>(N), slab, M, N, K,
+                       kt_per));
   ACHI_LAUNCHED(ctx);
   const int blocks = std::min<long>(cdiv(slab, 256), 4L * ctx.num_sms);
-  splitk_reduce_kernel<<<blocks, 256, 0, ctx.stream>>>(ws, slab, splits, C, ldc, N, M, N);
+  ACHI_CUDA(launch_pdl(splitk_reduce_kernel, blocks, 256, 0, ctx.stream, ws, slab, splits, C, ldc,
+                       static_cast<long>(N), M, N));
   ACHI_LAUNCHED(ctx);
 }
 

@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WTM, WTN, STAGES, AM, BMJ>::THREAD
     dmma_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB, double* __restrict__ C, long ldc,
                      long split_stride, int M, int N, int K, int kt_per_split) {
+  pdl_wait();  // launched with launch_pdl / the PDL attribute (common.cuh)
   using G = Cfg<BM, BN, WTM, WTN, STAGES, AM, BMJ>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(

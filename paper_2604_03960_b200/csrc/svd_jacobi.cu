@@ -392,6 +392,7 @@ __device__ __forceinline__ void rotate_resident(const double* X, int cld, int ro
 }
 
 __global__ void __launch_bounds__(JT, 1) jacobi_cluster_kernel(ClArgs a) {
+  pdl_wait();  // launched with launch_pdl / the PDL attribute (common.cuh)
   extern __shared__ __align__(16) unsigned char dyn[];
   // per-sweep measure of this CTA, three slots: slot s%3 is written during
   // sweep s, read by every CTA after its last barrier, and reset at the start
@@ -1533,13 +1534,15 @@ SvdResultDev svd_device(Ctx& ctx, SvdWs& ws, const double* theta, int m, int n, 
     lc.blockDim = dim3(JT);
     lc.dynamicSmemBytes = smem;
     lc.stream = ctx.stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = npairs;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
-    lc.numAttrs = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    lc.numAttrs = pdl_allowed(lc.stream) ? 2 : 1;
     ACHI_CUDA(cudaLaunchKernelEx(&lc, jacobi_cluster_kernel, a));
     ACHI_LAUNCHED(ctx);
     mark("cluster");

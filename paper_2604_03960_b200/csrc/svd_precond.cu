@@ -379,6 +379,7 @@ __device__ void factor_panel(PqSmem& sm, const PqArgs& a, int p) {
 }
 
 __global__ void __launch_bounds__(PQ_T, 1) qr_precond_kernel(PqArgs a) {
+  pdl_wait();  // launched with launch_pdl / the PDL attribute (common.cuh)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PqSmem& sm = *reinterpret_cast<PqSmem*>(smem_raw);
   cg::cluster_group cl = cg::this_cluster();
@@ -514,13 +515,15 @@ void qr_precond(Ctx& ctx, double* G, long ldg, int mr, int ng, int nr, int pad_m
   lc.blockDim = dim3(PQ_T);
   lc.dynamicSmemBytes = sizeof(PqSmem);
   lc.stream = ctx.stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = ncta;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
-  lc.numAttrs = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  lc.numAttrs = pdl_allowed(lc.stream) ? 2 : 1;
   ACHI_CUDA(cudaLaunchKernelEx(&lc, qr_precond_kernel, a));
   ACHI_LAUNCHED(ctx);
   if (prof_on) {
